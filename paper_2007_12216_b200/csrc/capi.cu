@@ -1,0 +1,357 @@
+// C ABI entry points (include/rnsw.h): plan construction, argument checking,
+// buffer sizing and stage orchestration.  Every entry point validates its
+// arguments on the host before any device work, mirroring the reference's
+// "raise before doing work" behaviour (rw/layer.py:321-359), and reports
+// failures as codes that the Python layer maps onto the reference's
+// exception classes (paper_2007_12216_b200/errors.py).
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "../../include/rnsw.h"
+#include "kernels.h"
+
+struct rnsw_plan {
+  rnsw::PlanHost host;
+};
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(RNSW_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a < 0 ? -a : a;
+}
+
+int32_t sym(int64_t x, int32_t m) {
+  int64_t r = x % m;
+  if (r < 0) r += m;
+  if (r > (m - 1) / 2) r -= m;
+  return (int32_t)r;
+}
+
+int64_t round_up(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
+
+int padded_channels(int C) {
+  if (C <= 32) return 32;
+  if (C <= 64) return 64;
+  return (int)round_up(C, 128);
+}
+
+int check_plan(const rnsw_plan* plan) {
+  if (plan == nullptr) return fail(RNSW_ERR_INVALID, "null plan");
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(RNSW_ERR_CUDA, "cudaGetDevice failed");
+  if (dev != plan->host.device)
+    return fail(RNSW_ERR_UNSUPPORTED, "plan was created on device %d, current device is %d", plan->host.device, dev);
+  return RNSW_OK;
+}
+
+int make_geometry(const rnsw_plan* plan, int B, int H, int W, int C, int K, int pad, int layout, rnsw::Geometry* g) {
+  const PlanDevice& d = plan->host.dev;
+  if (B < 1 || H < 1 || W < 1 || C < 1 || K < 1 || pad < 0)
+    return fail(RNSW_ERR_SHAPE, "bad layer geometry B=%d H=%d W=%d C=%d K=%d pad=%d", B, H, W, C, K, pad);
+  if (layout != RNSW_LAYOUT_NHWC && layout != RNSW_LAYOUT_NCHW) return fail(RNSW_ERR_INVALID, "bad layout %d", layout);
+  g->B = B;
+  g->H = H;
+  g->W = W;
+  g->C = C;
+  g->K = K;
+  g->pad = pad;
+  g->layout = layout;
+  g->Ho = H + 2 * pad - d.r + 1;
+  g->Wo = W + 2 * pad - d.r + 1;
+  if (g->Ho < 1 || g->Wo < 1) return fail(RNSW_ERR_SHAPE, "padded input smaller than the filter");
+  g->th = (g->Ho + d.m_out - 1) / d.m_out;
+  g->tw = (g->Wo + d.m_out - 1) / d.m_out;
+  g->P = (int64_t)B * g->th * g->tw;
+  // s32 accumulators: |sum| <= C * 128 * 128 must stay below 2^31.
+  if ((int64_t)C * 128 * 128 > 2147483647LL)
+    return fail(RNSW_ERR_OVERFLOW, "C=%d channels can overflow the int32 tensor-core accumulator", C);
+  if (g->P > 2147483647LL) return fail(RNSW_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)g->P);
+  g->Cp = padded_channels(C);
+  g->Kp = (int)round_up(K, 16);
+  g->bc = g->Cp < 128 ? g->Cp : 128;
+  return RNSW_OK;
+}
+
+size_t v_bytes(const PlanDevice& d, int64_t P, int Cp) { return (size_t)d.n_planes * d.n * d.n * P * Cp; }
+size_t m_bytes(const PlanDevice& d, int64_t P, int Kp) {
+  return (size_t)P * d.n_res * d.n * d.n * Kp * sizeof(int16_t);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rnsw_error_string(int code) {
+  switch (code) {
+    case RNSW_OK: return "ok";
+    case RNSW_ERR_INVALID: return "invalid argument";
+    case RNSW_ERR_SHAPE: return "shape mismatch";
+    case RNSW_ERR_STRIDE: return "unsupported stride";
+    case RNSW_ERR_RANGE: return "dynamic range exceeded";
+    case RNSW_ERR_NOT_COPRIME: return "moduli not coprime";
+    case RNSW_ERR_OVERFLOW: return "accumulator overflow risk";
+    case RNSW_ERR_SYSTEM: return "residue system mismatch";
+    case RNSW_ERR_CUDA: return "CUDA error";
+    case RNSW_ERR_WORKSPACE: return "buffer too small";
+    case RNSW_ERR_UNSUPPORTED: return "unsupported on the device path";
+    default: return "unknown error";
+  }
+}
+
+const char* rnsw_last_error(void) { return g_last_error; }
+
+int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_t* moduli, const int16_t* at,
+                     const int16_t* g, const int16_t* bt, const int32_t* mrc_inv) {
+  if (out == nullptr || moduli == nullptr || at == nullptr || g == nullptr || bt == nullptr || mrc_inv == nullptr)
+    return fail(RNSW_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (tile_m < 1 || r < 1) return fail(RNSW_ERR_INVALID, "need tile_m >= 1 and r >= 1");
+  const int n = tile_m + r - 1;
+  if (n < 2) return fail(RNSW_ERR_INVALID, "tile_m + r - 1 must be at least 2");
+  if (n > RNSW_MAX_N || r > RNSW_MAX_R)
+    return fail(RNSW_ERR_UNSUPPORTED, "F(%d,%d): tile side %d exceeds the device limit %d", tile_m, r, n, RNSW_MAX_N);
+  if (n_res < 1 || n_res > RNSW_MAX_RES)
+    return fail(RNSW_ERR_UNSUPPORTED, "%d moduli: the device path takes 1..%d", n_res, RNSW_MAX_RES);
+  for (int i = 0; i < n_res; ++i) {
+    const int m = moduli[i];
+    if (m < 3 || m % 2 == 0 || m > 32767) return fail(RNSW_ERR_INVALID, "modulus must be odd and in [3, 32767], got %d", m);
+    for (int j = 0; j < i; ++j)
+      if (gcd64(m, moduli[j]) != 1)
+        return fail(RNSW_ERR_NOT_COPRIME, "moduli %d and %d share factor %lld", moduli[j], m, (long long)gcd64(m, moduli[j]));
+  }
+  rnsw_plan* plan = new (std::nothrow) rnsw_plan();
+  if (plan == nullptr) return fail(RNSW_ERR_INVALID, "out of host memory");
+  PlanDevice& d = plan->host.dev;
+  memset(&d, 0, sizeof(d));
+  d.m_out = tile_m;
+  d.r = r;
+  d.n = n;
+  d.n_res = n_res;
+  d.dynamic_range = 1;
+  int plane = 0;
+  for (int i = 0; i < n_res; ++i) {
+    ResidueTables& t = d.res[i];
+    const int m = moduli[i];
+    const int half = (m - 1) / 2;
+    t.modulus = m;
+    t.planes = m < 256 ? 1 : 2;
+    t.plane_base = plane;
+    plane += t.planes;
+    t.inv_m = 1.0f / (float)m;
+    t.r_256 = sym(256, m);
+    t.r_65536 = sym(65536, m);
+    auto load = [&](const int16_t* src, int rows, int cols, int stride, int32_t* dst) -> bool {
+      for (int a = 0; a < rows; ++a)
+        for (int b = 0; b < cols; ++b) {
+          const int v = src[(size_t)i * rows * cols + a * cols + b];
+          if (v < -half || v > half) return false;
+          dst[a * stride + b] = v;
+        }
+      return true;
+    };
+    if (!load(at, tile_m, n, RNSW_MAX_N, t.at) || !load(g, n, r, RNSW_MAX_R, t.g) || !load(bt, n, n, RNSW_MAX_N, t.bt)) {
+      delete plan;
+      return fail(RNSW_ERR_INVALID, "transform entries for modulus %d are not symmetric residues", m);
+    }
+    d.dynamic_range *= m;
+  }
+  d.n_planes = plane;
+  d.signed_bound = (d.dynamic_range - 1) / 2;
+  for (int j = 0; j < n_res; ++j)
+    for (int i = 0; i < j; ++i) {
+      const int64_t inv = mrc_inv[j * n_res + i];
+      if (((int64_t)moduli[i] * inv % moduli[j] + moduli[j]) % moduli[j] != 1) {
+        delete plan;
+        return fail(RNSW_ERR_SYSTEM, "mrc_inv[%d][%d]=%lld is not %d^-1 mod %d", j, i, (long long)inv, moduli[i],
+                    moduli[j]);
+      }
+      d.mrc_inv[j][i] = inv;
+    }
+  cudaError_t e = cudaGetDevice(&plan->host.device);
+  if (e == cudaSuccess) e = cudaMalloc(&plan->host.d_plan, sizeof(PlanDevice));
+  if (e == cudaSuccess) e = cudaMemcpy(plan->host.d_plan, &d, sizeof(d), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (plan->host.d_plan) cudaFree(plan->host.d_plan);
+    delete plan;
+    return cuda_fail(e, "rnsw_plan_create");
+  }
+  *out = plan;
+  return RNSW_OK;
+}
+
+void rnsw_plan_destroy(rnsw_plan* plan) {
+  if (plan == nullptr) return;
+  if (plan->host.d_plan) cudaFree(plan->host.d_plan);
+  delete plan;
+}
+
+int rnsw_plan_info(const rnsw_plan* plan, int* n, int* n_planes) {
+  if (plan == nullptr) return fail(RNSW_ERR_INVALID, "null plan");
+  if (n) *n = plan->host.dev.n;
+  if (n_planes) *n_planes = plan->host.dev.n_planes;
+  return RNSW_OK;
+}
+
+size_t rnsw_filter_bytes(const rnsw_plan* plan, int C, int K) {
+  if (plan == nullptr || C < 1 || K < 1) return 0;
+  const PlanDevice& d = plan->host.dev;
+  return (size_t)d.n_planes * d.n * d.n * K * padded_channels(C);
+}
+
+size_t rnsw_v_bytes(const rnsw_plan* plan, int64_t P, int C) {
+  if (plan == nullptr || P < 1 || C < 1) return 0;
+  return v_bytes(plan->host.dev, P, padded_channels(C));
+}
+
+size_t rnsw_m_bytes(const rnsw_plan* plan, int64_t P, int K) {
+  if (plan == nullptr || P < 1 || K < 1) return 0;
+  return m_bytes(plan->host.dev, P, (int)round_up(K, 16));
+}
+
+size_t rnsw_workspace_bytes(const rnsw_plan* plan, int B, int H, int W, int C, int K, int pad) {
+  if (plan == nullptr) return 0;
+  rnsw::Geometry g;
+  if (make_geometry(plan, B, H, W, C, K, pad, RNSW_LAYOUT_NHWC, &g) != RNSW_OK) return 0;
+  return round_up(v_bytes(plan->host.dev, g.P, g.Cp), 256) + m_bytes(plan->host.dev, g.P, g.Kp);
+}
+
+int rnsw_filter_transform(const rnsw_plan* plan, const int8_t* w, int C, int K, int layout, void* U, size_t U_bytes,
+                          void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (w == nullptr || U == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (C < 1 || K < 1) return fail(RNSW_ERR_SHAPE, "bad filter shape C=%d K=%d", C, K);
+  if (layout != RNSW_LAYOUT_NHWC && layout != RNSW_LAYOUT_NCHW) return fail(RNSW_ERR_INVALID, "bad layout %d", layout);
+  if (U_bytes < rnsw_filter_bytes(plan, C, K)) return fail(RNSW_ERR_WORKSPACE, "filter bank buffer too small");
+  cudaError_t e = rnsw::launch_filter_transform(plan->host, w, C, K, padded_channels(C), layout,
+                                                static_cast<int8_t*>(U), (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "filter_transform");
+}
+
+int rnsw_filter_import(const rnsw_plan* plan, int res, const int16_t* u_nnck, int C, int K, void* U, size_t U_bytes,
+                       void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (u_nnck == nullptr || U == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (res < 0 || res >= plan->host.dev.n_res) return fail(RNSW_ERR_SYSTEM, "residue index %d out of range", res);
+  if (U_bytes < rnsw_filter_bytes(plan, C, K)) return fail(RNSW_ERR_WORKSPACE, "filter bank buffer too small");
+  cudaError_t e = rnsw::launch_filter_import(plan->host, res, u_nnck, C, K, padded_channels(C),
+                                             static_cast<int8_t*>(U), (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "filter_import");
+}
+
+int rnsw_input_transform(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int pad, int layout,
+                         void* V, size_t V_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (x == nullptr || V == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, C, 1, pad, layout, &g)) return rc;
+  if (V_bytes < v_bytes(plan->host.dev, g.P, g.Cp)) return fail(RNSW_ERR_WORKSPACE, "V buffer too small");
+  cudaError_t e = rnsw::launch_input_transform(plan->host, g, x, static_cast<int8_t*>(V), (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "input_transform");
+}
+
+int rnsw_winograd_gemm(const rnsw_plan* plan, const void* V, const void* U, int64_t P, int C, int K, void* Mw,
+                       size_t Mw_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (V == nullptr || U == nullptr || Mw == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (P < 1 || C < 1 || K < 1) return fail(RNSW_ERR_SHAPE, "bad GEMM shape P=%lld C=%d K=%d", (long long)P, C, K);
+  if ((int64_t)C * 128 * 128 > 2147483647LL) return fail(RNSW_ERR_OVERFLOW, "C=%d can overflow int32", C);
+  const int Cp = padded_channels(C), Kp = (int)round_up(K, 16);
+  if (Mw_bytes < m_bytes(plan->host.dev, P, Kp)) return fail(RNSW_ERR_WORKSPACE, "Mw buffer too small");
+  cudaError_t e = rnsw::launch_winograd_gemm(plan->host, static_cast<const int8_t*>(V), static_cast<const int8_t*>(U),
+                                             P, Cp, K, Kp, Cp < 128 ? Cp : 128, static_cast<int16_t*>(Mw),
+                                             (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "winograd_gemm");
+}
+
+int rnsw_output_transform(const rnsw_plan* plan, const void* Mw, int B, int H, int W, int K, int pad, int layout,
+                          int32_t* y, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (Mw == nullptr || y == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, 1, K, pad, layout, &g)) return rc;
+  cudaError_t e = rnsw::launch_output_transform(plan->host, g, static_cast<const int16_t*>(Mw), y, nullptr,
+                                                (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform");
+}
+
+int rnsw_output_residues(const rnsw_plan* plan, const void* Mw, int64_t P, int K, int16_t* y_res, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (Mw == nullptr || y_res == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (P < 1 || K < 1) return fail(RNSW_ERR_SHAPE, "bad shape");
+  const PlanDevice& d = plan->host.dev;
+  rnsw::Geometry g{};
+  g.B = 1;
+  g.K = K;
+  g.Kp = (int)round_up(K, 16);
+  g.P = P;
+  g.th = 1;
+  g.tw = (int)P;  // one row of tiles: only p matters for the residue view
+  g.Ho = d.m_out;
+  g.Wo = (int)(P * d.m_out);
+  cudaError_t e = rnsw::launch_output_transform(plan->host, g, static_cast<const int16_t*>(Mw), nullptr, y_res,
+                                                (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_residues");
+}
+
+int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad, int layout,
+                      const void* U, int32_t* y, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (x == nullptr || U == nullptr || y == nullptr || workspace == nullptr)
+    return fail(RNSW_ERR_INVALID, "null buffer");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, C, K, pad, layout, &g)) return rc;
+  const PlanDevice& d = plan->host.dev;
+  const size_t vb = round_up(v_bytes(d, g.P, g.Cp), 256);
+  const size_t mb = m_bytes(d, g.P, g.Kp);
+  if (workspace_bytes < vb + mb) return fail(RNSW_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, vb + mb);
+  int8_t* V = static_cast<int8_t*>(workspace);
+  int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = rnsw::launch_input_transform(plan->host, g, x, V, s);
+  if (e != cudaSuccess) return cuda_fail(e, "input_transform");
+  e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, K, g.Kp, g.bc, Mw, s);
+  if (e != cudaSuccess) return cuda_fail(e, "winograd_gemm");
+  e = rnsw::launch_output_transform(plan->host, g, Mw, y, nullptr, s);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform");
+}
+
+int rnsw_mrc_reconstruct(const rnsw_plan* plan, const int16_t* residues, int64_t count, int64_t* out, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (residues == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (count < 0) return fail(RNSW_ERR_SHAPE, "negative count");
+  if (count == 0) return RNSW_OK;
+  cudaError_t e = rnsw::launch_mrc(plan->host, residues, count, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "mrc_reconstruct");
+}
+
+int rnsw_requant_pool(const int32_t* y, int B, int H, int W, int C, int shift, int pool, int8_t* out, void* stream) {
+  if (y == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (B < 1 || H < 1 || W < 1 || C < 1 || shift < 0 || shift > 31) return fail(RNSW_ERR_SHAPE, "bad requant shape");
+  if (pool && (H < 2 || W < 2)) return fail(RNSW_ERR_SHAPE, "pooling needs H, W >= 2");
+  cudaError_t e = rnsw::launch_requant_pool(y, B, H, W, C, shift, pool, out, (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "requant_pool");
+}
+
+}  // extern "C"

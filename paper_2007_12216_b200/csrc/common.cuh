@@ -1,0 +1,178 @@
+// Shared device helpers for the RNS-Winograd sm_100a kernels:
+//  * exact symmetric modular reduction (no integer division),
+//  * limb split of 16-bit residues into two s8 planes,
+//  * thin inline-PTX wrappers for mbarrier / TMA / tcgen05.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "plan.h"
+
+#define RNSW_DEV __device__ __forceinline__
+
+// ---------------------------------------------------------------------------
+// Modular arithmetic.  Residues are kept in the symmetric range
+// [-(m-1)/2, (m-1)/2] of an odd modulus m (rw/residue.py:25-33); every stage
+// of the reference reduces into that range after each product
+// (rw/kernel.py:21-30, rw/gemm.py:91-97).
+
+// Exact symmetric reduction of any int32 x.  Two float quotient estimates:
+// the first brings |x| below ~2^9 + m, the second is then exact because x/m
+// can never sit on a .5 tie for odd m.
+RNSW_DEV int32_t sym_mod(int32_t x, int32_t m, float inv_m) {
+  int32_t q = __float2int_rn(__int2float_rn(x) * inv_m);
+  int32_t r = x - q * m;
+  q = __float2int_rn(__int2float_rn(r) * inv_m);
+  r -= q * m;
+  return r;
+}
+
+// Symmetric reduction for |x| < 2^22 using only FMA/ALU-pipe float ops.
+// x + 1.5*2^23 is exact in fp32 for |x| < 2^22, rint via the same magic.
+// The quotient estimate can be off by one near a half-way point, so a
+// final compare/select folds r back into [-(m-1)/2, (m-1)/2].
+RNSW_DEV int32_t sym_mod_small(int32_t x, float m, float inv_m) {
+  const float magic = 12582912.0f;  // 1.5 * 2^23
+  float f = __int_as_float(x + 0x4B400000) - magic;
+  float q = __fadd_rn(__fmul_rn(f, inv_m), magic) - magic;
+  float r = __fmaf_rn(-q, m, f);
+  const float half = 0.5f * m;
+  r = r > half ? r - m : r;
+  r = r < -half ? r + m : r;
+  return __float_as_int(r + magic) - 0x4B400000;
+}
+
+// 64-bit exact symmetric reduction (used for the mixed-radix digits).
+RNSW_DEV int64_t sym_mod64(int64_t x, int64_t m) {
+  int64_t r = x % m;
+  if (r > (m - 1) / 2) r -= m;
+  if (r < -(m - 1) / 2) r += m;
+  return r;
+}
+
+// Balanced two-limb split of a residue v with |v| <= 16383:
+// v = 256*hi + lo, lo = sign-extended low byte in [-128,127], hi in [-64,64].
+RNSW_DEV void split_limbs(int32_t v, int8_t& lo, int8_t& hi) {
+  lo = (int8_t)(v & 0xFF);
+  hi = (int8_t)((v - (int32_t)lo) >> 8);
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (sm_100a).
+
+RNSW_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+RNSW_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+RNSW_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+RNSW_DEV void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+RNSW_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+RNSW_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+RNSW_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t"
+      "}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+RNSW_DEV void tma_prefetch_desc(const void* desc) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
+}
+
+RNSW_DEV void tma_load_3d(void* dst, const void* desc, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+RNSW_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+RNSW_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <uint32_t kCols>
+RNSW_DEV void tmem_alloc(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+
+template <uint32_t kCols>
+RNSW_DEV void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+
+// D[tmem] (+)= A[smem] * B[smem], s8 x s8 -> s32, one elected thread.
+RNSW_DEV void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// Arrive on an mbarrier once all previously issued tcgen05.mma complete.
+RNSW_DEV void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns per thread.
+RNSW_DEV void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+RNSW_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor for a K-major operand tile whose rows are
+// `row_bytes` (32/64/128) wide and swizzled by the matching TMA mode.  Rows
+// are grouped in 8-row core matrices (SBO = 8 * row_bytes apart).
+RNSW_DEV uint64_t umma_desc_kmajor(uint32_t smem_addr, uint32_t row_bytes) {
+  uint64_t layout = row_bytes == 128 ? 2ull : (row_bytes == 64 ? 4ull : 6ull);
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(((8 * row_bytes) >> 4) & 0x3FFF) << 32;  // SBO
+  d |= (uint64_t)1 << 46;                                  // descriptor version (sm_100)
+  d |= layout << 61;
+  return d;
+}
+
+// Instruction descriptor: s8 x s8 -> s32, both K-major, M x N tile.
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n) {
+  return (2u << 4)             // D format: S32
+         | (1u << 7)           // A: signed 8-bit
+         | (1u << 10)          // B: signed 8-bit
+         | ((n >> 3) << 17)    // N / 8
+         | ((m >> 4) << 24);   // M / 16
+}

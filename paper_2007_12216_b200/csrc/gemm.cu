@@ -1,0 +1,360 @@
+// K3: the Winograd-domain contraction on the 5th-generation tensor cores.
+//
+// For every residue r and transform position pos the reference computes
+//     acc[pos] = (V[pos] (P x C)  @  U[pos] (C x K))  mod m_r
+// with int32 accumulation reduced every accumulation_chunk(m) channels
+// (rw/layer.py:251-263, 285-291; rw/gemm.py:43-97).  Here one persistent,
+// warp-specialised kernel runs all (residue, position, P-block, K-block)
+// tiles:
+//   warp 0      TMA producer: V and U limb planes -> 128B/64B/32B-swizzled smem
+//   warp 1      MMA issuer:   tcgen05.mma.cta_group::1.kind::i8, s32 in TMEM
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue:     tcgen05.ld -> limb recombination -> mod m -> int16
+// TMEM holds two accumulator sets so the epilogue of tile i overlaps the
+// MMAs of tile i+1.
+//
+// 16-bit moduli: a residue v (|v| <= 16383) is stored as two s8 planes
+// v = 256*hi + lo.  The product of two residues is
+//     hi_a*hi_b * 2^16 + (hi_a*lo_b + lo_a*hi_b) * 2^8 + lo_a*lo_b
+// so each chunk issues 4 MMAs into 3 accumulators (the two cross products
+// share one), recombined mod m in the epilogue.  |acc| <= C * 128^2 < 2^31
+// for C <= 131071 (checked on the host).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rnsw {
+
+namespace {
+
+constexpr int kBlockM = 128;  // tiles (P) per MMA tile: TMEM lanes
+constexpr int kThreads = 256;
+
+struct GemmArgs {
+  int64_t P;
+  int K, Kp, Cp, npos, n_res;
+  int num_pb, num_kb, nkc;
+  int64_t total_tiles;
+  int planes[RNSW_MAX_RES];
+  int plane_base[RNSW_MAX_RES];
+  int modulus[RNSW_MAX_RES];
+  float inv_m[RNSW_MAX_RES];
+  int r256[RNSW_MAX_RES];
+  int r65536[RNSW_MAX_RES];
+  int16_t* Mw;
+};
+
+template <int BN, int MAXPL>
+struct GemmTraits {
+  static constexpr int kAccCols = (MAXPL == 2 ? 3 : 1) * BN;  // TMEM columns per accumulator set
+  static constexpr int kTmemCols = (2 * kAccCols <= 32) ? 32
+                                   : (2 * kAccCols <= 64) ? 64
+                                   : (2 * kAccCols <= 128) ? 128
+                                   : (2 * kAccCols <= 256) ? 256 : 512;
+  static_assert(2 * kAccCols <= 512, "accumulators exceed TMEM");
+};
+
+template <int BC>
+constexpr int stage_bytes(int bn, int maxpl) {
+  return maxpl * (kBlockM + bn) * BC;
+}
+
+template <int BN, int BC, int MAXPL>
+struct GemmConfig {
+  static constexpr int kStageBytes = stage_bytes<BC>(BN, MAXPL);
+  static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kAPlaneBytes = kBlockM * BC;
+  static constexpr int kBPlaneBytes = BN * BC;
+  static constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256 /*barriers*/;
+};
+
+template <int BN, int BC, int MAXPL>
+__global__ void __launch_bounds__(kThreads, 1)
+    winograd_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
+                         GemmArgs args) {
+  using Cfg = GemmConfig<BN, BC, MAXPL>;
+  using Tr = GemmTraits<BN, MAXPL>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmU);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<Tr::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto stage_a = [&](int s, int pl) { return smem + s * Cfg::kStageBytes + pl * Cfg::kAPlaneBytes; };
+  auto stage_b = [&](int s, int pl) {
+    return smem + s * Cfg::kStageBytes + MAXPL * Cfg::kAPlaneBytes + pl * Cfg::kBPlaneBytes;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+        int64_t rest = t;
+        const int kb = (int)(rest % args.num_kb);
+        rest /= args.num_kb;
+        const int pb = (int)(rest % args.num_pb);
+        rest /= args.num_pb;
+        const int pos = (int)(rest % args.npos);
+        const int res = (int)(rest / args.npos);
+        const int pl = args.planes[res];
+        const uint32_t bytes = (uint32_t)(pl * (Cfg::kAPlaneBytes + Cfg::kBPlaneBytes));
+        for (int kc = 0; kc < args.nkc; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          for (int a = 0; a < pl; ++a) {
+            const int slab = (args.plane_base[res] + a) * args.npos + pos;
+            tma_load_3d(stage_a(stage, a), &tmV, &full[stage], kc * BC, pb * kBlockM, slab);
+            tma_load_3d(stage_b(stage, a), &tmU, &full[stage], kc * BC, kb * BN, slab);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = idesc_i8(kBlockM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+        const int res = (int)(t / ((int64_t)args.num_kb * args.num_pb * args.npos));
+        const int pl = args.planes[res];
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d0 = tmem_base + as * Tr::kAccCols;
+        for (int kc = 0; kc < args.nkc; ++kc) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(stage_a(stage, 0));
+          const uint32_t b0 = smem_u32(stage_b(stage, 0));
+#pragma unroll
+          for (int k = 0; k < BC / 32; ++k) {
+            const uint32_t acc = (kc | k) != 0;
+            const uint64_t da_lo = umma_desc_kmajor(a0 + 32 * k, BC);
+            const uint64_t db_lo = umma_desc_kmajor(b0 + 32 * k, BC);
+            if (MAXPL == 1 || pl == 1) {
+              mma_i8(d0, da_lo, db_lo, idesc, acc);
+            } else {
+              const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
+              const uint64_t db_hi = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);
+              mma_i8(d0, da_hi, db_hi, idesc, acc);
+              mma_i8(d0 + BN, da_hi, db_lo, idesc, acc);
+              mma_i8(d0 + BN, da_lo, db_hi, idesc, 1u);
+              mma_i8(d0 + 2 * BN, da_lo, db_lo, idesc, acc);
+            }
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[as]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+      int64_t rest = t;
+      const int kb = (int)(rest % args.num_kb);
+      rest /= args.num_kb;
+      const int pb = (int)(rest % args.num_pb);
+      rest /= args.num_pb;
+      const int pos = (int)(rest % args.npos);
+      const int res = (int)(rest / args.npos);
+      const int pl = args.planes[res];
+      const int32_t m = args.modulus[res];
+      const float inv = args.inv_m[res];
+      const int32_t r8 = args.r256[res], r16 = args.r65536[res];
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const int64_t p = (int64_t)pb * kBlockM + q * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Tr::kAccCols;
+      int16_t* out_row = args.Mw + ((p * args.n_res + res) * args.npos + pos) * (int64_t)args.Kp;
+#pragma unroll 1
+      for (int j = 0; j < BN / 16; ++j) {
+        int32_t v0[16];
+        tmem_ld16(taddr + j * 16, v0);
+        int32_t v1[16], v2[16];
+        if (MAXPL == 2 && pl == 2) {
+          tmem_ld16(taddr + BN + j * 16, v1);
+          tmem_ld16(taddr + 2 * BN + j * 16, v2);
+        }
+        tmem_ld_wait();
+        int16_t outv[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          int32_t r;
+          if (MAXPL == 2 && pl == 2) {
+            const int32_t hh = sym_mod(v0[e], m, inv);
+            const int32_t cr = sym_mod(v1[e], m, inv);
+            const int32_t ll = sym_mod(v2[e], m, inv);
+            r = sym_mod(hh * r16 + cr * r8 + ll, m, inv);
+          } else {
+            r = sym_mod(v0[e], m, inv);
+          }
+          outv[e] = (int16_t)r;
+        }
+        const int col = kb * BN + j * 16;
+        if (p < args.P && col < args.Kp) {
+          int4* dst = reinterpret_cast<int4*>(out_row + col);
+          dst[0] = *reinterpret_cast<const int4*>(&outv[0]);
+          dst[1] = *reinterpret_cast<const int4*>(&outv[8]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<Tr::kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side: tensor maps and dispatch.
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D view [slabs][rows][Cp] of int8 limb planes; box = (bc bytes, box_rows, 1).
+bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t slabs, int bc, int box_rows) {
+  auto encode = get_encode_fn();
+  if (encode == nullptr) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)Cp, (cuuint64_t)rows, (cuuint64_t)slabs};
+  cuuint64_t strides[2] = {(cuuint64_t)Cp, (cuuint64_t)(rows * Cp)};
+  cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMapSwizzle sw = bc == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : bc == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                     : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+
+template <int BN, int BC, int MAXPL>
+cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, cudaStream_t s) {
+  using Cfg = GemmConfig<BN, BC, MAXPL>;
+  CUtensorMap tmV, tmU;
+  if (!make_tmap(&tmV, V, a.Cp, a.P, (int64_t)n_planes * a.npos, BC, kBlockM)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_planes * a.npos, BC, BN)) return cudaErrorInvalidValue;
+  auto kern = winograd_gemm_kernel<BN, BC, MAXPL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = a.total_tiles < g_num_sms ? a.total_tiles : g_num_sms;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, kThreads, Cfg::kSmemBytes, s>>>(tmV, tmU, a);
+  return cudaGetLastError();
+}
+
+template <int BN, int MAXPL>
+cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes, cudaStream_t s) {
+  switch (bc) {
+    case 32: return run_gemm<BN, 32, MAXPL>(a, V, U, n_planes, s);
+    case 64: return run_gemm<BN, 64, MAXPL>(a, V, U, n_planes, s);
+    default: return run_gemm<BN, 128, MAXPL>(a, V, U, n_planes, s);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp, int K,
+                                 int Kp, int bc, int16_t* Mw, cudaStream_t s) {
+  const PlanDevice& d = plan.dev;
+  GemmArgs a{};
+  a.P = P;
+  a.K = K;
+  a.Kp = Kp;
+  a.Cp = Cp;
+  a.npos = d.n * d.n;
+  a.n_res = d.n_res;
+  a.nkc = Cp / bc;
+  a.Mw = Mw;
+  int maxpl = 1;
+  for (int r = 0; r < d.n_res; ++r) {
+    a.planes[r] = d.res[r].planes;
+    a.plane_base[r] = d.res[r].plane_base;
+    a.modulus[r] = d.res[r].modulus;
+    a.inv_m[r] = d.res[r].inv_m;
+    a.r256[r] = d.res[r].r_256;
+    a.r65536[r] = d.res[r].r_65536;
+    if (d.res[r].planes > maxpl) maxpl = d.res[r].planes;
+  }
+  int bn;
+  if (maxpl == 2) bn = 64;
+  else bn = Kp <= 64 ? 64 : (Kp <= 128 ? 128 : 256);
+  a.num_pb = (int)((P + kBlockM - 1) / kBlockM);
+  a.num_kb = (Kp + bn - 1) / bn;
+  a.total_tiles = (int64_t)d.n_res * a.npos * a.num_pb * a.num_kb;
+  if (maxpl == 2) return run_gemm_bc<64, 2>(a, bc, V, U, d.n_planes, s);
+  if (bn == 64) return run_gemm_bc<64, 1>(a, bc, V, U, d.n_planes, s);
+  if (bn == 128) return run_gemm_bc<128, 1>(a, bc, V, U, d.n_planes, s);
+  return run_gemm_bc<256, 1>(a, bc, V, U, d.n_planes, s);
+}
+
+}  // namespace rnsw

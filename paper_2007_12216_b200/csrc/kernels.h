@@ -1,0 +1,43 @@
+// Internal launch interface between the C ABI (capi.cu) and the kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "plan.h"
+
+namespace rnsw {
+
+// Geometry of one layer call on the device path.
+struct Geometry {
+  int B, H, W, C, K, pad, layout;
+  int Ho, Wo, th, tw;  // output plane, tiles per side
+  int64_t P;           // B * th * tw
+  int Cp;              // C padded for the tensor-core K dimension
+  int Kp;              // K padded to 16
+  int bc;              // channel chunk per MMA stage (32 / 64 / 128 bytes)
+};
+
+// Host-side mirror of the plan (kept next to the device copy).
+struct PlanHost {
+  PlanDevice dev;         // host copy of the tables
+  PlanDevice* d_plan;     // device copy
+  int device;             // CUDA device the tables live on
+};
+
+cudaError_t launch_filter_transform(const PlanHost& plan, const int8_t* w, int C, int K, int Cp, int layout,
+                                    int8_t* U, cudaStream_t s);
+cudaError_t launch_filter_import(const PlanHost& plan, int res, const int16_t* u_nnck, int C, int K, int Cp,
+                                 int8_t* U, cudaStream_t s);
+cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
+                                   cudaStream_t s);
+cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp,
+                                 int K, int Kp, int bc, int16_t* Mw, cudaStream_t s);
+cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
+                                    int16_t* y_res, cudaStream_t s);
+cudaError_t launch_mrc(const PlanHost& plan, const int16_t* residues, int64_t count, int64_t* out,
+                       cudaStream_t s);
+cudaError_t launch_requant_pool(const int32_t* y, int B, int H, int W, int C, int shift, int pool, int8_t* out,
+                                cudaStream_t s);
+
+}  // namespace rnsw

@@ -1,0 +1,33 @@
+// Internal plan layout shared by the host entry points and the kernels.
+#pragma once
+#include <cstdint>
+
+#define RNSW_MAX_RES 4   // residues per system
+#define RNSW_MAX_N 16    // tile side N = M + R - 1
+#define RNSW_MAX_R 8     // filter side
+
+// Constant tables one residue needs on the device, as int32 so kernels can
+// load them straight into shared memory.
+struct ResidueTables {
+  int32_t modulus;
+  int32_t planes;      // 1: |v| <= 127 fits s8; 2: balanced hi/lo s8 limbs
+  int32_t plane_base;  // first limb-plane index of this residue in V / U
+  float inv_m;         // 1.0f / modulus
+  int32_t r_256;       // 256 mod m (symmetric)
+  int32_t r_65536;     // 65536 mod m (symmetric)
+  int32_t at[RNSW_MAX_N * RNSW_MAX_N];  // AT (M x N), row-major, stride N
+  int32_t bt[RNSW_MAX_N * RNSW_MAX_N];  // BT (N x N)
+  int32_t g[RNSW_MAX_N * RNSW_MAX_R];   // G  (N x R), stride R
+};
+
+struct PlanDevice {
+  int32_t m_out;  // M (outputs per tile side)
+  int32_t r;      // R
+  int32_t n;      // N = M + R - 1
+  int32_t n_res;
+  int32_t n_planes;  // total limb planes over all residues
+  int64_t dynamic_range;
+  int64_t signed_bound;
+  int64_t mrc_inv[RNSW_MAX_RES][RNSW_MAX_RES];  // m_i^-1 mod m_j, i < j
+  ResidueTables res[RNSW_MAX_RES];
+};
