@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark: VGG16 conv stack through the B200 RNS-Winograd path.
+
+Workload (BASELINE.json config 4; config 2 at --batch 1): the 13 3x3 conv
+layers of VGG16 on 224x224x3 int8 images, every layer an exact int32
+RNS-Winograd convolution F(14x14,3x3) over RNS(4001,4331) plus the device
+glue (relu, >> shift, clip, 2x2 max-pool).  The batch is sharded by image
+over the ranks (one process per GPU); the only collective is one all-gather
+of the final (B/N,7,7,512) int8 maps.
+
+Metric: direct-conv-equivalent INT8 TOPS = sum over layers of
+2*B*Ho*Wo*C*K*9 divided by the stack latency (whole job, all ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl reference]
+
+One JSON line on rank 0.  ``--impl reference`` times the CPU reference arm:
+the numpy restatement of the reference's winograd_layer_conv
+(oracle/ref_port.py), on the host cores, one image per worker process.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "direct-conv-equivalent INT8 TOPS and layer latency (VGG16 3x3), 1/2/4/8 B200"
+UNIT = "TOPS"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=256, help="global batch (images), sharded over ranks")
+    ap.add_argument("--impl", default="rnsw", choices=["rnsw", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-images", type=int, default=1)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of rw/layer.py:301-389; bench convention of
+# rw/cli.py:445-472: filters precomputed outside the timed region)
+
+_REF_STATE = {}
+
+
+def _ref_worker_init(moduli, tile_m):
+    _REF_STATE["moduli"] = moduli
+    _REF_STATE["tile_m"] = tile_m
+
+
+def _ref_one_image(idx):
+    import numpy as np
+    from oracle import ref_port
+    from oracle.vgg_ref import requant_pool
+    from paper_2007_12216_b200 import workloads as W
+
+    x = W.vgg16_images(1, start=idx)
+    banks, mats = _REF_STATE["banks"], _REF_STATE["mats"]
+    t0 = time.perf_counter()
+    for i, (name, side, c, k, pool) in enumerate(W.VGG16_LAYERS):
+        y = ref_port.winograd_layer(x, _REF_STATE["weights"][i], 1, _REF_STATE["tile_m"], _REF_STATE["moduli"],
+                                    mats=mats, filters=banks[i])
+        x = requant_pool(y, W.VGG16_SHIFTS[i], pool)
+    return time.perf_counter() - t0, int(np.asarray(x, dtype=np.int64).sum())
+
+
+def _prepare_reference(moduli=(4001, 4331), tile_m=14):
+    """Filter banks for the CPU path (excluded from timing, as the reference
+    bench does).  Exact einsum formulation of G g G^T mod m, checked equal
+    to the reference-order computation in tests/test_oracle.py."""
+    from oracle import ref_port
+    from paper_2007_12216_b200 import workloads as W
+
+    weights = W.vgg16_weights()
+    mats = {m: ref_port.modular_matrices(tile_m, 3, m) for m in moduli}
+    banks = [ref_port.filter_bank_fast(w, mats) for w in weights]
+    _REF_STATE.update(weights=weights, mats=mats, banks=banks, moduli=tuple(moduli), tile_m=tile_m)
+
+
+def cpu_reference_throughput(images: int, procs: int, moduli=(4001, 4331)):
+    """Time `images` images through the CPU port with `procs` worker
+    processes (fork after the filter banks are built); returns
+    (TOPS, seconds, per-image seconds)."""
+    import multiprocessing as mp
+
+    from paper_2007_12216_b200 import workloads as W
+
+    if "banks" not in _REF_STATE:
+        _prepare_reference(moduli)
+    ops_per_image = W.VGGConfig(batch=1).direct_ops()
+    t0 = time.perf_counter()
+    if procs <= 1:
+        res = [_ref_one_image(i) for i in range(images)]
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            res = pool.map(_ref_one_image, range(images))
+    wall = time.perf_counter() - t0
+    return ops_per_image * images / wall / 1e12, wall, [r[0] for r in res]
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2007_12216_b200 import workloads as W
+
+    n_res = 2
+    cores = len(os.sched_getaffinity(0))
+    procs = max(1, cores // n_res)
+    _prepare_reference()
+    vals = []
+    for step in range(args.warmup + args.steps):
+        tops, wall, per = cpu_reference_throughput(procs, procs)
+        if step >= args.warmup:
+            vals.append((tops, wall))
+    value = statistics.median(v[0] for v in vals)
+    ms = statistics.median(v[1] for v in vals) * 1e3
+    sample = (f"{procs} images per step (one per worker process, {n_res} threads each: the reference's "
+              f"one-thread-per-modulus pool), all 13 VGG16 layers, F(14x14,3x3) RNS(4001,4331), numpy port of "
+              f"rw/layer.py winograd_layer_conv, filters precomputed")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded PCG64, rw/cli.py:82-94 convention)",
+        "config": {"workload": "VGG16 13x conv3x3 stack, 224x224x3, F(14x14,3x3), RNS(4001,4331), CPU sample",
+                   "images_per_step": procs},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": procs * n_res, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.out = out
+        else:
+            self.out = ""
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for line in self.out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measure_int8_peak(torch):
+    """Dense INT8 tensor throughput on this GPU: torch._int_mm (cuBLASLt
+    s8 x s8 -> s32) at 8192^3, best of 10 (burst)."""
+    n = 8192
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda").t()
+    for _ in range(3):
+        torch._int_mm(a, b)
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * n**3 / (best * 1e-3) / 1e12
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture (profiles/*traffic*.json), if one matches this build."""
+    for p in sorted((ROOT / "profiles").glob("*traffic*.json"), reverse=True):
+        try:
+            return json.loads(p.read_text())
+        except (OSError, ValueError):
+            continue
+    return {}
+
+
+def run_gpu_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_12216_b200 import workloads as W
+    from paper_2007_12216_b200.vgg import VGG16Rns
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.batch % world:
+        raise SystemExit(f"--batch {args.batch} must be divisible by {world} ranks")
+    shard = args.batch // world
+    net = VGG16Rns()
+    x_host = W.vgg16_images(shard, start=rank * shard)
+    x_pinned = torch.from_numpy(x_host).pin_memory()
+    x_dev = x_pinned.cuda()
+    gathered = torch.empty((args.batch, 7, 7, 512), dtype=torch.int8, device="cuda") if world > 1 else None
+    out_pinned = torch.empty((args.batch if rank == 0 else shard, 7, 7, 512), dtype=torch.int8).pin_memory()
+
+    def step(x):
+        y = net.forward(x)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, y)
+            return gathered
+        return y
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(x_dev)
+    torch.cuda.synchronize()
+    barrier()
+
+    # -------- timed region: K steps, inputs resident in HBM --------
+    gpu_index = local
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        gpu_index = vis.split(",")[local]
+    with ClockSampler(gpu_index) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step(x_dev)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    elapsed = e0.elapsed_time(e1) / 1e3
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    total_ops = W.VGGConfig(batch=args.batch).direct_ops() * args.steps
+    value = total_ops / elapsed / 1e12
+    ms_per_step = elapsed / args.steps * 1e3
+
+    # -------- per-kernel device times over a second timed pass --------
+    rec = []
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        net.forward_staged(x_dev, lambda kind, i, a, b: rec.append((kind, i, a, b)))
+    torch.cuda.synchronize()
+    per_kind, per_layer = {}, {}
+    for kind, i, a, b in rec:
+        dt = a.elapsed_time(b) / 1e3 / args.steps
+        per_kind[kind] = per_kind.get(kind, 0.0) + dt
+        per_layer.setdefault(i, {}).setdefault(kind, 0.0)
+        per_layer[i][kind] += dt
+    work = net.layer_work(shard)
+    stage_sum = sum(per_kind.values())
+    dominant = max(per_kind, key=per_kind.get)
+
+    # -------- e2e: host buffers through the public API, copies timed --------
+    barrier()
+    torch.cuda.synchronize()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record()
+    for _ in range(args.steps):
+        xd = x_pinned.to("cuda", non_blocking=True)
+        y = step(xd)
+        if rank == 0:
+            out_pinned.copy_(y, non_blocking=True)
+    h1.record()
+    torch.cuda.synchronize()
+    e2e_elapsed = h0.elapsed_time(h1) / 1e3
+    t = torch.tensor([e2e_elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_elapsed = float(t.item())
+    e2e_value = total_ops / e2e_elapsed / 1e12
+    h2d = x_host.nbytes * world
+    d2h = out_pinned.numel()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import json as _json
+
+    peaks = _json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    if dominant == "gemm":
+        int8_peak = measure_int8_peak(torch)
+        achieved = sum(w["gemm_ops"] for w in work) / per_kind["gemm"] / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(int8_peak, 1), "unit": "TFLOP/s",
+                "peak_source": "measured this run: torch._int_mm int8 8192^3 burst"}
+    else:
+        key = {"input_transform": "input_transform_bytes", "output_transform": "output_transform_bytes",
+               "glue": "glue_bytes"}[dominant]
+        achieved = sum(w[key] for w in work) / per_kind[dominant] / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["kernel"] = dominant
+    traffic = load_traffic().get(f"{dominant}:b{shard}")
+    roof["traffic"] = traffic
+
+    stages = {}
+    for kind, sec in per_kind.items():
+        s = {"ms": round(sec * 1e3, 3), "share": round(sec / stage_sum, 4)}
+        if kind == "gemm":
+            s["TOPS"] = round(sum(w["gemm_ops"] for w in work) / sec / 1e12, 2)
+        else:
+            k = {"input_transform": "input_transform_bytes", "output_transform": "output_transform_bytes",
+                 "glue": "glue_bytes"}[kind]
+            s["GB_s"] = round(sum(w[k] for w in work) / sec / 1e9, 1)
+        stages[kind] = s
+    layer_ms = {work[i]["name"]: round(sum(v.values()) * 1e3, 3) for i, v in sorted(per_layer.items())}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded PCG64 images U{0..127}, weights round(N(0,20^2)) clipped; no dataset)",
+        "config": {"workload": f"BASELINE config 4: VGG16 13x conv3x3 stack, 224x224x3, batch {args.batch} "
+                               f"sharded {shard}/rank, F(14x14,3x3), RNS(4001,4331), relu/shift/maxpool glue",
+                   "global_batch": args.batch, "per_rank_batch": shard, "tile": "F(14x14,3x3)",
+                   "moduli": [4001, 4331], "parallelism": f"image-sharded x{world}, one all-gather at the end",
+                   "l2": "inputs and intermediates larger than L2 (126 MB)",
+                   "layer_ms": layer_ms},
+        "stages": stages,
+        "gpu_launches": net.launches_per_forward() * args.steps,
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(e2e_elapsed / args.steps * 1e3, 3)},
+        "roofline": roof,
+        "clocks": clocks.summary(),
+    }
+
+    if world == 1 and not args.no_cpu_baseline:
+        n_res = 2
+        tops, wall, per = cpu_reference_throughput(args.cpu_sample_images, 1)
+        line["cpu_baseline"] = {
+            "value": round(tops, 6), "unit": UNIT, "cores": n_res, "kind": "port",
+            "sample": f"{args.cpu_sample_images} image(s) through all 13 layers on the host, numpy port of the "
+                      f"reference winograd_layer_conv (one thread per modulus, as shipped), filters precomputed; "
+                      f"{wall:.1f} s",
+        }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

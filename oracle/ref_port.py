@@ -153,6 +153,26 @@ def filter_bank(w: np.ndarray, mats: dict) -> dict:
     return out
 
 
+def filter_bank_fast(w: np.ndarray, mats: dict) -> dict:
+    """Same result as ``filter_bank`` (symmetric residues of G g G^T mod m),
+    computed with two int64 einsums; used only to prepare CPU-baseline
+    inputs quickly (the reference excludes the filter transform from its
+    bench timing, rw/cli.py:459-463)."""
+    out = {}
+    r, _, c, k = w.shape
+    wf = w.astype(np.float64).reshape(r, r * c * k)
+    def fmod_sym(a, m):  # exact: integers < 2^52, x/m never ties for odd m
+        a -= m * np.rint(a / m)
+        return a
+
+    for m, (at, g, bt) in mats.items():
+        gf = g.astype(np.float64)  # products stay far below 2^53: exact
+        t = fmod_sym((gf @ wf).reshape(-1, r, c * k), m)
+        u = fmod_sym(np.matmul(gf[None], t), m)  # (n, n, c*k)
+        out[m] = u.reshape(g.shape[0], g.shape[0], c, k).astype(narrow(m))
+    return out
+
+
 def input_stage(patches: np.ndarray, bt: np.ndarray, m: int) -> np.ndarray:
     """(B,th,tw,n,n,C) -> V (n*n, P, C)."""
     b, th, tw, n, _, c = patches.shape

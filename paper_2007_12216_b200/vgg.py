@@ -1,0 +1,164 @@
+"""VGG16 conv stack on the RNS-Winograd device path (BASELINE configs 2 and 4).
+
+Thirteen 3x3/pad-1 layers, each an exact int32 RNS-Winograd convolution
+(F(14x14,3x3) over RNS(4001,4331) by default) followed by the device glue
+relu -> >> shift -> clip [0,127] (-> 2x2 max-pool after each block).  The
+glue is defined by BASELINE.json, not by the reference package.
+Filters are transformed once at construction (the reference bench also
+excludes the filter transform from timing, rw/cli.py:459-472).
+
+Everything runs on one CUDA stream; buffers are allocated once per batch size
+so a forward pass issues only kernel launches (52 for the 13 layers).
+"""
+
+from __future__ import annotations
+
+import math
+
+from . import _native, workloads
+from .layer import _filters_on_device, _stream_ptr, plan_for, range_check, LayerSpec
+from .errors import DynamicRangeExceeded
+from .residue import RnsSystem
+from .transforms import cached_transforms
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class VGG16Rns:
+    def __init__(self, cfg: workloads.VGGConfig | None = None, weights=None):
+        torch = _torch()
+        self.cfg = cfg or workloads.VGGConfig()
+        self.system = RnsSystem(self.cfg.moduli)
+        self.plan = plan_for(cached_transforms(self.cfg.tile_m, 3), self.system)
+        self.weights = weights if weights is not None else workloads.vgg16_weights(self.cfg.seed)
+        self.bounds = workloads.vgg16_bounds(self.weights, self.cfg.moduli)
+        self.banks = []
+        for (name, side, c, k, _), w, bound in zip(self.cfg.layers, self.weights, self.bounds):
+            spec = LayerSpec(h=side, w=side, c=c, k=k, r=3, padding=1, tile_m=self.cfg.tile_m)
+            rep = range_check(spec, self.system, bound)
+            if not rep.fits:
+                raise DynamicRangeExceeded(f"{name}: bound {rep.bound} exceeds {rep.signed_bound}")
+            wd = torch.from_numpy(w).cuda()
+            self.banks.append(_filters_on_device(self.plan, wd, c, k, _native.LAYOUT_NHWC))
+        torch.cuda.synchronize()
+        self._buffers = {}
+
+    def _alloc(self, batch: int):
+        torch = _torch()
+        if batch in self._buffers:
+            return self._buffers[batch]
+        l = _native.lib()
+        dev = f"cuda:{torch.cuda.current_device()}"
+        ws = max(l.rnsw_workspace_bytes(self.plan.handle, batch, side, side, c, k, 1)
+                 for _, side, c, k, _ in self.cfg.layers)
+        ymax = max(batch * side * side * k for _, side, c, k, _ in self.cfg.layers)
+        amax = max(batch * side * side * c for _, side, c, k, _ in self.cfg.layers)
+        bufs = {
+            "ws": torch.empty(ws, dtype=torch.uint8, device=dev),
+            "y": torch.empty(ymax, dtype=torch.int32, device=dev),
+            "act": [torch.empty(amax, dtype=torch.int8, device=dev) for _ in range(2)],
+            "out": torch.empty((batch, 7, 7, 512), dtype=torch.int8, device=dev),
+        }
+        self._buffers[batch] = bufs
+        return bufs
+
+    def launches_per_forward(self) -> int:
+        return 4 * len(self.cfg.layers)  # input transform, GEMM, output transform, glue
+
+    def layer_work(self, batch: int) -> list[dict]:
+        """Algorithmic work per layer and kernel ("Roofline"):
+        bytes for the memory-bound stages, int8 tensor ops for the GEMM."""
+        out = []
+        n = self.plan.n
+        npos = n * n
+        planes = sum(1 if m < 256 else 2 for m in self.cfg.moduli)
+        mma_per_product = sum(1 if m < 256 else 4 for m in self.cfg.moduli)
+        for name, side, c, k, pool in self.cfg.layers:
+            tiles = batch * math.ceil(side / self.cfg.tile_m) ** 2
+            oside = side // 2 if pool else side
+            out.append({
+                "name": name,
+                "input_transform_bytes": batch * side * side * c + planes * npos * tiles * c,
+                "gemm_ops": 2 * tiles * npos * c * k * mma_per_product,
+                "output_transform_bytes": len(self.cfg.moduli) * npos * tiles * k * 2 + batch * side * side * k * 4,
+                "glue_bytes": batch * side * side * k * 4 + batch * oside * oside * k,
+                "direct_ops": 2 * batch * side * side * c * k * 9,
+            })
+        return out
+
+    def forward_staged(self, x, record):
+        """Same launches as forward(), one C-ABI stage call per kernel with a
+        CUDA event pair around each (``record(kind, layer, start, end)``)."""
+        torch = _torch()
+        l = _native.lib()
+        vp = _native.c_void_p
+        batch = int(x.shape[0])
+        bufs = self._alloc(batch)
+        s = _stream_ptr()
+        ws = bufs["ws"]
+        cur = x.contiguous()
+        nl = len(self.cfg.layers)
+
+        def timed(kind, i, fn):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _native.check(fn())
+            b.record()
+            record(kind, i, a, b)
+
+        for i, ((name, side, c, k, pool), bank) in enumerate(zip(self.cfg.layers, self.banks)):
+            y = bufs["y"][: batch * side * side * k].view(batch, side, side, k)
+            tiles = batch * math.ceil(side / self.cfg.tile_m) ** 2
+            vb = (l.rnsw_v_bytes(self.plan.handle, tiles, c) + 255) // 256 * 256
+            v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
+            timed("input_transform", i, lambda: l.rnsw_input_transform(
+                self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
+            timed("gemm", i, lambda: l.rnsw_winograd_gemm(
+                self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), ws.numel() - vb, s))
+            timed("output_transform", i, lambda: l.rnsw_output_transform(
+                self.plan.handle, vp(m_ptr), batch, side, side, k, 1, _native.LAYOUT_NHWC, vp(y.data_ptr()), s))
+            oside = side // 2 if pool else side
+            nxt = bufs["out"] if i == nl - 1 else \
+                bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
+            timed("glue", i, lambda: l.rnsw_requant_pool(vp(y.data_ptr()), batch, side, side, k, self.cfg.shifts[i],
+                                                         1 if pool else 0, vp(nxt.data_ptr()), s))
+            cur = nxt
+        return cur
+
+    def forward(self, x, keep_int32: bool = False):
+        """x: (B, 224, 224, 3) int8 CUDA tensor (NHWC).  Returns the final
+        (B, 7, 7, 512) int8 map, plus every layer's int32 output if asked."""
+        torch = _torch()
+        l = _native.lib()
+        vp = _native.c_void_p
+        batch = int(x.shape[0])
+        bufs = self._alloc(batch)
+        s = _stream_ptr()
+        ws = bufs["ws"]
+        cur = x.contiguous()
+        outs = []
+        nl = len(self.cfg.layers)
+        for i, ((name, side, c, k, pool), bank) in enumerate(zip(self.cfg.layers, self.banks)):
+            y = bufs["y"][: batch * side * side * k].view(batch, side, side, k)
+            _native.check(l.rnsw_conv_forward(self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, k, 1,
+                                              _native.LAYOUT_NHWC, vp(bank.data.data_ptr()), vp(y.data_ptr()),
+                                              vp(ws.data_ptr()), ws.numel(), s))
+            if keep_int32:
+                outs.append(y.clone())
+            oside = side // 2 if pool else side
+            if i == nl - 1:
+                nxt = bufs["out"]
+            else:
+                nxt = bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
+            _native.check(l.rnsw_requant_pool(vp(y.data_ptr()), batch, side, side, k, self.cfg.shifts[i],
+                                              1 if pool else 0, vp(nxt.data_ptr()), s))
+            cur = nxt
+        return (cur, outs) if keep_int32 else cur
+
+
+def direct_ops(batch: int) -> int:
+    return workloads.VGGConfig(batch=batch).direct_ops()
