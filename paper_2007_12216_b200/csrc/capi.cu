@@ -162,6 +162,16 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
     t.inv_m = 1.0f / (float)m;
     t.r_256 = sym(256, m);
     t.r_65536 = sym(65536, m);
+    t.half = half;
+    {
+      int sh = 0;
+      while ((2 << sh) <= m) ++sh;  // sh = floor(log2 m)
+      const unsigned __int128 num = (unsigned __int128)1 << (32 + sh);
+      t.red_mul = (uint32_t)((num + m - 1) / m);
+      t.red_shift = sh;
+      const int64_t L = ((1LL << 28) + m - 1) / m;
+      t.red_off = (int32_t)(half + m * L);
+    }
     auto load = [&](const int16_t* src, int rows, int cols, int stride, int32_t* dst) -> bool {
       for (int a = 0; a < rows; ++a)
         for (int b = 0; b < cols; ++b) {
@@ -178,6 +188,11 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
     d.dynamic_range *= m;
   }
   d.n_planes = plane;
+  {
+    bool fast = d.dynamic_range < (1LL << 31);
+    for (int i = 0; i < n_res; ++i) fast = fast && moduli[i] < 6000;
+    d.fast = fast ? 1 : 0;
+  }
   d.signed_bound = (d.dynamic_range - 1) / 2;
   for (int j = 0; j < n_res; ++j)
     for (int i = 0; i < j; ++i) {

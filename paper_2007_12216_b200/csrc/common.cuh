@@ -42,6 +42,26 @@ RNSW_DEV int32_t sym_mod_small(int32_t x, float m, float inv_m) {
   return __float_as_int(r + magic) - 0x4B400000;
 }
 
+// Exact symmetric reduction for |x| < 2^28 without division: with
+// s = floor(log2 m), mul = ceil(2^(32+s) / m) and n = x + h + m*ceil(2^28/m)
+// in [0, 2^30), floor(n/m) = umulhi(n, mul) >> s exactly (the rounding error
+// n*(mul*m - 2^(32+s)) / (m*2^(32+s)) stays below 1/(2m)).  Then
+// n - floor(n/m)*m - h is x's representative in [-h, h].
+struct FastMod {
+  uint32_t mul;
+  int32_t shift, off, m, h;
+};
+
+RNSW_DEV FastMod fast_mod_of(const ResidueTables& t) {
+  return FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half};
+}
+
+RNSW_DEV int32_t red_fast(int32_t x, const FastMod& f) {
+  const uint32_t n = (uint32_t)(x + f.off);
+  const uint32_t q = __umulhi(n, f.mul) >> f.shift;
+  return (int32_t)(n - q * (uint32_t)f.m) - f.h;
+}
+
 // 64-bit exact symmetric reduction (used for the mixed-radix digits).
 RNSW_DEV int64_t sym_mod64(int64_t x, int64_t m) {
   int64_t r = x % m;
@@ -176,3 +196,34 @@ __host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n) {
          | ((n >> 3) << 17)    // N / 8
          | ((m >> 4) << 24);   // M / 16
 }
+
+// ---------------------------------------------------------------------------
+// Warp-level int8 tensor-core MMA (mma.sync m16n8k16) for the small,
+// register-resident Winograd transforms.  Fragment ownership (g = lane/4,
+// t = lane%4): A rows g / g+8, k = 4t..4t+3; B k = 4t..4t+3, column g;
+// C rows g (c0,c1) / g+8 (c2,c3), columns 2t, 2t+1.
+
+RNSW_DEV void imma_ss(int32_t (&c)[4], uint32_t a0, uint32_t a1, uint32_t b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(b));
+}
+
+RNSW_DEV void imma_su(int32_t (&c)[4], uint32_t a0, uint32_t a1, uint32_t b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(b));
+}
+
+// Low bytes of four int32 values packed little-endian into one register.
+RNSW_DEV uint32_t pack4_lo(int32_t x0, int32_t x1, int32_t x2, int32_t x3) {
+  const uint32_t a = __byte_perm((uint32_t)x0, (uint32_t)x1, 0x0040);
+  const uint32_t b = __byte_perm((uint32_t)x2, (uint32_t)x3, 0x0040);
+  return __byte_perm(a, b, 0x5410);
+}
+
+// High limb of the balanced split v = 256*hi + lo, lo in [-128, 127].
+RNSW_DEV int32_t limb_hi(int32_t v) { return (v + 128) >> 8; }
+

@@ -32,7 +32,7 @@ namespace rnsw {
 namespace {
 
 constexpr int kBlockM = 128;  // tiles (P) per MMA tile: TMEM lanes
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // warps 0-3 producer/MMA/alloc/idle, 4-11 epilogue
 
 struct GemmArgs {
   int64_t P;
@@ -45,6 +45,8 @@ struct GemmArgs {
   float inv_m[RNSW_MAX_RES];
   int r256[RNSW_MAX_RES];
   int r65536[RNSW_MAX_RES];
+  FastMod fm[RNSW_MAX_RES];
+  int fast;  // exact division-free reductions apply (plan.fast and C <= 8192)
   int16_t* Mw;
 };
 
@@ -73,6 +75,99 @@ struct GemmConfig {
   static constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256 /*barriers*/;
 };
 
+// Epilogue helpers.  Each thread owns one accumulator row (tile p) and a
+// half of the BN columns.  All TMEM loads of a batch are issued before a
+// single wait; the accumulator is released (tempty arrive) as soon as the
+// last batch has landed in registers, so the next tile's MMAs overlap the
+// reductions and stores.
+
+RNSW_DEV int32_t reduce_generic(int32_t v, const GemmArgs& a, int res) {
+  return sym_mod(v, a.modulus[res], a.inv_m[res]);
+}
+
+RNSW_DEV void store16(int16_t* dst, const int32_t (&r)[16]) {
+  int16_t o[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) o[e] = (int16_t)r[e];
+  int4* d = reinterpret_cast<int4*>(dst);
+  d[0] = *reinterpret_cast<const int4*>(&o[0]);
+  d[1] = *reinterpret_cast<const int4*>(&o[8]);
+}
+
+RNSW_DEV void release_acc(uint64_t* bar, int lane) {
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
+}
+
+// 16-bit residues: three accumulators (hh, cross, ll) per column.
+template <int BN, int ACC_COLS>
+RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
+                             uint64_t* tempty, int lane) {
+  constexpr int kHalf = BN / 2;
+  constexpr int kBatch = 32;  // columns per batch: 3 x 32 registers in flight
+  const FastMod fm = a.fm[res];
+  const int32_t r8 = a.r256[res], r16 = a.r65536[res];
+#pragma unroll 1
+  for (int c0 = 0; c0 < kHalf; c0 += kBatch) {
+    int32_t hh[kBatch / 16][16], cr[kBatch / 16][16], ll[kBatch / 16][16];
+#pragma unroll
+    for (int j = 0; j < kBatch / 16; ++j) {
+      tmem_ld16(taddr + c0 + 16 * j, hh[j]);
+      tmem_ld16(taddr + BN + c0 + 16 * j, cr[j]);
+      tmem_ld16(taddr + 2 * BN + c0 + 16 * j, ll[j]);
+    }
+    tmem_ld_wait();
+    if (c0 + kBatch >= kHalf) release_acc(tempty, lane);
+#pragma unroll
+    for (int j = 0; j < kBatch / 16; ++j) {
+      int32_t r[16];
+      if (a.fast) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          r[e] = red_fast(red_fast(hh[j][e], fm) * r16 + red_fast(cr[j][e], fm) * r8 + ll[j][e], fm);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          r[e] = reduce_generic(reduce_generic(hh[j][e], a, res) * r16 + reduce_generic(cr[j][e], a, res) * r8 +
+                                    reduce_generic(ll[j][e], a, res), a, res);
+      }
+      const int col = col0 + c0 + 16 * j;
+      if (row_ok && col < a.Kp) store16(out_row + col, r);
+    }
+  }
+}
+
+// 8-bit residues: one accumulator per column.
+template <int BN>
+RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
+                              uint64_t* tempty, int lane) {
+  constexpr int kHalf = BN / 2;
+  constexpr int kBatch = kHalf < 64 ? kHalf : 64;
+  const FastMod fm = a.fm[res];
+#pragma unroll 1
+  for (int c0 = 0; c0 < kHalf; c0 += kBatch) {
+    int32_t v[kBatch / 16][16];
+#pragma unroll
+    for (int j = 0; j < kBatch / 16; ++j) tmem_ld16(taddr + c0 + 16 * j, v[j]);
+    tmem_ld_wait();
+    if (c0 + kBatch >= kHalf) release_acc(tempty, lane);
+#pragma unroll
+    for (int j = 0; j < kBatch / 16; ++j) {
+      int32_t r[16];
+      if (a.fast) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] = red_fast(v[j][e], fm);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] = reduce_generic(v[j][e], a, res);
+      }
+      const int col = col0 + c0 + 16 * j;
+      if (row_ok && col < a.Kp) store16(out_row + col, r);
+    }
+  }
+}
+
 template <int BN, int BC, int MAXPL>
 __global__ void __launch_bounds__(kThreads, 1)
     winograd_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
@@ -100,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 8);
     }
     fence_mbar_init();
   }
@@ -191,8 +286,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue ----------------
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    // ---------------- epilogue: 8 warps = 4 TMEM lane quadrants x 2 column halves ----------------
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int half = (warp - 4) >> 2;       // column half of the accumulator tile
+    constexpr int kHalf = BN / 2;
     int it = 0;
     for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
       int64_t rest = t;
@@ -203,50 +300,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int pos = (int)(rest % args.npos);
       const int res = (int)(rest / args.npos);
       const int pl = args.planes[res];
-      const int32_t m = args.modulus[res];
-      const float inv = args.inv_m[res];
-      const int32_t r8 = args.r256[res], r16 = args.r65536[res];
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const int64_t p = (int64_t)pb * kBlockM + q * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Tr::kAccCols;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Tr::kAccCols + half * kHalf;
       int16_t* out_row = args.Mw + ((p * args.n_res + res) * args.npos + pos) * (int64_t)args.Kp;
-#pragma unroll 1
-      for (int j = 0; j < BN / 16; ++j) {
-        int32_t v0[16];
-        tmem_ld16(taddr + j * 16, v0);
-        int32_t v1[16], v2[16];
-        if (MAXPL == 2 && pl == 2) {
-          tmem_ld16(taddr + BN + j * 16, v1);
-          tmem_ld16(taddr + 2 * BN + j * 16, v2);
-        }
-        tmem_ld_wait();
-        int16_t outv[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          int32_t r;
-          if (MAXPL == 2 && pl == 2) {
-            const int32_t hh = sym_mod(v0[e], m, inv);
-            const int32_t cr = sym_mod(v1[e], m, inv);
-            const int32_t ll = sym_mod(v2[e], m, inv);
-            r = sym_mod(hh * r16 + cr * r8 + ll, m, inv);
-          } else {
-            r = sym_mod(v0[e], m, inv);
-          }
-          outv[e] = (int16_t)r;
-        }
-        const int col = kb * BN + j * 16;
-        if (p < args.P && col < args.Kp) {
-          int4* dst = reinterpret_cast<int4*>(out_row + col);
-          dst[0] = *reinterpret_cast<const int4*>(&outv[0]);
-          dst[1] = *reinterpret_cast<const int4*>(&outv[8]);
-        }
+      const int col0 = kb * BN + half * kHalf;
+      const bool row_ok = p < args.P;
+      if (MAXPL == 2 && pl == 2) {
+        epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane);
+      } else {
+        epilogue_single<BN>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
     }
   }
 
@@ -343,8 +410,11 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
     a.inv_m[r] = d.res[r].inv_m;
     a.r256[r] = d.res[r].r_256;
     a.r65536[r] = d.res[r].r_65536;
+    const ResidueTables& t = d.res[r];
+    a.fm[r] = FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half};
     if (d.res[r].planes > maxpl) maxpl = d.res[r].planes;
   }
+  a.fast = (d.fast && Cp <= 8192) ? 1 : 0;
   int bn;
   if (maxpl == 2) bn = 64;
   else bn = Kp <= 64 ? 64 : (Kp <= 128 ? 128 : 256);

@@ -1,0 +1,201 @@
+// K1 on the tensor cores: V = BT d B mod m for every tile, channel and
+// residue (rw/layer.py:278-283, rw/kernel.py:44-47, 21-30), written straight
+// into the GEMM operand layout V[plane][pos][P][Cp].
+//
+// CTA = one tile p x 64 channels; each warp owns 16 channels.  A lane loads
+// 16 channels of 4 patch pixels (two 16-byte rows per n-tile), and 4x4 byte
+// transposes (PRMT) turn them into mma.sync B fragments, so the patch never
+// touches shared memory:
+//   pass 1  T^T = BT * D^T    (A = BT constants, B = patch bytes)
+//   pass 2  V^T = T^T * BT^T  (A = pass-1 C registers with the contraction
+//                              index permuted onto the k-slots, B = BT^T)
+// Each lane ends up holding 8 transform positions x 16 channels, i.e. one
+// 16-byte row segment of V per position and plane, stored with one vector
+// store.  16-bit moduli: BT and T are split into two s8 limbs; the exact
+// int32 recombination stays below 2^28 (m < 6000) so one division-free
+// reduction per value suffices.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rnsw {
+namespace {
+
+constexpr int kCTAChannels = 64;
+
+// Insert the low byte of v as byte q of w.
+RNSW_DEV uint32_t put_byte(uint32_t w, int32_t v, int q) {
+  const uint32_t sel = q == 0 ? 0x3214u : q == 1 ? 0x3240u : q == 2 ? 0x3410u : 0x4210u;
+  return __byte_perm(w, (uint32_t)v, sel);
+}
+
+// 4x4 byte transpose: in[e] = 4 channels of pixel e -> out[q] = channel q of pixels 0..3.
+RNSW_DEV void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
+  const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
+  const uint32_t t2 = __byte_perm(w0, w1, 0x7362), t3 = __byte_perm(w2, w3, 0x7362);
+  o[0] = __byte_perm(t0, t1, 0x5410);
+  o[1] = __byte_perm(t0, t1, 0x7632);
+  o[2] = __byte_perm(t2, t3, 0x5410);
+  o[3] = __byte_perm(t2, t3, 0x7632);
+}
+
+RNSW_DEV uint32_t word_of(const uint4& v, int u) { return u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w; }
+
+__global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
+                                                                 const int8_t* __restrict__ x,
+                                                                 int8_t* __restrict__ V) {
+  __shared__ int32_t BT16[RNSW_MAX_RES * 256];
+  const int N = plan->n, M = plan->m_out, npos = N * N, nres = plan->n_res;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
+  const int64_t p = blockIdx.x;
+  const int c_base = blockIdx.y * kCTAChannels + warp * 16;
+  for (int idx = tid; idx < nres * 256; idx += blockDim.x) {
+    const int r = idx >> 8, a = (idx >> 4) & 15, b = idx & 15;
+    BT16[idx] = (a < N && b < N) ? plan->res[r].bt[a * RNSW_MAX_N + b] : 0;
+  }
+  __syncthreads();
+  if (c_base >= g.Cp) return;
+  const int b_img = (int)(p / (g.th * g.tw));
+  const int ti = (int)((p / g.tw) % g.th);
+  const int tj = (int)(p % g.tw);
+  const int64_t plane_stride = (int64_t)npos * g.P * g.Cp;
+
+  // ---- patch: raw[ni][e] = channels c_base..+15 of pixel (a = g + 8 ni, b = 4t + e)
+  uint4 raw[2][4];
+  const bool vec = g.layout == 0 && (g.C & 15) == 0;
+#pragma unroll
+  for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int a = gq + 8 * ni, bcol = 4 * tq + e;
+      const int h = ti * M + a - g.pad, w = tj * M + bcol - g.pad;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (a < N && bcol < N && h >= 0 && h < g.H && w >= 0 && w < g.W && c_base < g.C) {
+        if (vec) {
+          v = __ldg(reinterpret_cast<const uint4*>(x + (((int64_t)b_img * g.H + h) * g.W + w) * g.C + c_base));
+        } else {
+          uint32_t wd[4] = {0, 0, 0, 0};
+          for (int q = 0; q < 16 && c_base + q < g.C; ++q) {
+            const int c = c_base + q;
+            const int64_t xi = g.layout == 0 ? (((int64_t)b_img * g.H + h) * g.W + w) * g.C + c
+                                             : (((int64_t)b_img * g.C + c) * g.H + h) * g.W + w;
+            wd[q >> 2] |= (uint32_t)(uint8_t)x[xi] << (8 * (q & 3));
+          }
+          v = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+      }
+      raw[ni][e] = v;
+    }
+
+  for (int r = 0; r < nres; ++r) {
+    const ResidueTables& tb = plan->res[r];
+    const FastMod fm = fast_mod_of(tb);
+    const int planes = tb.planes;
+    const int32_t* bt = BT16 + r * 256;
+    // pass-1 A: BT rows j = g / g+8, columns b = 4t..4t+3
+    int32_t av[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      av[e] = bt[gq * 16 + 4 * tq + e];
+      av[4 + e] = bt[(gq + 8) * 16 + 4 * tq + e];
+    }
+    const uint32_t alo0 = pack4_lo(av[0], av[1], av[2], av[3]);
+    const uint32_t alo1 = pack4_lo(av[4], av[5], av[6], av[7]);
+    const uint32_t ahi0 = pack4_lo(limb_hi(av[0]), limb_hi(av[1]), limb_hi(av[2]), limb_hi(av[3]));
+    const uint32_t ahi1 = pack4_lo(limb_hi(av[4]), limb_hi(av[5]), limb_hi(av[6]), limb_hi(av[7]));
+    // pass-2 B: column i = g + 8 ni, k-slot e <-> a = {2t, 2t+1, 8+2t, 9+2t}[e]
+    uint32_t blo[2], bhi[2];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const int i = gq + 8 * ni;
+      const int32_t v0 = bt[i * 16 + 2 * tq], v1 = bt[i * 16 + 2 * tq + 1];
+      const int32_t v2 = bt[i * 16 + 8 + 2 * tq], v3 = bt[i * 16 + 9 + 2 * tq];
+      blo[ni] = pack4_lo(v0, v1, v2, v3);
+      bhi[ni] = pack4_lo(limb_hi(v0), limb_hi(v1), limb_hi(v2), limb_hi(v3));
+    }
+
+    uint32_t outw[2][8][4];  // [plane][position slot][channel word]
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t din[2][4];
+      transpose4x4(word_of(raw[0][0], u), word_of(raw[0][1], u), word_of(raw[0][2], u), word_of(raw[0][3], u),
+                   din[0]);
+      transpose4x4(word_of(raw[1][0], u), word_of(raw[1][1], u), word_of(raw[1][2], u), word_of(raw[1][3], u),
+                   din[1]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int32_t t[2][4];
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          int32_t acc[4] = {0, 0, 0, 0};
+          if (planes == 2) {
+            int32_t hi[4] = {0, 0, 0, 0};
+            imma_ss(hi, ahi0, ahi1, din[ni][q]);
+            imma_ss(acc, alo0, alo1, din[ni][q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) t[ni][e] = red_fast(hi[e] * 256 + acc[e], fm);
+          } else {
+            imma_ss(acc, alo0, alo1, din[ni][q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) t[ni][e] = red_fast(acc[e], fm);
+          }
+        }
+        // pass 2: A rows j = g / g+8, k-slots = {2t, 2t+1, 8+2t, 9+2t}
+        const uint32_t tlo0 = pack4_lo(t[0][0], t[0][1], t[1][0], t[1][1]);
+        const uint32_t tlo1 = pack4_lo(t[0][2], t[0][3], t[1][2], t[1][3]);
+        int32_t v[2][4];
+        if (planes == 2) {
+          const uint32_t thi0 = pack4_lo(limb_hi(t[0][0]), limb_hi(t[0][1]), limb_hi(t[1][0]), limb_hi(t[1][1]));
+          const uint32_t thi1 = pack4_lo(limb_hi(t[0][2]), limb_hi(t[0][3]), limb_hi(t[1][2]), limb_hi(t[1][3]));
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
+            imma_ss(hh, thi0, thi1, bhi[ni]);
+            imma_ss(cr, thi0, thi1, blo[ni]);
+            imma_ss(cr, tlo0, tlo1, bhi[ni]);
+            imma_ss(ll, tlo0, tlo1, blo[ni]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[ni][e] = red_fast(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+          }
+        } else {
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            int32_t acc[4] = {0, 0, 0, 0};
+            imma_ss(acc, tlo0, tlo1, blo[ni]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[ni][e] = red_fast(acc[e], fm);
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const int32_t val = v[s >> 2][s & 3];
+          outw[0][s][u] = put_byte(q == 0 ? 0u : outw[0][s][u], val, q);
+          if (planes == 2) outw[1][s][u] = put_byte(q == 0 ? 0u : outw[1][s][u], limb_hi(val), q);
+        }
+      }
+    }
+    // slot s = 4 ni + e: row j = g + 8 (e >> 1), column i = 8 ni + 2t + (e & 1)
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int e = s & 3, ni = s >> 2;
+      const int j = gq + 8 * (e >> 1), i = 8 * ni + 2 * tq + (e & 1);
+      if (i >= N || j >= N) continue;
+      const int pos = i * N + j;
+      int8_t* dst = V + ((int64_t)tb.plane_base * npos + pos) * g.P * g.Cp + p * g.Cp + c_base;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(outw[0][s][0], outw[0][s][1], outw[0][s][2], outw[0][s][3]);
+      if (planes == 2)
+        *reinterpret_cast<uint4*>(dst + plane_stride) =
+            make_uint4(outw[1][s][0], outw[1][s][1], outw[1][s][2], outw[1][s][3]);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
+                                      cudaStream_t s) {
+  dim3 grid((unsigned)g.P, (g.Cp + kCTAChannels - 1) / kCTAChannels);
+  input_transform_tc_kernel<<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+  return cudaGetLastError();
+}
+
+}  // namespace rnsw

@@ -15,6 +15,12 @@ struct ResidueTables {
   float inv_m;         // 1.0f / modulus
   int32_t r_256;       // 256 mod m (symmetric)
   int32_t r_65536;     // 65536 mod m (symmetric)
+  // Exact division-free symmetric reduction for |x| < 2^28 (see red_fast in
+  // common.cuh): n = x + red_off in [0, 2^30), floor(n/m) = umulhi(n, red_mul) >> red_shift.
+  uint32_t red_mul;
+  int32_t red_shift;
+  int32_t red_off;
+  int32_t half;        // (m - 1) / 2
   int32_t at[RNSW_MAX_N * RNSW_MAX_N];  // AT (M x N), row-major, stride N
   int32_t bt[RNSW_MAX_N * RNSW_MAX_N];  // BT (N x N)
   int32_t g[RNSW_MAX_N * RNSW_MAX_R];   // G  (N x R), stride R
@@ -26,6 +32,7 @@ struct PlanDevice {
   int32_t n;      // N = M + R - 1
   int32_t n_res;
   int32_t n_planes;  // total limb planes over all residues
+  int32_t fast;      // 1: tensor-core transform kernels apply (all m < 6000, D < 2^31)
   int64_t dynamic_range;
   int64_t signed_bound;
   int64_t mrc_inv[RNSW_MAX_RES][RNSW_MAX_RES];  // m_i^-1 mod m_j, i < j

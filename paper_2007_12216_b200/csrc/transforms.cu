@@ -11,6 +11,7 @@
 //   V  [plane][pos][P][Cp]      P = B*th*tw tiles, tile p = (b*th + ti)*tw + tj
 //   Mw [P][res][pos][Kp] int16  GEMM output, symmetric residues
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -277,6 +278,15 @@ __global__ void requant_pool_kernel(const int32_t* __restrict__ y, int B, int H,
   }
 }
 
+bool force_generic() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RNSW_FORCE_GENERIC");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int grid_for(int64_t total, int threads) {
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 32) blocks = 148 * 32;
@@ -302,6 +312,7 @@ cudaError_t launch_filter_import(const PlanHost& plan, int res, const int16_t* u
 
 cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                    cudaStream_t s) {
+  if (plan.dev.fast && !force_generic()) return launch_input_transform_tc(plan, g, x, V, s);
   const int npos = plan.dev.n * plan.dev.n;
   const size_t smem = (size_t)(2 * npos * kChanBlock + plan.dev.n_res * npos) * sizeof(int32_t);
   static bool attr_set = false;
@@ -316,6 +327,7 @@ cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, cons
 
 cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
                                     int16_t* y_res, cudaStream_t s) {
+  if (plan.dev.fast && !force_generic()) return launch_output_transform_tc(plan, g, Mw, y, y_res, s);
   const int N = plan.dev.n, M = plan.dev.m_out, nres = plan.dev.n_res;
   const size_t smem =
       (size_t)(nres * N * N * kChanBlock + N * M * kChanBlock + nres * M * M * kChanBlock + nres * M * N) *
