@@ -190,7 +190,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
   d.n_planes = plane;
   {
     bool fast = d.dynamic_range < (1LL << 31);
-    for (int i = 0; i < n_res; ++i) fast = fast && moduli[i] < 6000;
+    for (int i = 0; i < n_res; ++i) fast = fast && moduli[i] < 4500;  // keeps every limb recombination below 2^28
     d.fast = fast ? 1 : 0;
   }
   d.signed_bound = (d.dynamic_range - 1) / 2;

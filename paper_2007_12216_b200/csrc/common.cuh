@@ -62,6 +62,19 @@ RNSW_DEV int32_t red_fast(int32_t x, const FastMod& f) {
   return (int32_t)(n - q * (uint32_t)f.m) - f.h;
 }
 
+// Non-negative representative in [0, m) of n - f.off + (f.off - f.h)... i.e.
+// red_pos_biased(n) = (x mod m) when n = x + m*L with L = ceil(2^28/m) (see
+// pos_bias).  The bias can be pre-loaded into an MMA accumulator so the
+// reduction is IMAD.HI + SHF + IMAD only.
+RNSW_DEV int32_t pos_bias(const FastMod& f) { return f.off - f.h; }
+
+RNSW_DEV int32_t red_pos_biased(int32_t n, const FastMod& f) {
+  const uint32_t q = __umulhi((uint32_t)n, f.mul) >> f.shift;
+  return (int32_t)((uint32_t)n - q * (uint32_t)f.m);
+}
+
+RNSW_DEV int32_t red_pos(int32_t x, const FastMod& f) { return red_pos_biased(x + pos_bias(f), f); }
+
 // 64-bit exact symmetric reduction (used for the mixed-radix digits).
 RNSW_DEV int64_t sym_mod64(int64_t x, int64_t m) {
   int64_t r = x % m;
@@ -206,6 +219,13 @@ __host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n) {
 RNSW_DEV void imma_ss(int32_t (&c)[4], uint32_t a0, uint32_t a1, uint32_t b) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(b));
+}
+
+RNSW_DEV void imma_us(int32_t (&c)[4], uint32_t a0, uint32_t a1, uint32_t b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a0), "r"(a1), "r"(b));
 }

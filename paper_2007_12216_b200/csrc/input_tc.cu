@@ -12,7 +12,7 @@
 // Each lane ends up holding 8 transform positions x 16 channels, i.e. one
 // 16-byte row segment of V per position and plane, stored with one vector
 // store.  16-bit moduli: BT and T are split into two s8 limbs; the exact
-// int32 recombination stays below 2^28 (m < 6000) so one division-free
+// int32 recombination stays below 2^28 (m < 4500) so one division-free
 // reduction per value suffices.
 #include "common.cuh"
 #include "kernels.h"

@@ -32,7 +32,7 @@ struct PlanDevice {
   int32_t n;      // N = M + R - 1
   int32_t n_res;
   int32_t n_planes;  // total limb planes over all residues
-  int32_t fast;      // 1: tensor-core transform kernels apply (all m < 6000, D < 2^31)
+  int32_t fast;      // 1: tensor-core transform kernels apply (all m < 4500, D < 2^31)
   int64_t dynamic_range;
   int64_t signed_bound;
   int64_t mrc_inv[RNSW_MAX_RES][RNSW_MAX_RES];  // m_i^-1 mod m_j, i < j
