@@ -15,7 +15,7 @@ import numpy as np
 
 from .errors import raise_for
 
-_LIB_PATH = Path(__file__).resolve().parent / "librnsw.so"
+_LIB_PATH = Path(os.environ.get("RNSW_LIB") or Path(__file__).resolve().parent / "librnsw.so")
 _lock = threading.Lock()
 _lib = None
 

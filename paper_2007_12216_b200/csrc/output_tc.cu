@@ -51,18 +51,31 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
     __syncthreads();
   }
   // stage: 16 B (8 channels) per load, 4 loads per (res, pos) row segment;
-  // idx walks the padded 16x16 grid so all index math is shifts
-  for (int idx = tid; idx < nres * 1024; idx += blockDim.x) {
-    const int kc = idx & 3, j = (idx >> 2) & 15, i = (idx >> 6) & 15, r = idx >> 10;
-    if (i >= N || j >= N) continue;
-    int4 v = make_int4(0, 0, 0, 0);
-    if (k0 + 8 * kc < g.Kp)
-      v = __ldg(reinterpret_cast<const int4*>(Mw + ((p * nres + r) * npos + i * N + j) * (int64_t)g.Kp + k0 +
-                                              8 * kc));
-    const int16_t* e = reinterpret_cast<const int16_t*>(&v);
-    int16_t* dst = S + (r * kKB + 8 * kc) * kRowS + stage_off(i, j);
+  // idx walks the padded 16x16 grid so all index math is shifts.  Each
+  // thread issues its loads in batches of 8 before the transposing stores,
+  // so the global latency is paid once per batch, not once per load.
+  constexpr int kBatch = 8;
+  for (int base = tid; base < nres * 1024; base += kBatch * 128) {
+    int4 v[kBatch];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) dst[q * kRowS] = e[q];
+    for (int u = 0; u < kBatch; ++u) {
+      const int idx = base + u * 128;
+      const int kc = idx & 3, j = (idx >> 2) & 15, i = (idx >> 6) & 15, r = idx >> 10;
+      v[u] = make_int4(0, 0, 0, 0);
+      if (idx < nres * 1024 && i < N && j < N && k0 + 8 * kc < g.Kp)
+        v[u] = __ldg(reinterpret_cast<const int4*>(Mw + ((p * nres + r) * npos + i * N + j) * (int64_t)g.Kp + k0 +
+                                                   8 * kc));
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int idx = base + u * 128;
+      const int kc = idx & 3, j = (idx >> 2) & 15, i = (idx >> 6) & 15, r = idx >> 10;
+      if (idx >= nres * 1024 || i >= N || j >= N) continue;
+      const int16_t* e = reinterpret_cast<const int16_t*>(&v[u]);
+      int16_t* dst = S + (r * kKB + 8 * kc) * kRowS + stage_off(i, j);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[q * kRowS] = e[q];
+    }
   }
   __syncthreads();
 
@@ -76,8 +89,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
   int32_t minv[NRES][NRES];
 #pragma unroll
   for (int r = 0; r < NRES; ++r) {
-    if (r >= nres) break;
-    fmr[r] = fast_mod_of(plan->res[r]);
+        fmr[r] = fast_mod_of(plan->res[r]);
     plr[r] = plan->res[r].planes;
 #pragma unroll
     for (int i2 = 0; i2 < NRES; ++i2) minv[r][i2] = i2 < r ? (int32_t)plan->mrc_inv[r][i2] : 0;
@@ -101,13 +113,27 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
   const int ti = (int)((p / g.tw) % g.th);
   const int tj = (int)(p % g.tw);
   const int b_lo = gq, b_hi = gq + 8;  // pass-2 C rows = output column offset b
+  // Output addressing is fixed per lane: slot q -> pixel (a, b).  Precompute
+  // the element offset of channel k0 for each slot (-1: outside the output).
+  int64_t out_off[8];
+  int64_t kstride = g.layout == 0 ? 1 : (int64_t)g.Ho * g.Wo;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
+    const int b = (q & 2) ? b_hi : b_lo;
+    const int ho = ti * M + a, wo = tj * M + b;
+    out_off[q] = -1;
+    if (a < M && b < M && ho < g.Ho && wo < g.Wo)
+      out_off[q] = g.layout == 0 ? (((int64_t)b_img * g.Ho + ho) * g.Wo + wo) * g.K + k0
+                                 : (((int64_t)b_img * g.K + k0) * g.Ho + ho) * g.Wo + wo;
+  }
   for (int kk = 0; kk < kKB / 4; ++kk) {
     const int k = warp * (kKB / 4) + kk;
+    const bool kvalid = k0 + k < g.K;
     int32_t yv[NRES][8];
 #pragma unroll
     for (int r = 0; r < NRES; ++r) {
-      if (r >= nres) break;
-      const int16_t* row = S + (r * kKB + k) * kRowS;
+            const int16_t* row = S + (r * kKB + k) * kRowS;
       const FastMod fm = fmr[r];
       int32_t z[2][4];
       if (plr[r] == 2) {
@@ -176,44 +202,35 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
     // yv[r][4*na + e]: a = 8*na + 2t + (e & 1), b = g + 8*(e >> 1)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
-      const int b = (q & 2) ? b_hi : b_lo;
-      if (a >= M || b >= M) continue;
       if (y_res != nullptr) {
-        if (k0 + k < g.K) {
+        const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
+        const int b = (q & 2) ? b_hi : b_lo;
+        if (a < M && b < M && k0 + k < g.K) {
 #pragma unroll
-          for (int r = 0; r < NRES; ++r)
-            if (r < nres) {
-              const int32_t v = yv[r][q] > fmr[r].h ? yv[r][q] - fmr[r].m : yv[r][q];
-              y_res[(((int64_t)r * g.P + p) * g.K + k0 + k) * M * M + a * M + b] = (int16_t)v;
-            }
+          for (int r = 0; r < NRES; ++r) {
+            const int32_t v = yv[r][q] > fmr[r].h ? yv[r][q] - fmr[r].m : yv[r][q];
+            y_res[(((int64_t)r * g.P + p) * g.K + k0 + k) * M * M + a * M + b] = (int16_t)v;
+          }
         }
-        continue;
-      }
-      // mixed-radix reconstruction (rw/residue.py:195-206), exact in int32 for D < 2^31
-      // digits in [0, m_j): yv already holds y mod m_j in [0, m_j)
-      int32_t d[NRES];
-      d[0] = yv[0][q];
-      uint32_t x = (uint32_t)d[0], radix = (uint32_t)fmr[0].m;
+      } else {
+        // mixed-radix reconstruction (rw/residue.py:195-206) from digits in
+        // [0, m_j) (yv holds y mod m_j), exact in uint32 for D < 2^31
+        uint32_t x = (uint32_t)yv[0][q], radix = (uint32_t)fmr[0].m;
+        int32_t d[NRES];
+        d[0] = yv[0][q];
 #pragma unroll
-      for (int j = 1; j < NRES; ++j) {
-        if (j >= nres) break;
-        int32_t t = yv[j][q];
+        for (int j = 1; j < NRES; ++j) {
+          int32_t t = yv[j][q];
 #pragma unroll
-        for (int i2 = 0; i2 < j; ++i2) t = red_pos((t - d[i2]) * minv[j][i2], fmr[j]);
-        d[j] = t;
-        x += radix * (uint32_t)d[j];
-        radix *= (uint32_t)fmr[j].m;
-      }
-      int64_t v = (int64_t)x;
-      if (v > signed_bound) v -= dyn_range;
-      // direct store: over this warp's 8 channels each pixel receives one
-      // complete 32-byte sector (NHWC), merged in L2
-      const int ho = ti * M + a, wo = tj * M + b;
-      if (ho < g.Ho && wo < g.Wo && k0 + k < g.K) {
-        const int64_t yi = g.layout == 0 ? (((int64_t)b_img * g.Ho + ho) * g.Wo + wo) * g.K + k0 + k
-                                         : (((int64_t)b_img * g.K + k0 + k) * g.Ho + ho) * g.Wo + wo;
-        y[yi] = (int32_t)v;
+          for (int i2 = 0; i2 < j; ++i2) t = red_pos((t - d[i2]) * minv[j][i2], fmr[j]);
+          d[j] = t;
+          x += radix * (uint32_t)t;
+          radix *= (uint32_t)fmr[j].m;
+        }
+        const int32_t v = (int64_t)x > signed_bound ? (int32_t)((int64_t)x - dyn_range) : (int32_t)x;
+        // direct store: over this warp's 8 channels each pixel receives one
+        // complete 32-byte sector (NHWC), merged in L2
+        if (out_off[q] >= 0 && kvalid) y[out_off[q] + k * kstride] = v;
       }
     }
   }
