@@ -287,6 +287,36 @@ bool force_generic() {
   return v == 1;
 }
 
+// Vectorised glue for C % 4 == 0: four channels per thread (int4 loads,
+// one 32-bit store of four int8).
+__global__ void requant_pool_vec4_kernel(const int4* __restrict__ y, int B, int H, int W, int C4, int shift,
+                                         int pool, uint32_t* __restrict__ out) {
+  const int Ho = pool ? H / 2 : H, Wo = pool ? W / 2 : W;
+  const int64_t total = (int64_t)B * Ho * Wo * C4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = (int)(e % C4);
+    int64_t r = e / C4;
+    const int wo = (int)(r % Wo);
+    r /= Wo;
+    const int ho = (int)(r % Ho);
+    const int b = (int)(r / Ho);
+    int4 v;
+    if (pool) {
+      const int64_t base = (((int64_t)b * H + 2 * ho) * W + 2 * wo) * C4 + c4;
+      const int4 a0 = __ldg(y + base), a1 = __ldg(y + base + C4);
+      const int4 a2 = __ldg(y + base + (int64_t)W * C4), a3 = __ldg(y + base + (int64_t)W * C4 + C4);
+      v.x = max(max(a0.x, a1.x), max(a2.x, a3.x));
+      v.y = max(max(a0.y, a1.y), max(a2.y, a3.y));
+      v.z = max(max(a0.z, a1.z), max(a2.z, a3.z));
+      v.w = max(max(a0.w, a1.w), max(a2.w, a3.w));
+    } else {
+      v = __ldg(y + (((int64_t)b * H + ho) * W + wo) * C4 + c4);
+    }
+    auto q = [shift](int32_t t) -> uint32_t { return (uint32_t)min(t > 0 ? t >> shift : 0, 127); };
+    out[e] = q(v.x) | (q(v.y) << 8) | (q(v.z) << 16) | (q(v.w) << 24);
+  }
+}
+
 int grid_for(int64_t total, int threads) {
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 32) blocks = 148 * 32;
@@ -350,6 +380,12 @@ cudaError_t launch_mrc(const PlanHost& plan, const int16_t* residues, int64_t co
 cudaError_t launch_requant_pool(const int32_t* y, int B, int H, int W, int C, int shift, int pool, int8_t* out,
                                 cudaStream_t s) {
   const int64_t total = (int64_t)B * (pool ? H / 2 : H) * (pool ? W / 2 : W) * C;
+  if ((C & 3) == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
+    requant_pool_vec4_kernel<<<grid_for(total / 4, 256), 256, 0, s>>>(reinterpret_cast<const int4*>(y), B, H, W,
+                                                                      C / 4, shift, pool,
+                                                                      reinterpret_cast<uint32_t*>(out));
+    return cudaGetLastError();
+  }
   requant_pool_kernel<<<grid_for(total, 256), 256, 0, s>>>(y, B, H, W, C, shift, pool, out);
   return cudaGetLastError();
 }
