@@ -245,6 +245,7 @@ def run_gpu_arm(args):
     import torch
     import torch.distributed as dist
 
+    from paper_2007_12216_b200 import parallel
     from paper_2007_12216_b200 import workloads as W
     from paper_2007_12216_b200.vgg import VGG16Rns
 
@@ -252,22 +253,16 @@ def run_gpu_arm(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.batch % world:
-        raise SystemExit(f"--batch {args.batch} must be divisible by {world} ranks")
-    shard = args.batch // world
+    start, shard = parallel.shard_range(args.batch, world, rank)
     net = VGG16Rns()
-    x_host = W.vgg16_images(shard, start=rank * shard)
+    x_host = W.vgg16_images(shard, start=start)
     x_pinned = torch.from_numpy(x_host).pin_memory()
     x_dev = x_pinned.cuda()
     gathered = torch.empty((args.batch, 7, 7, 512), dtype=torch.int8, device="cuda") if world > 1 else None
     out_pinned = torch.empty((args.batch if rank == 0 else shard, 7, 7, 512), dtype=torch.int8).pin_memory()
 
     def step(x):
-        y = net.forward(x)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, y)
-            return gathered
-        return y
+        return parallel.gather_maps(net.forward(x), world, out=gathered)
 
     def barrier():
         if world > 1:
@@ -293,11 +288,7 @@ def run_gpu_arm(args):
         e1.record()
         torch.cuda.synchronize()
         barrier()
-    elapsed = e0.elapsed_time(e1) / 1e3
-    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed = float(t.item())
+    elapsed = parallel.max_over_ranks(e0.elapsed_time(e1) / 1e3, world, device="cuda")
     total_ops = W.VGGConfig(batch=args.batch).direct_ops() * args.steps
     value = total_ops / elapsed / 1e12
     ms_per_step = elapsed / args.steps * 1e3
@@ -330,11 +321,7 @@ def run_gpu_arm(args):
             out_pinned.copy_(y, non_blocking=True)
     h1.record()
     torch.cuda.synchronize()
-    e2e_elapsed = h0.elapsed_time(h1) / 1e3
-    t = torch.tensor([e2e_elapsed], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_elapsed = float(t.item())
+    e2e_elapsed = parallel.max_over_ranks(h0.elapsed_time(h1) / 1e3, world, device="cuda")
     e2e_value = total_ops / e2e_elapsed / 1e12
     h2d = x_host.nbytes * world
     d2h = out_pinned.numel()

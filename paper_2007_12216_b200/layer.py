@@ -158,16 +158,28 @@ _plans_lock = threading.Lock()
 def plan_for(ts: transforms.ExactTransformSet, system: RnsSystem) -> _native.Plan:
     """Native plan for (transform set, system) on the current CUDA device."""
     torch = _torch()
+    mts = _modular_sets(ts, system)  # NotCoprime surfaces here, before any device work
     dev = torch.cuda.current_device()
     key = (ts.m, ts.r, ts.points, system.moduli, dev)
     plan = _plans.get(key)
     if plan is None:
-        mts = transforms.reduce_for_system(ts, system)  # NotCoprime surfaces here
         plan = plan_from_modular(mts, system)
         with _plans_lock:
             _plans.setdefault(key, plan)
             plan = _plans[key]
     return plan
+
+
+_mts_cache: dict = {}
+
+
+def _modular_sets(ts: transforms.ExactTransformSet, system: RnsSystem):
+    key = (ts.m, ts.r, ts.points, system.moduli)
+    mts = _mts_cache.get(key)
+    if mts is None:
+        mts = transforms.reduce_for_system(ts, system)
+        _mts_cache[key] = mts
+    return mts
 
 
 def plan_from_modular(mts: Sequence[transforms.ModularTransformSet], system: RnsSystem) -> _native.Plan:

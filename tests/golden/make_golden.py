@@ -1,0 +1,195 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container, where the reference package is importable
+read-only (it is absent on the GPU box, so the fixtures are committed):
+
+    PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src \\
+        python tests/golden/make_golden.py
+
+Outputs
+  transforms.json   modular AT/G/BT for every (M, R, modulus) the configs and
+                    parity cases use, plus compatibility flags
+                    (rnswinograd.transforms.reduce_transforms_mod)
+  small_cases.npz   seeded small layers: inputs, reference winograd_layer_conv
+                    and direct_conv outputs, per-stage outputs
+  digests.json      sha256 of inputs / outputs of the full-size BASELINE
+                    configs (1, 3, 5 and VGG16 batch 1, every layer) computed
+                    by the reference
+  scalars.json      known answers: MRC inverses, signed bounds, chunk sizes
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, str(ROOT))
+
+from rnswinograd import gemm, kernel, layer, residue, transforms  # noqa: E402  (the reference)
+
+from paper_2007_12216_b200 import workloads as W  # noqa: E402  (seeded input generation only)
+
+TILES = [(2, 3), (4, 3), (6, 3), (8, 3), (10, 3), (12, 3), (14, 3), (8, 5), (12, 5), (2, 5), (4, 5)]
+MODULI = [251, 241, 239, 253, 247, 4001, 4331, 7, 11, 13]
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def gen_transforms():
+    out = {}
+    for m, r in TILES:
+        ts = transforms.cached_transforms(m, r)
+        for q in MODULI:
+            key = f"F{m}x{r}/{q}"
+            ok = transforms.check_modulus_compatibility(ts, q)
+            ent = {"compatible": bool(ok)}
+            if ok:
+                mt = transforms.reduce_transforms_mod(ts, q)
+                ent.update(at=mt.at.tolist(), g=mt.g.tolist(), bt=mt.bt.tolist(), dtype=str(mt.at.dtype))
+            out[key] = ent
+    return out
+
+
+SMALL = [
+    # name, h, w, c, k, r, pad, batch, tile_m, moduli, value range
+    ("fast1", 8, 8, 3, 5, 3, 1, 2, 4, (251, 241, 239), 128),
+    ("fast2", 16, 16, 4, 3, 5, 2, 1, 12, (4001, 4331), 128),
+    ("fast3", 30, 30, 7, 2, 3, 0, 1, 14, (251, 241, 239), 128),
+    ("fast4", 28, 28, 32, 16, 3, 1, 1, 14, (251, 241, 239), 128),
+    ("fast5", 6, 10, 2, 2, 3, 1, 1, 2, (253, 251, 247), 128),
+    ("cfg1s", 20, 20, 64, 64, 3, 1, 1, 8, (251, 241, 239), 32),
+    ("cfg3s", 15, 13, 24, 40, 5, 2, 2, 8, (251, 241, 239), 16),
+    ("vgg16s", 16, 16, 48, 40, 3, 1, 1, 14, (4001, 4331), 128),
+    ("small7", 9, 9, 5, 3, 3, 1, 1, 4, (7, 11, 13), 4),
+    ("mixed", 12, 12, 12, 20, 3, 1, 1, 10, (251, 4001), 64),
+]
+STAGE_CASES = {"fast1", "fast2", "fast3", "fast5", "small7", "mixed"}  # per-stage arrays kept small
+
+
+def gen_small():
+    arrays = {}
+    meta = []
+    for name, h, w, c, k, r, pad, batch, tm, mods, vr in SMALL:
+        rng = W.make_rng(2020, f"golden/{name}")
+        wt = rng.integers(-vr, vr, (r, r, c, k)).astype(np.int8)
+        x = rng.integers(-vr, vr, (batch, h, w, c)).astype(np.int8)
+        spec = layer.LayerSpec(h=h, w=w, c=c, k=k, r=r, padding=pad, batch=batch, tile_m=tm)
+        system = residue.RnsSystem(mods)
+        direct = layer.direct_conv(spec, wt, x)
+        rns = layer.winograd_layer_conv(spec, wt, x, system, declared_bound=system.signed_bound)
+        arrays[f"{name}/x"] = x
+        arrays[f"{name}/w"] = wt
+        arrays[f"{name}/direct"] = direct
+        arrays[f"{name}/rns"] = rns
+        # per-stage outputs (rw/layer.py:266-298) for every modulus
+        ts = transforms.cached_transforms(tm, r)
+        mts = transforms.reduce_for_system(ts, system)
+        patches, _ = layer.tile_decompose(x, tm, r, pad)
+        filt = layer.precompute_filter_transforms(wt, mts)
+        for mt in (mts if name in STAGE_CASES else ()):
+            mm = mt.modulus
+            d = kernel.residue_encode_array(patches.transpose(0, 1, 2, 5, 3, 4), mm)
+            v = kernel.input_transform_mod(d, mt)
+            n = mt.n
+            p = patches.shape[0] * patches.shape[1] * patches.shape[2]
+            vpos = np.ascontiguousarray(v.transpose(4, 5, 0, 1, 2, 3)).reshape(n * n, p, c)
+            acc = layer._modular_gemm(vpos, filt[mm].reshape(n * n, c, k), mm)
+            prod = np.ascontiguousarray(acc.reshape(n, n, p, k).transpose(2, 3, 0, 1)).astype(
+                gemm.dtype_for_modulus(mm))
+            y = kernel.backward_transform_mod(prod, mt)
+            arrays[f"{name}/{mm}/U"] = filt[mm]
+            arrays[f"{name}/{mm}/V"] = vpos
+            arrays[f"{name}/{mm}/acc"] = acc
+            arrays[f"{name}/{mm}/y"] = y
+        meta.append(dict(name=name, h=h, w=w, c=c, k=k, r=r, pad=pad, batch=batch, tile_m=tm, moduli=list(mods)))
+    return arrays, meta
+
+
+def gen_digests():
+    out = {}
+    t0 = time.time()
+    case, w, x = W.config1()
+    spec = layer.LayerSpec(h=case.h, w=case.w, c=case.c, k=case.k, r=case.r, padding=case.pad, batch=case.batch,
+                           tile_m=case.tile_m)
+    y = layer.winograd_layer_conv(spec, w, x, residue.RnsSystem(case.moduli), declared_bound=case.declared_bound)
+    assert np.array_equal(y, layer.direct_conv(spec, w, x))
+    out["cfg1"] = dict(x=sha(x), w=sha(w), y=sha(y), ysum=int(y.astype(np.int64).sum()))
+    print("cfg1", time.time() - t0, flush=True)
+
+    case, w, x = W.config3()
+    spec = layer.LayerSpec(h=case.h, w=case.w, c=case.c, k=case.k, r=case.r, padding=case.pad, batch=case.batch,
+                           tile_m=case.tile_m)
+    y = layer.winograd_layer_conv(spec, w, x, residue.RnsSystem(case.moduli), declared_bound=case.declared_bound)
+    assert np.array_equal(y, layer.direct_conv(spec, w, x))
+    out["cfg3"] = dict(x=sha(x), w=sha(w), y=sha(y), ysum=int(y.astype(np.int64).sum()))
+    print("cfg3", time.time() - t0, flush=True)
+
+    w, x = W.config5_operands()
+    base = layer.LayerSpec(h=28, w=28, c=256, k=256, r=3, padding=1, batch=32)
+    direct = layer.direct_conv(base, w, x)
+    out["cfg5/direct"] = dict(x=sha(x), w=sha(w), y=sha(direct), ysum=int(direct.astype(np.int64).sum()))
+    for case in W.config5_cases():
+        spec = layer.LayerSpec(h=28, w=28, c=256, k=256, r=3, padding=1, batch=32, tile_m=case.tile_m)
+        y = layer.winograd_layer_conv(spec, w, x, residue.RnsSystem(case.moduli), declared_bound=case.declared_bound)
+        assert np.array_equal(y, direct), case.name
+        out[case.name] = dict(y=sha(y))
+        print(case.name, time.time() - t0, flush=True)
+
+    weights = W.vgg16_weights()
+    bounds = W.vgg16_bounds(weights)
+    x = W.vgg16_images(1)
+    out["vgg16/image0"] = dict(x=sha(x))
+    system = residue.RnsSystem(W.SYS16)
+    for i, ((name, side, c, k, pool), wt) in enumerate(zip(W.VGG16_LAYERS, weights)):
+        spec = layer.LayerSpec(h=side, w=side, c=c, k=k, r=3, padding=1, batch=1, tile_m=14)
+        y = layer.winograd_layer_conv(spec, wt, x, system, declared_bound=bounds[i])
+        d = layer.direct_conv(spec, wt, x)
+        assert np.array_equal(y, d), name
+        out[f"vgg16/{name}"] = dict(w=sha(wt), y=sha(y), bound=bounds[i], max_abs=int(np.abs(d).max()))
+        v = np.clip(np.maximum(y, 0) >> W.VGG16_SHIFTS[i], 0, 127).astype(np.int8)
+        if pool:
+            b, hh, ww, cc = v.shape
+            v = v.reshape(b, hh // 2, 2, ww // 2, 2, cc).max(axis=(2, 4))
+        x = np.ascontiguousarray(v)
+        print(name, time.time() - t0, flush=True)
+    out["vgg16/final"] = dict(y=sha(x))
+    return out
+
+
+def gen_scalars():
+    out = {}
+    for mods in [(251, 241, 239), (253, 251, 247), (4001, 4331), (7, 11, 13), (251, 4001)]:
+        s = residue.RnsSystem(mods)
+        out["x".join(map(str, mods))] = dict(signed_bound=s.signed_bound, dynamic_range=s.dynamic_range,
+                                             mrc_inv=s._mrc_inv)
+    out["accumulation_chunk"] = {str(m): gemm.accumulation_chunk(m) for m in MODULI if m >= 3}
+    out["mod_inverse_14400"] = {str(m): residue.mod_inverse(14400, m) for m in (253, 251, 247)}
+    rng = np.random.default_rng(7)
+    vals = rng.integers(-7_000_000, 7_000_000, 64)
+    s = residue.RnsSystem((251, 241, 239))
+    res = [np.array([residue.mod_reduce(int(v), m) for v in vals]) for m in s.moduli]
+    out["mrc_251x241x239"] = dict(values=vals.tolist(), residues=[r.tolist() for r in res],
+                                  reconstructed=residue.mrc_reconstruct_arrays(res, s).tolist())
+    return out
+
+
+def main():
+    (HERE / "transforms.json").write_text(json.dumps(gen_transforms()))
+    (HERE / "scalars.json").write_text(json.dumps(gen_scalars(), indent=1))
+    arrays, meta = gen_small()
+    np.savez_compressed(HERE / "small_cases.npz", **arrays)
+    (HERE / "small_cases.json").write_text(json.dumps(meta, indent=1))
+    if "--no-digests" not in sys.argv:
+        (HERE / "digests.json").write_text(json.dumps(gen_digests(), indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+"""The reference-facing API on the GPU: operand types, precomputed filters,
+timings, declared-bound wrap semantics, edge geometries and worst-case values.
+Every result is compared with the CPU oracle (reference restatement) and the
+exact direct convolution."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import ref_port as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _rnsw():
+    import paper_2007_12216_b200 as rnsw
+
+    return rnsw
+
+
+def _operands(spec, seed, lo=-128, hi=127):
+    rng = np.random.default_rng(seed)
+    return (rng.integers(lo, hi + 1, spec.weight_shape()).astype(np.int8),
+            rng.integers(lo, hi + 1, spec.input_shape()).astype(np.int8))
+
+
+EDGE = [
+    # h, w, c, k, r, pad, batch, tile_m, moduli
+    (3, 3, 1, 1, 3, 0, 1, 4, (251, 241, 239)),          # single output pixel, tile larger than output
+    (5, 17, 2, 1, 3, 1, 3, 6, (4001, 4331)),            # ragged width, K = 1
+    (7, 7, 17, 33, 5, 2, 2, 12, (4001, 4331)),          # N = 16 with R = 5, odd C and K
+    (33, 31, 64, 48, 3, 1, 5, 8, (253, 251, 247)),      # P not a multiple of 128
+    (14, 14, 512, 16, 3, 1, 1, 14, (4001, 4331)),       # deep C (4 chunks of 128)
+    (9, 9, 130, 300, 3, 1, 1, 10, (251, 241, 239)),     # C -> Cp = 256, K padded to 304
+    (10, 12, 40, 24, 3, 2, 2, 6, (251, 241, 239)),      # padding 2 with R = 3
+    (6, 6, 8, 8, 3, 0, 200, 4, (7, 11, 13)),            # many tiny tiles, tiny moduli
+    (20, 20, 16, 16, 3, 1, 1, 2, (251, 241, 239, 233)), # four residues, F(2,3)
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=lambda c: "x".join(map(str, c[:8])))
+def test_edge_geometries(case):
+    rnsw = _rnsw()
+    h, w, c, k, r, pad, batch, tm, mods = case
+    spec = rnsw.LayerSpec(h=h, w=w, c=c, k=k, r=r, padding=pad, batch=batch, tile_m=tm)
+    system = rnsw.RnsSystem(mods)
+    lo, hi = (-2, 2) if max(mods) < 20 else (-128, 127)
+    wt, x = _operands(spec, h * 7 + c, lo, hi)
+    got = rnsw.winograd_layer_conv(spec, wt, x, system, declared_bound=system.signed_bound)
+    assert np.array_equal(got, O.winograd_layer(x, wt, pad, tm, mods))
+    direct = oracle.direct_conv_c(x, wt, pad)
+    if np.abs(direct.astype(np.int64)).max() <= system.signed_bound:
+        assert np.array_equal(got, direct)
+
+
+def test_worst_case_extremes():
+    """All operands at the int8 extremes -128 / 127 (t/test_kernel.py:191-199)."""
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=12, w=12, c=8, k=4, r=3, padding=1, tile_m=10)
+    for xv, wv in [(-128, 127), (-128, -128), (127, 127)]:
+        x = np.full(spec.input_shape(), xv, np.int8)
+        w = np.full(spec.weight_shape(), wv, np.int8)
+        system = rnsw.RnsSystem((4001, 4331))
+        got = rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=9 * 8 * 128 * 128)
+        assert np.array_equal(got, oracle.direct_conv_c(x, w, 1))
+
+
+def test_declared_bound_wraps_like_the_reference():
+    """A false declared bound wraps modulo D exactly as the reference does
+    (SURVEY.md finding 3): same output as the reference path, congruent to
+    direct conv, not equal to it."""
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=8, w=8, c=64, k=8, r=3, padding=1, tile_m=4)
+    w, x = _operands(spec, 3)
+    system = rnsw.RnsSystem((7, 11, 13))
+    got = rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=100)
+    assert np.array_equal(got, O.winograd_layer(x, w, 1, 4, (7, 11, 13)))
+    direct = oracle.direct_conv_c(x, w, 1).astype(np.int64)
+    assert np.all((direct - got) % 1001 == 0) and not np.array_equal(got, direct)
+
+
+def test_declared_bound_at_512_channels():
+    # t/test_layer.py:181-194: ternary weights keep |y| < 300000 at C = 512
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=6, w=6, c=512, k=4, r=3, padding=1, tile_m=4)
+    rng = np.random.default_rng(512)
+    w = rng.integers(-1, 2, spec.weight_shape()).astype(np.int8)
+    x = rng.integers(-128, 128, spec.input_shape()).astype(np.int8)
+    sys8 = rnsw.RnsSystem((251, 241, 239))
+    with pytest.raises(rnsw.DynamicRangeExceeded):
+        rnsw.winograd_layer_conv(spec, w, x, sys8)
+    got = rnsw.winograd_layer_conv(spec, w, x, sys8, declared_bound=300_000)
+    assert np.array_equal(got, oracle.direct_conv_c(x, w, 1))
+
+
+def test_precomputed_filters_all_forms():
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=12, w=12, c=3, k=4, r=3, padding=1, tile_m=4)
+    w, x = _operands(spec, 4)
+    system = rnsw.RnsSystem((251, 241, 239))
+    mts = rnsw.reduce_for_system(rnsw.cached_transforms(4, 3), system)
+    bank = rnsw.precompute_filter_transforms(w, mts)
+    assert sorted(bank) == sorted(system.moduli) and bank[251].shape == (6, 6, 3, 4)
+    ref_bank = O.filter_bank(w, {m: O.modular_matrices(4, 3, m) for m in system.moduli})
+    for m in system.moduli:
+        assert np.array_equal(bank[m], ref_bank[m])
+    base = rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=system.signed_bound)
+    for filt in (bank, ref_bank, {m: v.astype(np.int16) for m, v in ref_bank.items()}):
+        got = rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=system.signed_bound, filters=filt)
+        assert np.array_equal(got, base)
+    with pytest.raises(rnsw.ShapeMismatch):
+        rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=system.signed_bound, filters={251: bank[251]})
+    with pytest.raises(rnsw.ShapeMismatch):
+        rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=system.signed_bound,
+                                 filters={m: f[:, :, :2] for m, f in ref_bank.items()})
+
+
+def test_torch_operands_stay_on_device_and_timings():
+    import torch
+
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=28, w=28, c=32, k=32, r=3, padding=1, tile_m=14, batch=2)
+    w, x = _operands(spec, 9)
+    system = rnsw.RnsSystem((4001, 4331))
+    t = rnsw.StageTimings()
+    y = rnsw.winograd_layer_conv(spec, torch.from_numpy(w).cuda(), torch.from_numpy(x).cuda(), system,
+                                 declared_bound=system.signed_bound, timings=t)
+    assert isinstance(y, torch.Tensor) and y.is_cuda and y.dtype == torch.int32
+    assert t.input_transform > 0 and t.gemm > 0 and t.backward_transform > 0
+    assert np.array_equal(y.cpu().numpy(), oracle.direct_conv_c(x, w, 1))
+
+
+def test_errors_are_raised_before_device_work():
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=8, w=8, c=2, k=2, r=3, padding=1, tile_m=4)
+    w, x = _operands(spec, 1)
+    sys8 = rnsw.RnsSystem((251, 241, 239))
+    with pytest.raises(rnsw.ShapeMismatch):
+        rnsw.winograd_layer_conv(spec, w, x[:, :, :5], sys8)
+    with pytest.raises(rnsw.UnsupportedStride):
+        rnsw.winograd_layer_conv(rnsw.LayerSpec(h=8, w=8, c=2, k=2, r=3, padding=1, stride=2, tile_m=4), w, x, sys8)
+    with pytest.raises(rnsw.DeviceError):
+        # F(14,5): tile side 18 is outside the device path (N <= 16)
+        s18 = rnsw.LayerSpec(h=20, w=20, c=2, k=2, r=5, padding=2, tile_m=14)
+        w18, x18 = _operands(s18, 2)
+        rnsw.winograd_layer_conv(s18, w18, x18, rnsw.RnsSystem((4001, 4331)), declared_bound=1000)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_geometry_sweep(seed):
+    rnsw = _rnsw()
+    rng = np.random.default_rng(100 + seed)
+    r = int(rng.choice([3, 5]))
+    tm = int(rng.choice([t for t in (2, 4, 6, 8, 10, 12, 14) if t + r - 1 <= 16]))
+    mods = [(251, 241, 239), (4001, 4331), (253, 251, 247)][seed % 3]
+    if tm + r - 1 > 12 and mods == (253, 251, 247):
+        mods = (251, 241, 239)
+    spec = rnsw.LayerSpec(h=int(rng.integers(r, 40)), w=int(rng.integers(r, 40)), c=int(rng.integers(1, 200)),
+                          k=int(rng.integers(1, 150)), r=r, padding=int(rng.integers(0, r)), tile_m=tm,
+                          batch=int(rng.integers(1, 4)))
+    w, x = _operands(spec, seed, -20, 20)
+    system = rnsw.RnsSystem(mods)
+    got = rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=system.signed_bound)
+    assert np.array_equal(got, oracle.direct_conv_c(x, w, spec.padding))

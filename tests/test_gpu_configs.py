@@ -1,0 +1,93 @@
+"""Full-size BASELINE configs on the GPU, bit-exact against the reference:
+output digests were computed by rnswinograd.winograd_layer_conv (and checked
+equal to direct_conv) in tests/golden/make_golden.py."""
+import numpy as np
+import pytest
+
+import oracle
+from golden_util import digests, sha
+
+pytestmark = pytest.mark.gpu
+
+
+def _rnsw():
+    import paper_2007_12216_b200 as rnsw
+
+    return rnsw
+
+
+def _run(case, w, x, layout="nhwc"):
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=case.h, w=case.w, c=case.c, k=case.k, r=case.r, padding=case.pad, batch=case.batch,
+                          tile_m=case.tile_m)
+    return rnsw.winograd_layer_conv(spec, w, x, rnsw.RnsSystem(case.moduli), declared_bound=case.declared_bound)
+
+
+def test_config1_bit_exact():
+    from paper_2007_12216_b200 import workloads as W
+
+    case, w, x = W.config1()
+    y = _run(case, w, x)
+    assert sha(y) == digests()["cfg1"]["y"]
+    assert np.array_equal(y, oracle.direct_conv_c(x, w, case.pad))
+
+
+def test_config1_nchw_front_door():
+    from paper_2007_12216_b200 import workloads as W
+
+    rnsw = _rnsw()
+    case, w, x = W.config1()
+    y = rnsw.conv2d_rns(np.ascontiguousarray(x.transpose(0, 3, 1, 2)), np.ascontiguousarray(w.transpose(3, 2, 0, 1)),
+                        case.moduli, case.tile_m, case.pad, declared_bound=case.declared_bound)
+    assert sha(np.ascontiguousarray(y.transpose(0, 2, 3, 1))) == digests()["cfg1"]["y"]
+
+
+def test_config3_bit_exact():
+    from paper_2007_12216_b200 import workloads as W
+
+    case, w, x = W.config3()
+    y = _run(case, w, x)
+    assert sha(y) == digests()["cfg3"]["y"]
+    assert np.array_equal(y, oracle.direct_conv_c(x, w, case.pad))
+
+
+@pytest.mark.parametrize("idx", range(13))
+def test_config5_sweep_bit_exact(idx):
+    from paper_2007_12216_b200 import workloads as W
+
+    case = W.config5_cases()[idx]
+    w, x = W.config5_operands()
+    y = _run(case, w, x)
+    d = digests()
+    assert sha(y) == d[case.name]["y"] == d["cfg5/direct"]["y"], case.name
+
+
+def test_vgg16_batch1_every_layer_bit_exact():
+    """Config 2: all 13 layers' int32 outputs and the final map match the
+    reference RNS path (and direct conv) byte for byte."""
+    import torch
+    from paper_2007_12216_b200 import workloads as W
+    from paper_2007_12216_b200.vgg import VGG16Rns
+
+    net = VGG16Rns()
+    x = torch.from_numpy(W.vgg16_images(1)).cuda()
+    final, outs = net.forward(x, keep_int32=True)
+    d = digests()
+    for (name, *_), y in zip(W.VGG16_LAYERS, outs):
+        assert sha(y.cpu().numpy()) == d[f"vgg16/{name}"]["y"], name
+    assert sha(final.cpu().numpy()) == d["vgg16/final"]["y"]
+
+
+def test_vgg16_batch4_matches_per_image_runs():
+    import torch
+    from paper_2007_12216_b200 import workloads as W
+    from paper_2007_12216_b200.vgg import VGG16Rns
+
+    net = VGG16Rns()
+    xb = torch.from_numpy(W.vgg16_images(4)).cuda()
+    full = net.forward(xb).cpu().numpy()
+    for i in range(4):
+        one = net.forward(torch.from_numpy(W.vgg16_images(1, start=i)).cuda()).cpu().numpy()
+        assert np.array_equal(full[i:i + 1], one)
+    staged = net.forward_staged(xb, lambda *a: None).cpu().numpy()
+    assert np.array_equal(staged, full)
