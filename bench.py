@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--impl", default="rnsw", choices=["rnsw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-images", type=int, default=1)
+    ap.add_argument("--unfused", action="store_true",
+                    help="materialise every layer's int32 output and run the glue as a separate kernel")
     return ap.parse_args()
 
 
@@ -261,8 +263,11 @@ def run_gpu_arm(args):
     gathered = torch.empty((args.batch, 7, 7, 512), dtype=torch.int8, device="cuda") if world > 1 else None
     out_pinned = torch.empty((args.batch if rank == 0 else shard, 7, 7, 512), dtype=torch.int8).pin_memory()
 
+    fwd = net.forward if args.unfused else net.forward_fused
+    fwd_staged = net.forward_staged if args.unfused else net.forward_fused_staged
+
     def step(x):
-        return parallel.gather_maps(net.forward(x), world, out=gathered)
+        return parallel.gather_maps(fwd(x), world, out=gathered)
 
     def barrier():
         if world > 1:
@@ -297,7 +302,7 @@ def run_gpu_arm(args):
     rec = []
     torch.cuda.synchronize()
     for _ in range(args.steps):
-        net.forward_staged(x_dev, lambda kind, i, a, b: rec.append((kind, i, a, b)))
+        fwd_staged(x_dev, lambda kind, i, a, b: rec.append((kind, i, a, b)))
     torch.cuda.synchronize()
     per_kind, per_layer = {}, {}
     for kind, i, a, b in rec:
@@ -305,7 +310,7 @@ def run_gpu_arm(args):
         per_kind[kind] = per_kind.get(kind, 0.0) + dt
         per_layer.setdefault(i, {}).setdefault(kind, 0.0)
         per_layer[i][kind] += dt
-    work = net.layer_work(shard)
+    work = net.layer_work(shard, fused=not args.unfused)
     stage_sum = sum(per_kind.values())
     dominant = max(per_kind, key=per_kind.get)
 
@@ -370,13 +375,15 @@ def run_gpu_arm(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded PCG64 images U{0..127}, weights round(N(0,20^2)) clipped; no dataset)",
         "config": {"workload": f"BASELINE config 4: VGG16 13x conv3x3 stack, 224x224x3, batch {args.batch} "
-                               f"sharded {shard}/rank, F(14x14,3x3), RNS(4001,4331), relu/shift/maxpool glue",
+                               f"sharded {shard}/rank, F(14x14,3x3), RNS(4001,4331), relu/shift/maxpool glue "
+                               + ("as a separate kernel (int32 outputs materialised)" if args.unfused else
+                                  "fused into each layer's output stage"),
                    "global_batch": args.batch, "per_rank_batch": shard, "tile": "F(14x14,3x3)",
                    "moduli": [4001, 4331], "parallelism": f"image-sharded x{world}, one all-gather at the end",
                    "l2": "inputs and intermediates larger than L2 (126 MB)",
                    "layer_ms": layer_ms},
         "stages": stages,
-        "gpu_launches": net.launches_per_forward() * args.steps,
+        "gpu_launches": (net.launches_per_forward() if args.unfused else 3 * len(W.VGG16_LAYERS)) * args.steps,
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(e2e_elapsed / args.steps * 1e3, 3)},
         "roofline": roof,

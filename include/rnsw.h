@@ -109,6 +109,19 @@ int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int 
                       int pad, int layout, const void* U, int32_t* y, void* workspace,
                       size_t workspace_bytes, void* stream);
 
+/* Whole layer with the VGG16-stack glue fused into the output stage:
+ * relu, >> shift, clip to [0,127], optional 2x2 max-pool (even tile_m),
+ * written as int8 NHWC (B, Ho[/2], Wo[/2], K) -- the int32 output is never
+ * materialised.  Not part of the reference package (BASELINE.json configs
+ * 2/4 define the glue); equals rnsw_conv_forward followed by
+ * rnsw_requant_pool.  NHWC only; K % 4 == 0; moduli < 4500. */
+int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K,
+                              int pad, const void* U, int shift, int pool, int8_t* out, void* workspace,
+                              size_t workspace_bytes, void* stream);
+/* Stage 3 with the fused glue (Mw from rnsw_winograd_gemm). */
+int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, int H, int W, int K, int pad,
+                                  int shift, int pool, int8_t* out, void* stream);
+
 /* Vectorised MRC of n_res residue arrays ([n_res][count] int16, any congruent
  * representatives) into signed int64. */
 int rnsw_mrc_reconstruct(const rnsw_plan* plan, const int16_t* residues, int64_t count,

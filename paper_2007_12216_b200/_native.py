@@ -44,6 +44,10 @@ _SIGNATURES = {
     "rnsw_output_residues": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "rnsw_conv_forward": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                   c_void_p, c_void_p, c_size_t, c_void_p]),
+    "rnsw_conv_forward_requant": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                          c_int, c_int, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "rnsw_output_transform_requant": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                              c_void_p, c_void_p]),
     "rnsw_mrc_reconstruct": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "rnsw_requant_pool": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "rnsw_error_string": (ctypes.c_char_p, [c_int]),

@@ -352,6 +352,48 @@ int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int 
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform");
 }
 
+int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
+                              const void* U, int shift, int pool, int8_t* out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (x == nullptr || U == nullptr || out == nullptr || workspace == nullptr)
+    return fail(RNSW_ERR_INVALID, "null buffer");
+  if (shift < 0 || shift > 31) return fail(RNSW_ERR_INVALID, "shift must be in [0, 31]");
+  if (!plan->host.dev.fast)
+    return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs the tensor-core transform path (moduli < 4500)");
+  if ((K & 3) != 0) return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs K %% 4 == 0");
+  if (pool && (plan->host.dev.m_out & 1)) return fail(RNSW_ERR_UNSUPPORTED, "fused 2x2 pooling needs an even tile_m");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, C, K, pad, RNSW_LAYOUT_NHWC, &g)) return rc;
+  if (pool && (g.Ho < 2 || g.Wo < 2)) return fail(RNSW_ERR_SHAPE, "pooling needs Ho, Wo >= 2");
+  const PlanDevice& d = plan->host.dev;
+  const size_t vb = round_up(v_bytes(d, g.P, g.Cp), 256);
+  const size_t mb = m_bytes(d, g.P, g.Kp);
+  if (workspace_bytes < vb + mb) return fail(RNSW_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, vb + mb);
+  int8_t* V = static_cast<int8_t*>(workspace);
+  int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = rnsw::launch_input_transform(plan->host, g, x, V, s);
+  if (e != cudaSuccess) return cuda_fail(e, "input_transform");
+  e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, K, g.Kp, g.bc, Mw, s);
+  if (e != cudaSuccess) return cuda_fail(e, "winograd_gemm");
+  e = rnsw::launch_output_transform_tc(plan->host, g, Mw, nullptr, nullptr, s, out, shift, pool);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant");
+}
+
+int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, int H, int W, int K, int pad,
+                                  int shift, int pool, int8_t* out, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (Mw == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (!plan->host.dev.fast || (K & 3) != 0 || (pool && (plan->host.dev.m_out & 1)))
+    return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation not available for this plan/geometry");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, 1, K, pad, RNSW_LAYOUT_NHWC, &g)) return rc;
+  cudaError_t e = rnsw::launch_output_transform_tc(plan->host, g, static_cast<const int16_t*>(Mw), nullptr, nullptr,
+                                                   (cudaStream_t)stream, out, shift, pool);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant");
+}
+
 int rnsw_mrc_reconstruct(const rnsw_plan* plan, const int16_t* residues, int64_t count, int64_t* out, void* stream) {
   if (int rc = check_plan(plan)) return rc;
   if (residues == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");

@@ -46,8 +46,9 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
   __shared__ int32_t BT16[RNSW_MAX_RES * 256];
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = plan->n_res;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-  const int64_t p = blockIdx.x;
-  const int c_base = blockIdx.y * kCTAChannels + warp * 16;
+  const int ncb = (g.Cp + kCTAChannels - 1) / kCTAChannels;
+  const int64_t p = blockIdx.x / ncb;  // channel blocks of one tile are adjacent in launch order
+  const int c_base = (int)(blockIdx.x % ncb) * kCTAChannels + warp * 16;
   for (int idx = tid; idx < nres * 256; idx += blockDim.x) {
     const int r = idx >> 8, a = (idx >> 4) & 15, b = idx & 15;
     BT16[idx] = (a < N && b < N) ? plan->res[r].bt[a * RNSW_MAX_N + b] : 0;
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
 
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s) {
-  dim3 grid((unsigned)g.P, (g.Cp + kCTAChannels - 1) / kCTAChannels);
+  dim3 grid((unsigned)(g.P * ((g.Cp + kCTAChannels - 1) / kCTAChannels)));
   input_transform_tc_kernel<<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
   return cudaGetLastError();
 }

@@ -36,7 +36,8 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
 cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
                                     int16_t* y_res, cudaStream_t s);
 cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
-                                       int16_t* y_res, cudaStream_t s);
+                                       int16_t* y_res, cudaStream_t s, int8_t* out8 = nullptr, int shift = 0,
+                                       int pool = 0);
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s);
 cudaError_t launch_mrc(const PlanHost& plan, const int16_t* residues, int64_t count, int64_t* out,

@@ -27,16 +27,26 @@ constexpr int kKB = 32;       // output channels per CTA
 constexpr int kRowS = 266;    // int16 per staged row
 RNSW_DEV int stage_off(int i, int j) { return 16 * i + 2 * (i >> 2) + j; }
 
-template <int NRES>
+// Fused requantisation epilogue (VGG16 stack glue, BASELINE configs 2/4):
+// relu -> >> shift -> clip [0,127] (-> 2x2 max-pool inside the tile) written
+// as int8 NHWC instead of the int32 output.
+struct Requant {
+  int8_t* out;  // nullptr: plain int32 output
+  int shift;
+  int pool;
+};
+
+template <int NRES, bool kFused>
 __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                   const int16_t* __restrict__ Mw,
                                                                   int32_t* __restrict__ y,
-                                                                  int16_t* __restrict__ y_res) {
+                                                                  int16_t* __restrict__ y_res, Requant rq) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = NRES;
   int16_t* S = reinterpret_cast<int16_t*>(smem_raw);  // [nres][kKB][kRowS]
   const int s_bytes = (nres * kKB * kRowS * 2 + 15) & ~15;
   int32_t* AT16 = reinterpret_cast<int32_t*>(smem_raw + s_bytes);  // [nres][16][16], zero padded
+  uint8_t* O8 = reinterpret_cast<uint8_t*>(AT16 + nres * 256);      // [pixel][kKB] int8 (fused requant)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   const int64_t p = blockIdx.x;
@@ -113,19 +123,21 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
   const int ti = (int)((p / g.tw) % g.th);
   const int tj = (int)(p % g.tw);
   const int b_lo = gq, b_hi = gq + 8;  // pass-2 C rows = output column offset b
-  // Output addressing is fixed per lane: slot q -> pixel (a, b).  Precompute
-  // the element offset of channel k0 for each slot (-1: outside the output).
-  int64_t out_off[8];
-  int64_t kstride = g.layout == 0 ? 1 : (int64_t)g.Ho * g.Wo;
+  // Output addressing is fixed per lane: slot q -> pixel (a, b).  32-bit
+  // offsets from the tile origin (channel k0); -1 marks pixels outside the
+  // output plane.
+  int32_t out_off[8];
+  const int32_t kstride = g.layout == 0 ? 1 : g.Ho * g.Wo;
+  int32_t* ytile = nullptr;
+  if (!kFused && y != nullptr)
+    ytile = y + (g.layout == 0 ? (((int64_t)b_img * g.Ho + ti * M) * g.Wo + tj * M) * g.K + k0
+                               : (((int64_t)b_img * g.K + k0) * g.Ho + ti * M) * g.Wo + tj * M);
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
     const int b = (q & 2) ? b_hi : b_lo;
-    const int ho = ti * M + a, wo = tj * M + b;
-    out_off[q] = -1;
-    if (a < M && b < M && ho < g.Ho && wo < g.Wo)
-      out_off[q] = g.layout == 0 ? (((int64_t)b_img * g.Ho + ho) * g.Wo + wo) * g.K + k0
-                                 : (((int64_t)b_img * g.K + k0) * g.Ho + ho) * g.Wo + wo;
+    const bool ok = a < M && b < M && ti * M + a < g.Ho && tj * M + b < g.Wo;
+    out_off[q] = !ok ? -1 : (g.layout == 0 ? (a * g.Wo + b) * g.K : a * g.Wo + b);
   }
   for (int kk = 0; kk < kKB / 4; ++kk) {
     const int k = warp * (kKB / 4) + kk;
@@ -200,6 +212,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
       }
     }
     // yv[r][4*na + e]: a = 8*na + 2t + (e & 1), b = g + 8*(e >> 1)
+    int32_t qv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       if (y_res != nullptr) {
@@ -228,10 +241,49 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
           radix *= (uint32_t)fmr[j].m;
         }
         const int32_t v = (int64_t)x > signed_bound ? (int32_t)((int64_t)x - dyn_range) : (int32_t)x;
-        // direct store: over this warp's 8 channels each pixel receives one
-        // complete 32-byte sector (NHWC), merged in L2
-        if (out_off[q] >= 0 && kvalid) y[out_off[q] + k * kstride] = v;
+        if constexpr (kFused) {
+          qv[q] = min(v > 0 ? v >> rq.shift : 0, 127);
+        } else if (out_off[q] >= 0 && kvalid) {
+          // direct store: over this warp's 8 channels each pixel receives one
+          // complete 32-byte sector (NHWC), merged in L2
+          ytile[out_off[q] + k * kstride] = v;
+        }
       }
+    }
+    if (kFused && y_res == nullptr) {
+      if (rq.pool) {
+        // pairs along a (q, q^1) share a lane; pairs along b are lanes 4 apart
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          int32_t m2 = max(qv[2 * h], qv[2 * h + 1]);
+          m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 4));
+          const int a = 8 * (h >> 1) + 2 * tq;  // even row of the pair
+          const int b = (h & 1) ? b_hi : b_lo;
+          if ((gq & 1) == 0 && a < M && b < M) O8[((a >> 1) * (M >> 1) + (b >> 1)) * kKB + k] = (uint8_t)m2;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
+          const int b = (q & 2) ? b_hi : b_lo;
+          if (a < M && b < M) O8[(a * M + b) * kKB + k] = (uint8_t)qv[q];
+        }
+      }
+    }
+  }
+  if (kFused && y_res == nullptr) {
+    __syncthreads();
+    // int8 NHWC rows of kKB channels (4-byte words)
+    const int side = rq.pool ? (M >> 1) : M;
+    const int Ho = rq.pool ? g.Ho / 2 : g.Ho, Wo = rq.pool ? g.Wo / 2 : g.Wo;
+    const int kw = min(kKB, g.K - k0);
+    for (int idx = tid; idx < side * side * (kKB / 4); idx += blockDim.x) {
+      const int wq = idx % (kKB / 4), pix = idx / (kKB / 4);
+      const int a = pix / side, b = pix - a * side;
+      const int ho = ti * side + a, wo = tj * side + b;
+      if (ho >= Ho || wo >= Wo || 4 * wq >= kw) continue;
+      const uint32_t word = *reinterpret_cast<const uint32_t*>(O8 + pix * kKB + 4 * wq);
+      *reinterpret_cast<uint32_t*>(rq.out + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 4 * wq) = word;
     }
   }
 }
@@ -239,22 +291,23 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
 }  // namespace
 
 size_t output_tc_smem(const PlanDevice& d) {
-  return (size_t)((d.n_res * kKB * kRowS * 2 + 15) & ~15) + d.n_res * 256 * 4;
+  return (size_t)((d.n_res * kKB * kRowS * 2 + 15) & ~15) + d.n_res * 256 * 4 + (size_t)d.m_out * d.m_out * kKB;
 }
 
 cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
-                                       int16_t* y_res, cudaStream_t s) {
+                                       int16_t* y_res, cudaStream_t s, int8_t* out8, int shift, int pool) {
+  const Requant rq{out8, shift, pool};
   const size_t smem = output_tc_smem(plan.dev);
   dim3 grid((unsigned)g.P, (g.K + kKB - 1) / kKB);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res);
+    kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res, rq);
   };
   switch (plan.dev.n_res) {
-    case 1: launch(output_transform_tc_kernel<1>); break;
-    case 2: launch(output_transform_tc_kernel<2>); break;
-    case 3: launch(output_transform_tc_kernel<3>); break;
-    default: launch(output_transform_tc_kernel<4>); break;
+    case 1: out8 ? launch(output_transform_tc_kernel<1, true>) : launch(output_transform_tc_kernel<1, false>); break;
+    case 2: out8 ? launch(output_transform_tc_kernel<2, true>) : launch(output_transform_tc_kernel<2, false>); break;
+    case 3: out8 ? launch(output_transform_tc_kernel<3, true>) : launch(output_transform_tc_kernel<3, false>); break;
+    default: out8 ? launch(output_transform_tc_kernel<4, true>) : launch(output_transform_tc_kernel<4, false>); break;
   }
   return cudaGetLastError();
 }

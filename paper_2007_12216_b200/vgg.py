@@ -69,7 +69,7 @@ class VGG16Rns:
     def launches_per_forward(self) -> int:
         return 4 * len(self.cfg.layers)  # input transform, GEMM, output transform, glue
 
-    def layer_work(self, batch: int) -> list[dict]:
+    def layer_work(self, batch: int, fused: bool = False) -> list[dict]:
         """Algorithmic work per layer and kernel ("Roofline"):
         bytes for the memory-bound stages, int8 tensor ops for the GEMM."""
         out = []
@@ -84,7 +84,8 @@ class VGG16Rns:
                 "name": name,
                 "input_transform_bytes": batch * side * side * c + planes * npos * tiles * c,
                 "gemm_ops": 2 * tiles * npos * c * k * mma_per_product,
-                "output_transform_bytes": len(self.cfg.moduli) * npos * tiles * k * 2 + batch * side * side * k * 4,
+                "output_transform_bytes": len(self.cfg.moduli) * npos * tiles * k * 2 + (
+                    batch * oside * oside * k if fused else batch * side * side * k * 4),
                 "glue_bytes": batch * side * side * k * 4 + batch * oside * oside * k,
                 "direct_ops": 2 * batch * side * side * c * k * 9,
             })
@@ -126,6 +127,65 @@ class VGG16Rns:
                 bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
             timed("glue", i, lambda: l.rnsw_requant_pool(vp(y.data_ptr()), batch, side, side, k, self.cfg.shifts[i],
                                                          1 if pool else 0, vp(nxt.data_ptr()), s))
+            cur = nxt
+        return cur
+
+    def forward_fused(self, x):
+        """Same stack with the glue fused into each layer's output stage
+        (rnsw_conv_forward_requant): the int32 outputs are never written.
+        Bit-identical to forward() (tests/test_gpu_configs.py)."""
+        l = _native.lib()
+        vp = _native.c_void_p
+        batch = int(x.shape[0])
+        bufs = self._alloc(batch)
+        s = _stream_ptr()
+        ws = bufs["ws"]
+        cur = x.contiguous()
+        nl = len(self.cfg.layers)
+        for i, ((name, side, c, k, pool), bank) in enumerate(zip(self.cfg.layers, self.banks)):
+            oside = side // 2 if pool else side
+            nxt = bufs["out"] if i == nl - 1 else \
+                bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
+            _native.check(l.rnsw_conv_forward_requant(self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, k,
+                                                      1, vp(bank.data.data_ptr()), self.cfg.shifts[i],
+                                                      1 if pool else 0, vp(nxt.data_ptr()), vp(ws.data_ptr()),
+                                                      ws.numel(), s))
+            cur = nxt
+        return cur
+
+    def forward_fused_staged(self, x, record):
+        """forward_fused() with a CUDA event pair around every kernel."""
+        torch = _torch()
+        l = _native.lib()
+        vp = _native.c_void_p
+        batch = int(x.shape[0])
+        bufs = self._alloc(batch)
+        s = _stream_ptr()
+        ws = bufs["ws"]
+        cur = x.contiguous()
+        nl = len(self.cfg.layers)
+
+        def timed(kind, i, fn):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _native.check(fn())
+            b.record()
+            record(kind, i, a, b)
+
+        for i, ((name, side, c, k, pool), bank) in enumerate(zip(self.cfg.layers, self.banks)):
+            tiles = batch * math.ceil(side / self.cfg.tile_m) ** 2
+            vb = (l.rnsw_v_bytes(self.plan.handle, tiles, c) + 255) // 256 * 256
+            v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
+            oside = side // 2 if pool else side
+            nxt = bufs["out"] if i == nl - 1 else \
+                bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
+            timed("input_transform", i, lambda: l.rnsw_input_transform(
+                self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
+            timed("gemm", i, lambda: l.rnsw_winograd_gemm(
+                self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), ws.numel() - vb, s))
+            timed("output_transform", i, lambda: l.rnsw_output_transform_requant(
+                self.plan.handle, vp(m_ptr), batch, side, side, k, 1, self.cfg.shifts[i], 1 if pool else 0,
+                vp(nxt.data_ptr()), s))
             cur = nxt
         return cur
 

@@ -91,3 +91,49 @@ def test_vgg16_batch4_matches_per_image_runs():
         assert np.array_equal(full[i:i + 1], one)
     staged = net.forward_staged(xb, lambda *a: None).cpu().numpy()
     assert np.array_equal(staged, full)
+
+
+def test_vgg16_fused_glue_matches_unfused():
+    """The fused requant/pool epilogue (rnsw_conv_forward_requant) gives the
+    same int8 maps as int32 output + separate glue, layer by layer."""
+    import torch
+    from paper_2007_12216_b200 import workloads as W
+    from paper_2007_12216_b200.vgg import VGG16Rns
+
+    net = VGG16Rns()
+    x = torch.from_numpy(W.vgg16_images(3)).cuda()
+    a = net.forward(x).cpu().numpy()
+    b = net.forward_fused(x).cpu().numpy()
+    c = net.forward_fused_staged(x, lambda *args: None).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    one = net.forward_fused(x[:1]).cpu().numpy()
+    assert sha(one) == digests()["vgg16/final"]["y"]
+
+
+def test_fused_requant_single_layers():
+    import torch
+    from oracle.vgg_ref import requant_pool
+    from paper_2007_12216_b200 import _native
+    from paper_2007_12216_b200.layer import _filters_on_device, _stream_ptr, plan_for
+    import paper_2007_12216_b200 as rnsw
+
+    rng = np.random.default_rng(77)
+    for (h, c, k, tm, pool, shift) in [(28, 32, 64, 14, 1, 9), (20, 16, 36, 6, 0, 7), (17, 48, 8, 8, 1, 11),
+                                       (12, 64, 20, 10, 1, 8)]:
+        system = rnsw.RnsSystem((4001, 4331) if tm % 2 == 0 and tm > 8 else (251, 241, 239))
+        plan = plan_for(rnsw.cached_transforms(tm, 3), system)
+        x = rng.integers(0, 128, (2, h, h, c)).astype(np.int8)
+        w = np.clip(np.rint(rng.normal(0, 20, (3, 3, c, k))), -127, 127).astype(np.int8)
+        bank = _filters_on_device(plan, torch.from_numpy(w).cuda(), c, k, _native.LAYOUT_NHWC)
+        l = _native.lib()
+        ws_bytes = l.rnsw_workspace_bytes(plan.handle, 2, h, h, c, k, 1)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+        oh = h // 2 if pool else h
+        out = torch.empty((2, oh, oh, k), dtype=torch.int8, device="cuda")
+        xd = torch.from_numpy(x).cuda()
+        vp = _native.c_void_p
+        _native.check(l.rnsw_conv_forward_requant(plan.handle, vp(xd.data_ptr()), 2, h, h, c, k, 1,
+                                                  vp(bank.data.data_ptr()), shift, pool, vp(out.data_ptr()),
+                                                  vp(ws.data_ptr()), ws_bytes, _stream_ptr()))
+        want = requant_pool(oracle.direct_conv_c(x, w, 1), shift, bool(pool))
+        assert np.array_equal(out.cpu().numpy(), want), (h, c, k, tm, pool)

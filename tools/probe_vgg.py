@@ -35,6 +35,15 @@ for B in batches:
               f"  gemm {wk['gemm_ops']/r['gemm']/1e9:6.0f} TOPS"
               f"  out {wk['output_transform_bytes']/r['output_transform']/1e6:6.0f} GB/s")
     print(f"  direct-equiv {sum(w['direct_ops'] for w in work)/tot/1e9:.1f} TOPS")
+    rec = []
+    net.forward_fused_staged(x, lambda kind, i, a, b: rec.append((kind, i, a, b)))
+    torch.cuda.synchronize()
+    perf = defaultdict(float)
+    for kind, i, a, b in rec:
+        perf[kind] += a.elapsed_time(b)
+    totf = sum(perf.values())
+    print(f"B={B} fused total {totf:.3f} ms  " + "  ".join(f"{k} {v:.3f}" for k, v in perf.items()) +
+          f"  direct-equiv {sum(w['direct_ops'] for w in work)/totf/1e9:.1f} TOPS")
 if "--check" in sys.argv or True:
     import oracle
     from oracle.vgg_ref import vgg16_stack
