@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
   for (int r = 0; r < nres; ++r) {
     const ResidueTables& tb = plan->res[r];
     const FastMod fm = fast_mod_of(tb);
+    const int32_t pbias = pos_bias(fm);  // -> representative in [0, m)
+    const int32_t sbias = fm.off;        // -> [0, m) shifted by h: subtract h for the symmetric residue
     const int planes = tb.planes;
     const int32_t* bt = BT16 + r * 256;
     // pass-1 A: BT rows j = g / g+8, columns b = 4t..4t+3
@@ -123,54 +125,63 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       transpose4x4(word_of(raw[1][0], u), word_of(raw[1][1], u), word_of(raw[1][2], u), word_of(raw[1][3], u),
                    din[1]);
 #pragma unroll
+      for (int s = 0; s < 8; ++s) outw[0][s][u] = outw[1][s][u] = 0u;
+      // channels of this word: a rolled loop keeps the kernel inside the
+      // instruction cache (the fully unrolled body missed in L0/L1.5)
+#pragma unroll 1
       for (int q = 0; q < 4; ++q) {
+        const uint32_t dq0 = q == 0 ? din[0][0] : q == 1 ? din[0][1] : q == 2 ? din[0][2] : din[0][3];
+        const uint32_t dq1 = q == 0 ? din[1][0] : q == 1 ? din[1][1] : q == 2 ? din[1][2] : din[1][3];
+        const uint32_t bsel = (0x3210u & ~(0xFu << (4 * q))) | (0x4u << (4 * q));  // insert at byte q
+        // pass 1 -> T in [0, m): the reduction bias rides in the accumulator
         int32_t t[2][4];
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) {
-          int32_t acc[4] = {0, 0, 0, 0};
+          int32_t acc[4] = {pbias, pbias, pbias, pbias};
           if (planes == 2) {
             int32_t hi[4] = {0, 0, 0, 0};
-            imma_ss(hi, ahi0, ahi1, din[ni][q]);
-            imma_ss(acc, alo0, alo1, din[ni][q]);
+            imma_ss(hi, ahi0, ahi1, ni ? dq1 : dq0);
+            imma_ss(acc, alo0, alo1, ni ? dq1 : dq0);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) t[ni][e] = red_fast(hi[e] * 256 + acc[e], fm);
+            for (int e = 0; e < 4; ++e) t[ni][e] = red_pos_biased(hi[e] * 256 + acc[e], fm);
           } else {
-            imma_ss(acc, alo0, alo1, din[ni][q]);
+            imma_ss(acc, alo0, alo1, ni ? dq1 : dq0);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) t[ni][e] = red_fast(acc[e], fm);
+            for (int e = 0; e < 4; ++e) t[ni][e] = red_pos_biased(acc[e], fm);
           }
         }
-        // pass 2: A rows j = g / g+8, k-slots = {2t, 2t+1, 8+2t, 9+2t}
+        // pass 2: A rows j = g / g+8, k-slots = {2t, 2t+1, 8+2t, 9+2t}; T is
+        // non-negative, so its low limb is the u8 low byte and the high limb T >> 8
         const uint32_t tlo0 = pack4_lo(t[0][0], t[0][1], t[1][0], t[1][1]);
         const uint32_t tlo1 = pack4_lo(t[0][2], t[0][3], t[1][2], t[1][3]);
         int32_t v[2][4];
         if (planes == 2) {
-          const uint32_t thi0 = pack4_lo(limb_hi(t[0][0]), limb_hi(t[0][1]), limb_hi(t[1][0]), limb_hi(t[1][1]));
-          const uint32_t thi1 = pack4_lo(limb_hi(t[0][2]), limb_hi(t[0][3]), limb_hi(t[1][2]), limb_hi(t[1][3]));
+          const uint32_t thi0 = pack4_lo(t[0][0] >> 8, t[0][1] >> 8, t[1][0] >> 8, t[1][1] >> 8);
+          const uint32_t thi1 = pack4_lo(t[0][2] >> 8, t[0][3] >> 8, t[1][2] >> 8, t[1][3] >> 8);
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni) {
-            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {0, 0, 0, 0};
-            imma_ss(hh, thi0, thi1, bhi[ni]);
-            imma_ss(cr, thi0, thi1, blo[ni]);
-            imma_ss(cr, tlo0, tlo1, bhi[ni]);
-            imma_ss(ll, tlo0, tlo1, blo[ni]);
+            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {sbias, sbias, sbias, sbias};
+            imma_us(hh, thi0, thi1, bhi[ni]);
+            imma_us(cr, thi0, thi1, blo[ni]);
+            imma_us(cr, tlo0, tlo1, bhi[ni]);
+            imma_us(ll, tlo0, tlo1, blo[ni]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[ni][e] = red_fast(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+            for (int e = 0; e < 4; ++e) v[ni][e] = red_pos_biased(hh[e] * 65536 + cr[e] * 256 + ll[e], fm) - fm.h;
           }
         } else {
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni) {
-            int32_t acc[4] = {0, 0, 0, 0};
-            imma_ss(acc, tlo0, tlo1, blo[ni]);
+            int32_t acc[4] = {sbias, sbias, sbias, sbias};
+            imma_us(acc, tlo0, tlo1, blo[ni]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[ni][e] = red_fast(acc[e], fm);
+            for (int e = 0; e < 4; ++e) v[ni][e] = red_pos_biased(acc[e], fm) - fm.h;
           }
         }
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
           const int32_t val = v[s >> 2][s & 3];
-          outw[0][s][u] = put_byte(q == 0 ? 0u : outw[0][s][u], val, q);
-          if (planes == 2) outw[1][s][u] = put_byte(q == 0 ? 0u : outw[1][s][u], limb_hi(val), q);
+          outw[0][s][u] = __byte_perm(outw[0][s][u], (uint32_t)val, bsel);
+          if (planes == 2) outw[1][s][u] = __byte_perm(outw[1][s][u], (uint32_t)limb_hi(val), bsel);
         }
       }
     }
