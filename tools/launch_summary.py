@@ -17,7 +17,8 @@ for r in rows:
              "filter_transform" if "filter" in name else name[:60])
     v = float(r["Metric Value"])
     unit = r["Metric Unit"]
-    v = v / 1e3 if unit == "nsecond" else v * 1e3 if unit == "msecond" else v  # -> usecond
+    unit = unit.strip().lower()
+    v = v / 1e3 if unit in ("ns", "nsecond") else v * 1e3 if unit in ("ms", "msecond") else v  # -> usecond
     per[short][0] += 1
     per[short][1] += v
 tot = sum(t for _, t in per.values())
