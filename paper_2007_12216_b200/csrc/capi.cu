@@ -359,7 +359,7 @@ int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int
   if (x == nullptr || U == nullptr || out == nullptr || workspace == nullptr)
     return fail(RNSW_ERR_INVALID, "null buffer");
   if (shift < 0 || shift > 31) return fail(RNSW_ERR_INVALID, "shift must be in [0, 31]");
-  if (!plan->host.dev.fast)
+  if (!rnsw::tc_output_ok(plan->host.dev))
     return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs the tensor-core transform path (moduli < 4500)");
   if ((K & 3) != 0) return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs K %% 4 == 0");
   if (pool && (plan->host.dev.m_out & 1)) return fail(RNSW_ERR_UNSUPPORTED, "fused 2x2 pooling needs an even tile_m");
@@ -385,7 +385,7 @@ int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, 
                                   int shift, int pool, int8_t* out, void* stream) {
   if (int rc = check_plan(plan)) return rc;
   if (Mw == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
-  if (!plan->host.dev.fast || (K & 3) != 0 || (pool && (plan->host.dev.m_out & 1)))
+  if (!rnsw::tc_output_ok(plan->host.dev) || (K & 3) != 0 || (pool && (plan->host.dev.m_out & 1)))
     return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation not available for this plan/geometry");
   rnsw::Geometry g;
   if (int rc = make_geometry(plan, B, H, W, 1, K, pad, RNSW_LAYOUT_NHWC, &g)) return rc;

@@ -40,6 +40,7 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
                                        int pool = 0);
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s);
+bool tc_output_ok(const PlanDevice& d);
 cudaError_t launch_mrc(const PlanHost& plan, const int16_t* residues, int64_t count, int64_t* out,
                        cudaStream_t s);
 cudaError_t launch_requant_pool(const int32_t* y, int B, int H, int W, int C, int shift, int pool, int8_t* out,

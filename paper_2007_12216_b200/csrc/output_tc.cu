@@ -36,8 +36,9 @@ struct Requant {
   int pool;
 };
 
-template <int NRES, bool kFused>
-__global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
+// kMode: 0 int32 output, 1 fused requant (int8), 2 per-residue debug output
+template <int NRES, int kPL, int kMode>
+__global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                   const int16_t* __restrict__ Mw,
                                                                   int32_t* __restrict__ y,
                                                                   int16_t* __restrict__ y_res, Requant rq) {
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
   int32_t out_off[8];
   const int32_t kstride = g.layout == 0 ? 1 : g.Ho * g.Wo;
   int32_t* ytile = nullptr;
-  if (!kFused && y != nullptr)
+  if (kMode == 0)
     ytile = y + (g.layout == 0 ? (((int64_t)b_img * g.Ho + ti * M) * g.Wo + tj * M) * g.K + k0
                                : (((int64_t)b_img * g.K + k0) * g.Ho + ti * M) * g.Wo + tj * M);
 #pragma unroll
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
             const int16_t* row = S + (r * kKB + k) * kRowS;
       const FastMod fm = fmr[r];
       int32_t z[2][4];
-      if (plr[r] == 2) {
+      if (kPL == 2) {
 #pragma unroll
         for (int ni = 0; ni < 2; ++ni) {
           const int i = gq + 8 * ni;
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
         }
       }
       // pass 2: A = Z^T (rows b = g / g+8; k-slots <- columns i of pass 1)
-      if (plr[r] == 2) {
+      if (kPL == 2) {
         // z in [0, m): u8 low byte, high part z >> 8 in [0, 23]
         const uint32_t zlo0 = pack4_lo(z[0][0], z[0][1], z[1][0], z[1][1]);
         const uint32_t zlo1 = pack4_lo(z[0][2], z[0][3], z[1][2], z[1][3]);
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
     int32_t qv[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      if (y_res != nullptr) {
+      if constexpr (kMode == 2) {
         const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
         const int b = (q & 2) ? b_hi : b_lo;
         if (a < M && b < M && k0 + k < g.K) {
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
           radix *= (uint32_t)fmr[j].m;
         }
         const int32_t v = (int64_t)x > signed_bound ? (int32_t)((int64_t)x - dyn_range) : (int32_t)x;
-        if constexpr (kFused) {
+        if constexpr (kMode == 1) {
           qv[q] = min(v > 0 ? v >> rq.shift : 0, 127);
         } else if (out_off[q] >= 0 && kvalid) {
           // direct store: over this warp's 8 channels each pixel receives one
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
         }
       }
     }
-    if (kFused && y_res == nullptr) {
+    if (kMode == 1) {
       if (rq.pool) {
         // pairs along a (q, q^1) share a lane; pairs along b are lanes 4 apart
 #pragma unroll
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(128) output_transform_tc_kernel(const PlanDevi
       }
     }
   }
-  if (kFused && y_res == nullptr) {
+  if (kMode == 1) {
     __syncthreads();
     // int8 NHWC rows of kKB channels (4-byte words)
     const int side = rq.pool ? (M >> 1) : M;
@@ -302,13 +303,24 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res, rq);
+    return 0;
   };
-  switch (plan.dev.n_res) {
-    case 1: out8 ? launch(output_transform_tc_kernel<1, true>) : launch(output_transform_tc_kernel<1, false>); break;
-    case 2: out8 ? launch(output_transform_tc_kernel<2, true>) : launch(output_transform_tc_kernel<2, false>); break;
-    case 3: out8 ? launch(output_transform_tc_kernel<3, true>) : launch(output_transform_tc_kernel<3, false>); break;
-    default: out8 ? launch(output_transform_tc_kernel<4, true>) : launch(output_transform_tc_kernel<4, false>); break;
+  const int mode = y_res != nullptr ? 2 : (out8 != nullptr ? 1 : 0);
+  const bool pl2 = plan.dev.res[0].planes == 2;
+#define RNSW_OT_MODES(NR, PL)                                             \
+  (mode == 0 ? launch(output_transform_tc_kernel<NR, PL, 0>)              \
+   : mode == 1 ? launch(output_transform_tc_kernel<NR, PL, 1>)            \
+               : launch(output_transform_tc_kernel<NR, PL, 2>))
+  switch (plan.dev.n_res * (pl2 ? 10 : 1)) {
+    case 10: RNSW_OT_MODES(1, 2); break;
+    case 20: RNSW_OT_MODES(2, 2); break;
+    case 1: RNSW_OT_MODES(1, 1); break;
+    case 2: RNSW_OT_MODES(2, 1); break;
+    case 3: RNSW_OT_MODES(3, 1); break;
+    case 4: RNSW_OT_MODES(4, 1); break;
+    default: return cudaErrorInvalidValue;  // the dispatcher keeps other systems on the generic kernel
   }
+#undef RNSW_OT_MODES
   return cudaGetLastError();
 }
 

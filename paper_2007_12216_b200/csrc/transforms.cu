@@ -317,6 +317,19 @@ __global__ void requant_pool_vec4_kernel(const int4* __restrict__ y, int B, int 
   }
 }
 
+}  // namespace
+
+// The tensor-core output kernel is instantiated for uniform limb planes:
+// 1-2 residues of 16-bit moduli or 1-4 residues of 8-bit moduli.
+bool tc_output_ok(const PlanDevice& d) {
+  if (!d.fast) return false;
+  for (int r = 1; r < d.n_res; ++r)
+    if (d.res[r].planes != d.res[0].planes) return false;
+  return d.res[0].planes == 1 || d.n_res <= 2;
+}
+
+namespace {
+
 int grid_for(int64_t total, int threads) {
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 32) blocks = 148 * 32;
@@ -357,7 +370,7 @@ cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, cons
 
 cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
                                     int16_t* y_res, cudaStream_t s) {
-  if (plan.dev.fast && !force_generic()) return launch_output_transform_tc(plan, g, Mw, y, y_res, s);
+  if (tc_output_ok(plan.dev) && !force_generic()) return launch_output_transform_tc(plan, g, Mw, y, y_res, s);
   const int N = plan.dev.n, M = plan.dev.m_out, nres = plan.dev.n_res;
   const size_t smem =
       (size_t)(nres * N * N * kChanBlock + N * M * kChanBlock + nres * M * M * kChanBlock + nres * M * N) *
