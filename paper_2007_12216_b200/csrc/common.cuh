@@ -50,16 +50,17 @@ RNSW_DEV int32_t sym_mod_small(int32_t x, float m, float inv_m) {
 struct FastMod {
   uint32_t mul;
   int32_t shift, off, m, h;
+  uint32_t negm;  // (uint32)(-m): n - q*m as one IMAD q*negm + n
 };
 
 RNSW_DEV FastMod fast_mod_of(const ResidueTables& t) {
-  return FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half};
+  return FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half, (uint32_t)(-t.modulus)};
 }
 
 RNSW_DEV int32_t red_fast(int32_t x, const FastMod& f) {
   const uint32_t n = (uint32_t)(x + f.off);
   const uint32_t q = __umulhi(n, f.mul) >> f.shift;
-  return (int32_t)(n - q * (uint32_t)f.m) - f.h;
+  return (int32_t)(q * f.negm + n) - f.h;
 }
 
 // Non-negative representative in [0, m) of n - f.off + (f.off - f.h)... i.e.
@@ -70,10 +71,17 @@ RNSW_DEV int32_t pos_bias(const FastMod& f) { return f.off - f.h; }
 
 RNSW_DEV int32_t red_pos_biased(int32_t n, const FastMod& f) {
   const uint32_t q = __umulhi((uint32_t)n, f.mul) >> f.shift;
-  return (int32_t)((uint32_t)n - q * (uint32_t)f.m);
+  return (int32_t)(q * f.negm + (uint32_t)n);
 }
 
 RNSW_DEV int32_t red_pos(int32_t x, const FastMod& f) { return red_pos_biased(x + pos_bias(f), f); }
+
+// Same result as red_pos_biased, computed as n - q*m (IMAD with a negated
+// quotient); ptxas schedules the output transform better with this form.
+RNSW_DEV int32_t red_pos_biased_sub(int32_t n, const FastMod& f) {
+  const uint32_t q = __umulhi((uint32_t)n, f.mul) >> f.shift;
+  return (int32_t)((uint32_t)n - q * (uint32_t)f.m);
+}
 
 // 64-bit exact symmetric reduction (used for the mixed-radix digits).
 RNSW_DEV int64_t sym_mod64(int64_t x, int64_t m) {

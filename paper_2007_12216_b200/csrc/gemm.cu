@@ -411,7 +411,7 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
     a.r256[r] = d.res[r].r_256;
     a.r65536[r] = d.res[r].r_65536;
     const ResidueTables& t = d.res[r];
-    a.fm[r] = FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half};
+    a.fm[r] = FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half, (uint32_t)(-t.modulus)};
     if (d.res[r].planes > maxpl) maxpl = d.res[r].planes;
   }
   a.fast = (d.fast && Cp <= 8192) ? 1 : 0;

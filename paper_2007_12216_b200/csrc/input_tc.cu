@@ -40,6 +40,7 @@ RNSW_DEV void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, u
 
 RNSW_DEV uint32_t word_of(const uint4& v, int u) { return u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w; }
 
+template <int kPL>
 __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                  const int8_t* __restrict__ x,
                                                                  int8_t* __restrict__ V) {
@@ -75,11 +76,14 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
           v = __ldg(reinterpret_cast<const uint4*>(x + (((int64_t)b_img * g.H + h) * g.W + w) * g.C + c_base));
         } else {
           uint32_t wd[4] = {0, 0, 0, 0};
-          for (int q = 0; q < 16 && c_base + q < g.C; ++q) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
             const int c = c_base + q;
-            const int64_t xi = g.layout == 0 ? (((int64_t)b_img * g.H + h) * g.W + w) * g.C + c
-                                             : (((int64_t)b_img * g.C + c) * g.H + h) * g.W + w;
-            wd[q >> 2] |= (uint32_t)(uint8_t)x[xi] << (8 * (q & 3));
+            if (c < g.C) {
+              const int64_t xi = g.layout == 0 ? (((int64_t)b_img * g.H + h) * g.W + w) * g.C + c
+                                               : (((int64_t)b_img * g.C + c) * g.H + h) * g.W + w;
+              wd[q >> 2] |= (uint32_t)(uint8_t)x[xi] << (8 * (q & 3));
+            }
           }
           v = make_uint4(wd[0], wd[1], wd[2], wd[3]);
         }
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
     const FastMod fm = fast_mod_of(tb);
     const int32_t pbias = pos_bias(fm);  // -> representative in [0, m)
     const int32_t sbias = fm.off;        // -> [0, m) shifted by h: subtract h for the symmetric residue
-    const int planes = tb.planes;
+    constexpr int planes = kPL;
     const int32_t* bt = BT16 + r * 256;
     // pass-1 A: BT rows j = g / g+8, columns b = 4t..4t+3
     int32_t av[8];
@@ -206,7 +210,10 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s) {
   dim3 grid((unsigned)(g.P * ((g.Cp + kCTAChannels - 1) / kCTAChannels)));
-  input_transform_tc_kernel<<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+  if (plan.dev.res[0].planes == 2)
+    input_transform_tc_kernel<2><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+  else
+    input_transform_tc_kernel<1><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
   return cudaGetLastError();
 }
 

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           imma_ss(cr, A1lo[r][0], A1lo[r][1], bhi);
           imma_su(ll, A1lo[r][0], A1lo[r][1], blo);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+          for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased_sub(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
         }
       } else {
 #pragma unroll
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           int32_t acc[4] = {bias, bias, bias, bias};
           imma_ss(acc, A1lo[r][0], A1lo[r][1], b);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased(acc[e], fm);
+          for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased_sub(acc[e], fm);
         }
       }
       // pass 2: A = Z^T (rows b = g / g+8; k-slots <- columns i of pass 1)
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           imma_us(cr, zlo0, zlo1, B2hi[r][na]);
           imma_us(ll, zlo0, zlo1, B2lo[r][na]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_pos_biased(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_pos_biased_sub(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
         }
       } else {
         // z in [0, m < 256): u8
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           int32_t acc[4] = {bias, bias, bias, bias};
           imma_us(acc, za0, za1, B2lo[r][na]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_pos_biased(acc[e], fm);
+          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_pos_biased_sub(acc[e], fm);
         }
       }
     }
