@@ -46,7 +46,8 @@ struct GemmArgs {
   int r256[RNSW_MAX_RES];
   int r65536[RNSW_MAX_RES];
   FastMod fm[RNSW_MAX_RES];
-  int fast;  // exact division-free reductions apply (plan.fast and C <= 8192)
+  int fast;   // exact division-free reductions apply (plan.fast and C <= 8192)
+  int fast2;  // additionally C <= 512: hh needs no separate reduction
   int16_t* Mw;
 };
 
@@ -122,7 +123,12 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
 #pragma unroll
     for (int j = 0; j < kBatch / 16; ++j) {
       int32_t r[16];
-      if (a.fast) {
+      if (a.fast2) {
+        // C <= 512, m < 4500: |hh * (2^16 mod m)| <= 512*81*2250 < 2^27, so hh
+        // goes into the recombination unreduced (2 reductions per output)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] = red_fast(hh[j][e] * r16 + red_fast(cr[j][e], fm) * r8 + ll[j][e], fm);
+      } else if (a.fast) {
 #pragma unroll
         for (int e = 0; e < 16; ++e)
           r[e] = red_fast(red_fast(hh[j][e], fm) * r16 + red_fast(cr[j][e], fm) * r8 + ll[j][e], fm);
@@ -415,6 +421,7 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
     if (d.res[r].planes > maxpl) maxpl = d.res[r].planes;
   }
   a.fast = (d.fast && Cp <= 8192) ? 1 : 0;
+  a.fast2 = (a.fast && Cp <= 512) ? 1 : 0;
   int bn;
   if (maxpl == 2) bn = 64;
   else bn = Kp <= 64 ? 64 : (Kp <= 128 ? 128 : 256);

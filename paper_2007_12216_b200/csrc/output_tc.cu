@@ -36,6 +36,15 @@ struct Requant {
   int pool;
 };
 
+// Both forms of the biased reduction give identical results; ptxas
+// schedules the fused instance better with n - q*m and the int32 instance
+// with q*(-m) + n (measured, profiles/r01_*).
+template <int kMode>
+RNSW_DEV int32_t red_k4(int32_t n, const FastMod& f) {
+  if constexpr (kMode == 1) return red_pos_biased_sub(n, f);
+  else return red_pos_biased(n, f);
+}
+
 // kMode: 0 int32 output, 1 fused requant (int8), 2 per-residue debug output
 template <int NRES, int kPL, int kMode>
 __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           imma_ss(cr, A1lo[r][0], A1lo[r][1], bhi);
           imma_su(ll, A1lo[r][0], A1lo[r][1], blo);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased_sub(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+          for (int e = 0; e < 4; ++e) z[ni][e] = red_k4<kMode>(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
         }
       } else {
 #pragma unroll
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           int32_t acc[4] = {bias, bias, bias, bias};
           imma_ss(acc, A1lo[r][0], A1lo[r][1], b);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased_sub(acc[e], fm);
+          for (int e = 0; e < 4; ++e) z[ni][e] = red_k4<kMode>(acc[e], fm);
         }
       }
       // pass 2: A = Z^T (rows b = g / g+8; k-slots <- columns i of pass 1)
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           imma_us(cr, zlo0, zlo1, B2hi[r][na]);
           imma_us(ll, zlo0, zlo1, B2lo[r][na]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_pos_biased_sub(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_k4<kMode>(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
         }
       } else {
         // z in [0, m < 256): u8
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           int32_t acc[4] = {bias, bias, bias, bias};
           imma_us(acc, za0, za1, B2lo[r][na]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_pos_biased_sub(acc[e], fm);
+          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_k4<kMode>(acc[e], fm);
         }
       }
     }
