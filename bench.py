@@ -40,7 +40,7 @@ UNIT = "TOPS"
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=256, help="global batch (images), sharded over ranks")
     ap.add_argument("--impl", default="rnsw", choices=["rnsw", "reference"])
@@ -273,18 +273,28 @@ def run_gpu_arm(args):
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
-        step(x_dev)
-    torch.cuda.synchronize()
-    barrier()
-
-    # -------- timed region: K steps, inputs resident in HBM --------
+    # clocks are sampled from before the warm-up (nvidia-smi needs ~0.5 s to
+    # produce its first sample) until the timed region ends; every sample is
+    # taken with the GPU under this workload's load
     gpu_index = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
         gpu_index = vis.split(",")[local]
     with ClockSampler(gpu_index) as clocks:
+        t_warm = time.time()
+        n_warm = 0
+        while True:
+            for _ in range(args.warmup):
+                step(x_dev)
+            n_warm += args.warmup
+            torch.cuda.synchronize()
+            flag = torch.tensor([1.0 if time.time() - t_warm > 1.0 else 0.0], device="cuda")
+            if world > 1:
+                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if flag.item() > 0:
+                break
         barrier()
+        # -------- timed region: K steps, inputs resident in HBM --------
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -368,10 +378,11 @@ def run_gpu_arm(args):
             s["GB_s"] = round(sum(w[k] for w in work) / sec / 1e9, 1)
         stages[kind] = s
     layer_ms = {work[i]["name"]: round(sum(v.values()) * 1e3, 3) for i, v in sorted(per_layer.items())}
+    layer_stage_ms = {work[i]["name"]: {k: round(t * 1e3, 3) for k, t in v.items()} for i, v in sorted(per_layer.items())}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "warmup": n_warm, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded PCG64 images U{0..127}, weights round(N(0,20^2)) clipped; no dataset)",
         "config": {"workload": f"BASELINE config 4: VGG16 13x conv3x3 stack, 224x224x3, batch {args.batch} "
@@ -381,7 +392,7 @@ def run_gpu_arm(args):
                    "global_batch": args.batch, "per_rank_batch": shard, "tile": "F(14x14,3x3)",
                    "moduli": [4001, 4331], "parallelism": f"image-sharded x{world}, one all-gather at the end",
                    "l2": "inputs and intermediates larger than L2 (126 MB)",
-                   "layer_ms": layer_ms},
+                   "layer_ms": layer_ms, "layer_stage_ms": layer_stage_ms},
         "stages": stages,
         "gpu_launches": (net.launches_per_forward() if args.unfused else 3 * len(W.VGG16_LAYERS)) * args.steps,
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -91,6 +91,19 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       raw[ni][e] = v;
     }
 
+  if (c_base >= g.C) {
+    // all 16 channels of this warp are Cp padding: V = BT 0 BT^T = 0
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int e = s & 3, ni = s >> 2;
+      const int j = gq + 8 * (e >> 1), i = 8 * ni + 2 * tq + (e & 1);
+      if (i >= N || j >= N) continue;
+      for (int pl = 0; pl < plan->n_planes; ++pl)
+        *reinterpret_cast<uint4*>(V + ((int64_t)pl * npos + i * N + j) * g.P * g.Cp + p * g.Cp + c_base) =
+            make_uint4(0, 0, 0, 0);
+    }
+    return;
+  }
   for (int r = 0; r < nres; ++r) {
     const ResidueTables& tb = plan->res[r];
     const FastMod fm = fast_mod_of(tb);
@@ -134,6 +147,7 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       // instruction cache (the fully unrolled body missed in L0/L1.5)
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
+        if (c_base + 4 * u + q >= g.C) break;  // padding channels stay 0
         const uint32_t dq0 = q == 0 ? din[0][0] : q == 1 ? din[0][1] : q == 2 ? din[0][2] : din[0][3];
         const uint32_t dq1 = q == 0 ? din[1][0] : q == 1 ? din[1][1] : q == 2 ? din[1][2] : din[1][3];
         const uint32_t bsel = (0x3210u & ~(0xFu << (4 * q))) | (0x4u << (4 * q));  // insert at byte q
