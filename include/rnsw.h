@@ -127,6 +127,17 @@ int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, 
 int rnsw_mrc_reconstruct(const rnsw_plan* plan, const int16_t* residues, int64_t count,
                          int64_t* out, void* stream);
 
+/* Direct int8 implicit-GEMM convolution on tcgen05, the
+ * device counterpart of direct_conv / im2col (rw/layer.py:81-103) for any
+ * stride: x NHWC int8 (C % 16 == 0), y NHWC int32, exact.  Weights are
+ * packed once by rnsw_direct_pack_weights from (R,R,C,K) (layout 0) or OIHW
+ * (layout 1). */
+size_t rnsw_direct_weight_bytes(int R, int C, int K);
+int rnsw_direct_pack_weights(const int8_t* w, int R, int C, int K, int layout, void* w2, size_t w2_bytes,
+                             void* stream);
+int rnsw_direct_conv(const int8_t* x, int B, int H, int W, int C, const void* w2, int K, int R, int pad,
+                     int stride, int32_t* y, void* stream);
+
 /* Inter-layer glue for the VGG16 stack (not part of the reference package;
  * BASELINE.json config 2/4): relu, >> shift, clip to [0,127], optional 2x2
  * max-pool, NHWC int32 -> NHWC int8. */

@@ -19,12 +19,14 @@ from .errors import (
     UnsupportedStride,
 )
 from .layer import (
+    DirectWeights,
     FilterBank,
     LayerSpec,
     RangeReport,
     StageTimings,
     conv2d_rns,
     count_operations,
+    direct_conv,
     layer_conv,
     precompute_filter_transforms,
     precompute_filters_oihw,
@@ -57,5 +59,6 @@ __all__ = [
     "reduce_for_system",
     "LayerSpec", "RangeReport", "StageTimings", "FilterBank", "range_check", "count_operations",
     "precompute_filter_transforms", "precompute_filters_oihw", "winograd_layer_conv", "layer_conv", "conv2d_rns",
+    "direct_conv", "DirectWeights",
     "__version__",
 ]

@@ -48,6 +48,10 @@ _SIGNATURES = {
                                           c_int, c_int, c_void_p, c_void_p, c_size_t, c_void_p]),
     "rnsw_output_transform_requant": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                               c_void_p, c_void_p]),
+    "rnsw_direct_weight_bytes": (c_size_t, [c_int, c_int, c_int]),
+    "rnsw_direct_pack_weights": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
+    "rnsw_direct_conv": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_int, c_int, c_int,
+                                 c_void_p, c_void_p]),
     "rnsw_mrc_reconstruct": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "rnsw_requant_pool": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "rnsw_error_string": (ctypes.c_char_p, [c_int]),

@@ -394,6 +394,37 @@ int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, 
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant");
 }
 
+size_t rnsw_direct_weight_bytes(int R, int C, int K) {
+  if (R < 1 || C < 1 || K < 1) return 0;
+  return rnsw::direct_weight_bytes(R, C, K);
+}
+
+int rnsw_direct_pack_weights(const int8_t* w, int R, int C, int K, int layout, void* w2, size_t w2_bytes,
+                             void* stream) {
+  if (w == nullptr || w2 == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (R < 1 || C < 1 || K < 1) return fail(RNSW_ERR_SHAPE, "bad filter shape");
+  if (layout != RNSW_LAYOUT_NHWC && layout != RNSW_LAYOUT_NCHW) return fail(RNSW_ERR_INVALID, "bad layout %d", layout);
+  if (w2_bytes < rnsw::direct_weight_bytes(R, C, K)) return fail(RNSW_ERR_WORKSPACE, "packed weight buffer too small");
+  cudaError_t e = rnsw::launch_pack_weights(w, R, C, K, layout, static_cast<int8_t*>(w2), (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "direct_pack_weights");
+}
+
+int rnsw_direct_conv(const int8_t* x, int B, int H, int W, int C, const void* w2, int K, int R, int pad, int stride,
+                     int32_t* y, void* stream) {
+  if (x == nullptr || w2 == nullptr || y == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (B < 1 || H < 1 || W < 1 || C < 1 || K < 1 || R < 1 || pad < 0 || stride < 1)
+    return fail(RNSW_ERR_SHAPE, "bad direct conv geometry");
+  if (C % 16 != 0) return fail(RNSW_ERR_UNSUPPORTED, "direct conv needs C %% 16 == 0 (TMA row alignment), got %d", C);
+  if ((int64_t)R * R * C * 128 * 128 > 2147483647LL)
+    return fail(RNSW_ERR_OVERFLOW, "R*R*C = %d can overflow the int32 accumulator", R * R * C);
+  const int Ho = (H + 2 * pad - R) / stride + 1, Wo = (W + 2 * pad - R) / stride + 1;
+  if (H + 2 * pad < R || W + 2 * pad < R || Ho < 1 || Wo < 1) return fail(RNSW_ERR_SHAPE, "padded input smaller than the filter");
+  if (stride > 16) return fail(RNSW_ERR_UNSUPPORTED, "stride %d too large for the TMA box", stride);
+  cudaError_t e = rnsw::launch_direct_conv(x, B, H, W, C, static_cast<const int8_t*>(w2), K, R, pad, stride, y,
+                                           (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "direct_conv");
+}
+
 int rnsw_mrc_reconstruct(const rnsw_plan* plan, const int16_t* residues, int64_t count, int64_t* out, void* stream) {
   if (int rc = check_plan(plan)) return rc;
   if (residues == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");

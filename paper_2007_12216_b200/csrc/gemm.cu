@@ -29,6 +29,18 @@
 
 namespace rnsw {
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
 namespace {
 
 constexpr int kBlockM = 128;  // tiles (P) per MMA tile: TMEM lanes
@@ -334,21 +346,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------------------
 // Host side: tensor maps and dispatch.
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (fn == nullptr) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
 // 3-D view [slabs][rows][Cp] of int8 limb planes; box = (bc bytes, box_rows, 1).
 bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t slabs, int bc, int box_rows) {
-  auto encode = get_encode_fn();
+  auto encode = encode_fn();
   if (encode == nullptr) return false;
   cuuint64_t dims[3] = {(cuuint64_t)Cp, (cuuint64_t)rows, (cuuint64_t)slabs};
   cuuint64_t strides[2] = {(cuuint64_t)Cp, (cuuint64_t)(rows * Cp)};

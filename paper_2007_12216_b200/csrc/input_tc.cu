@@ -22,12 +22,6 @@ namespace {
 
 constexpr int kCTAChannels = 64;
 
-// Insert the low byte of v as byte q of w.
-RNSW_DEV uint32_t put_byte(uint32_t w, int32_t v, int q) {
-  const uint32_t sel = q == 0 ? 0x3214u : q == 1 ? 0x3240u : q == 2 ? 0x3410u : 0x4210u;
-  return __byte_perm(w, (uint32_t)v, sel);
-}
-
 // 4x4 byte transpose: in[e] = 4 channels of pixel e -> out[q] = channel q of pixels 0..3.
 RNSW_DEV void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
   const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);

@@ -2,6 +2,8 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "plan.h"
@@ -41,6 +43,11 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s);
 bool tc_output_ok(const PlanDevice& d);
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
+size_t direct_weight_bytes(int R, int C, int K);
+cudaError_t launch_pack_weights(const int8_t* w, int R, int C, int K, int layout, int8_t* w2, cudaStream_t s);
+cudaError_t launch_direct_conv(const int8_t* x, int B, int H, int W, int C, const int8_t* w2, int K, int R, int pad,
+                               int stride, int32_t* y, cudaStream_t s);
 cudaError_t launch_mrc(const PlanHost& plan, const int16_t* residues, int64_t count, int64_t* out,
                        cudaStream_t s);
 cudaError_t launch_requant_pool(const int32_t* y, int B, int H, int W, int C, int shift, int pool, int8_t* out,

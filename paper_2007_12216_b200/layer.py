@@ -402,13 +402,51 @@ def winograd_layer_conv(spec: LayerSpec, weights, x, system: RnsSystem, declared
     return y.cpu().numpy() if host_result else y
 
 
+class DirectWeights:
+    """Weights packed once for the direct tcgen05 convolution ([K][R*R*Cp])."""
+
+    def __init__(self, weights, layout: int = _native.LAYOUT_NHWC):
+        torch = _torch()
+        wd = to_device(weights)
+        if layout == _native.LAYOUT_NHWC:
+            r, _, c, k = (int(v) for v in wd.shape)
+        else:
+            k, c, r, _ = (int(v) for v in wd.shape)
+        l = _native.lib()
+        nbytes = l.rnsw_direct_weight_bytes(r, c, k)
+        self.data = torch.empty(nbytes, dtype=torch.int8, device=wd.device)
+        _native.check(l.rnsw_direct_pack_weights(_native.c_void_p(wd.data_ptr()), r, c, k, layout,
+                                                 _native.c_void_p(self.data.data_ptr()), nbytes, _stream_ptr()))
+        self.r, self.c, self.k = r, c, k
+
+
+def direct_conv(spec: LayerSpec, weights, x, packed: DirectWeights | None = None):
+    """Exact int32 convolution on the tensor cores: the device counterpart of
+    the reference's oracle direct_conv (rw/layer.py:93-103), any stride.
+    Implicit GEMM on tcgen05 kind::i8 with TMA im2col boxes; needs C % 16 == 0."""
+    torch = _torch()
+    _check_operands(spec, weights, x)
+    host_result = isinstance(x, np.ndarray)
+    xd = to_device(x)
+    if packed is None:
+        packed = DirectWeights(weights)
+    y = torch.empty((spec.batch, spec.out_h, spec.out_w, spec.k), dtype=torch.int32, device=xd.device)
+    l = _native.lib()
+    _native.check(l.rnsw_direct_conv(_native.c_void_p(xd.data_ptr()), spec.batch, spec.h, spec.w, spec.c,
+                                     _native.c_void_p(packed.data.data_ptr()), spec.k, spec.r, spec.padding,
+                                     spec.stride, _native.c_void_p(y.data_ptr()), _stream_ptr()))
+    return y.cpu().numpy() if host_result else y
+
+
 def layer_conv(spec: LayerSpec, weights, x, system: RnsSystem, declared_bound: int | None = None, filters=None,
                timings: StageTimings | None = None):
-    """rw/layer.py:392-412.  The reference falls back to a CPU direct conv for
-    stride != 1; this build has no CPU path, so strided layers raise
-    UnsupportedStride until the GPU direct conv lands."""
+    """rw/layer.py:392-412: stride != 1 goes to the direct convolution --
+    here the tcgen05 implicit-GEMM kernel, not a CPU fallback."""
     if spec.stride != 1:
-        raise UnsupportedStride(f"stride {spec.stride}: the GPU build has no strided path yet (no CPU fallback)")
+        _check_operands(spec, weights, x)
+        if spec.c % 16:
+            raise UnsupportedStride(f"stride {spec.stride} with C={spec.c}: the device direct conv needs C % 16 == 0")
+        return direct_conv(spec, weights, x)
     return winograd_layer_conv(spec, weights, x, system, declared_bound=declared_bound, filters=filters,
                                timings=timings)
 

@@ -161,3 +161,52 @@ def test_random_geometry_sweep(seed):
     system = rnsw.RnsSystem(mods)
     got = rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=system.signed_bound)
     assert np.array_equal(got, oracle.direct_conv_c(x, w, spec.padding))
+
+
+DIRECT = [
+    # b, h, w, c, k, r, pad, stride
+    (1, 56, 56, 64, 64, 3, 1, 1),
+    (2, 28, 28, 256, 96, 3, 1, 1),
+    (3, 17, 23, 32, 40, 3, 1, 2),
+    (1, 224, 224, 64, 64, 3, 1, 1),
+    (2, 30, 30, 128, 300, 5, 2, 1),
+    (1, 9, 9, 48, 8, 3, 0, 3),
+    (4, 14, 14, 512, 512, 3, 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", DIRECT, ids=lambda c: "x".join(map(str, c)))
+def test_direct_conv_matches_oracle(case):
+    rnsw = _rnsw()
+    b, h, w, c, k, r, pad, stride = case
+    spec = rnsw.LayerSpec(h=h, w=w, c=c, k=k, r=r, padding=pad, stride=stride, batch=b)
+    wt, x = _operands(spec, h + c)
+    got = rnsw.direct_conv(spec, wt, x)
+    want = O.direct_conv(x, wt, pad) if stride == 1 else None
+    if stride == 1:
+        assert np.array_equal(got, want)
+    else:
+        full = oracle.direct_conv_c(x, wt, pad)
+        assert np.array_equal(got, full[:, ::stride, ::stride][:, : spec.out_h, : spec.out_w])
+
+
+def test_layer_conv_strided_uses_device_direct_conv():
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=9, w=9, c=16, k=3, r=3, padding=1, stride=2, tile_m=4)
+    wt, x = _operands(spec, 3)
+    got = rnsw.layer_conv(spec, wt, x, rnsw.RnsSystem((251, 241, 239)))
+    assert np.array_equal(got, oracle.direct_conv_c(x, wt, 1)[:, ::2, ::2])
+    bad = rnsw.LayerSpec(h=9, w=9, c=2, k=3, r=3, padding=1, stride=2, tile_m=4)
+    wb, xb = _operands(bad, 4)
+    with pytest.raises(rnsw.UnsupportedStride):
+        rnsw.layer_conv(bad, wb, xb, rnsw.RnsSystem((251, 241, 239)))
+
+
+def test_direct_conv_config5_digest():
+    from golden_util import digests, sha
+    from paper_2007_12216_b200 import workloads as W
+
+    rnsw = _rnsw()
+    w, x = W.config5_operands()
+    spec = rnsw.LayerSpec(h=28, w=28, c=256, k=256, r=3, padding=1, batch=32)
+    assert sha(rnsw.direct_conv(spec, w, x)) == digests()["cfg5/direct"]["y"]
