@@ -150,7 +150,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
   d.n = n;
   d.n_res = n_res;
   d.dynamic_range = 1;
-  int plane = 0;
+  int plane = 0, uplane = 0;
   for (int i = 0; i < n_res; ++i) {
     ResidueTables& t = d.res[i];
     const int m = moduli[i];
@@ -159,6 +159,9 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
     t.planes = m < 256 ? 1 : 2;
     t.plane_base = plane;
     plane += t.planes;
+    t.uplanes = m < 256 ? 1 : 4;
+    t.uplane_base = uplane;
+    uplane += t.uplanes;
     t.inv_m = 1.0f / (float)m;
     t.r_256 = sym(256, m);
     t.r_65536 = sym(65536, m);
@@ -188,6 +191,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
     d.dynamic_range *= m;
   }
   d.n_planes = plane;
+  d.n_uplanes = uplane;
   {
     bool fast = d.dynamic_range < (1LL << 31);
     for (int i = 0; i < n_res; ++i) fast = fast && moduli[i] < 4500;  // keeps every limb recombination below 2^28
@@ -232,7 +236,7 @@ int rnsw_plan_info(const rnsw_plan* plan, int* n, int* n_planes) {
 size_t rnsw_filter_bytes(const rnsw_plan* plan, int C, int K) {
   if (plan == nullptr || C < 1 || K < 1) return 0;
   const PlanDevice& d = plan->host.dev;
-  return (size_t)d.n_planes * d.n * d.n * K * padded_channels(C);
+  return (size_t)d.n_uplanes * d.n * d.n * K * padded_channels(C);
 }
 
 size_t rnsw_v_bytes(const rnsw_plan* plan, int64_t P, int C) {

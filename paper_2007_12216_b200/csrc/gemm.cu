@@ -13,12 +13,13 @@
 // TMEM holds two accumulator sets so the epilogue of tile i overlaps the
 // MMAs of tile i+1.
 //
-// 16-bit moduli: a residue v (|v| <= 16383) is stored as two s8 planes
-// v = 256*hi + lo.  The product of two residues is
-//     hi_a*hi_b * 2^16 + (hi_a*lo_b + lo_a*hi_b) * 2^8 + lo_a*lo_b
-// so each chunk issues 4 MMAs into 3 accumulators (the two cross products
-// share one), recombined mod m in the epilogue.  |acc| <= C * 128^2 < 2^31
-// for C <= 131071 (checked on the host).
+// 16-bit moduli: V residues are two s8 planes v = 256*v_hi + v_lo; the
+// filter bank holds the limbs of u and of u' = 256*u mod m.  Then
+//     v*u = v_hi*256*u + v_lo*u  ==  v_hi*u' + v_lo*u               (mod m)
+//         == 256*(v_hi*u'_hi + v_lo*u_hi) + (v_hi*u'_lo + v_lo*u_lo)
+// so each chunk issues 4 MMAs into 2 accumulators (A256, A1); the epilogue
+// recombines 256*A256 + A1 (< 2^28 for C <= 512) with a single exact
+// reduction.  |acc| <= C * 128^2 < 2^31 for C <= 131071 (host-checked).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -52,20 +53,21 @@ struct GemmArgs {
   int num_pb, num_kb, nkc;
   int64_t total_tiles;
   int planes[RNSW_MAX_RES];
-  int plane_base[RNSW_MAX_RES];
+  int plane_base[RNSW_MAX_RES];   // V planes
+  int uplane_base[RNSW_MAX_RES];  // filter-bank planes (4 per 16-bit residue)
   int modulus[RNSW_MAX_RES];
   float inv_m[RNSW_MAX_RES];
   int r256[RNSW_MAX_RES];
   int r65536[RNSW_MAX_RES];
   FastMod fm[RNSW_MAX_RES];
   int fast;   // exact division-free reductions apply (plan.fast and C <= 8192)
-  int fast2;  // additionally C <= 512: hh needs no separate reduction
+  int fast2;  // additionally C <= 512: 256*A256 + A1 needs a single reduction
   int16_t* Mw;
 };
 
 template <int BN, int MAXPL>
 struct GemmTraits {
-  static constexpr int kAccCols = (MAXPL == 2 ? 3 : 1) * BN;  // TMEM columns per accumulator set
+  static constexpr int kAccCols = (MAXPL == 2 ? 2 : 1) * BN;  // TMEM columns per accumulator set
   static constexpr int kTmemCols = (2 * kAccCols <= 32) ? 32
                                    : (2 * kAccCols <= 64) ? 64
                                    : (2 * kAccCols <= 128) ? 128
@@ -75,7 +77,8 @@ struct GemmTraits {
 
 template <int BC>
 constexpr int stage_bytes(int bn, int maxpl) {
-  return maxpl * (kBlockM + bn) * BC;
+  // A: V planes (maxpl); B: filter-bank planes (1 or 4)
+  return maxpl * kBlockM * BC + (maxpl == 2 ? 4 : 1) * bn * BC;
 }
 
 template <int BN, int BC, int MAXPL>
@@ -113,22 +116,20 @@ RNSW_DEV void release_acc(uint64_t* bar, int lane) {
   if (lane == 0) mbar_arrive(bar);
 }
 
-// 16-bit residues: three accumulators (hh, cross, ll) per column.
+// 16-bit residues: two accumulators (A256, A1) per column.
 template <int BN, int ACC_COLS>
 RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
                              uint64_t* tempty, int lane) {
   constexpr int kHalf = BN / 2;
-  constexpr int kBatch = 32;  // columns per batch: 3 x 32 registers in flight
+  constexpr int kBatch = kHalf < 32 ? kHalf : 32;  // 2 x 32 registers in flight
   const FastMod fm = a.fm[res];
-  const int32_t r8 = a.r256[res], r16 = a.r65536[res];
 #pragma unroll 1
   for (int c0 = 0; c0 < kHalf; c0 += kBatch) {
-    int32_t hh[kBatch / 16][16], cr[kBatch / 16][16], ll[kBatch / 16][16];
+    int32_t hi[kBatch / 16][16], lo[kBatch / 16][16];
 #pragma unroll
     for (int j = 0; j < kBatch / 16; ++j) {
-      tmem_ld16(taddr + c0 + 16 * j, hh[j]);
-      tmem_ld16(taddr + BN + c0 + 16 * j, cr[j]);
-      tmem_ld16(taddr + 2 * BN + c0 + 16 * j, ll[j]);
+      tmem_ld16(taddr + c0 + 16 * j, hi[j]);
+      tmem_ld16(taddr + BN + c0 + 16 * j, lo[j]);
     }
     tmem_ld_wait();
     if (c0 + kBatch >= kHalf) release_acc(tempty, lane);
@@ -136,19 +137,16 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
     for (int j = 0; j < kBatch / 16; ++j) {
       int32_t r[16];
       if (a.fast2) {
-        // C <= 512, m < 4500: |hh * (2^16 mod m)| <= 512*81*2250 < 2^27, so hh
-        // goes into the recombination unreduced (2 reductions per output)
+        // C <= 512, m < 4500: |256*A256 + A1| <= 512*(9*9+128*9)*256 + 512*(9*128+128*128) < 2^28
 #pragma unroll
-        for (int e = 0; e < 16; ++e) r[e] = red_fast(hh[j][e] * r16 + red_fast(cr[j][e], fm) * r8 + ll[j][e], fm);
+        for (int e = 0; e < 16; ++e) r[e] = red_fast(hi[j][e] * 256 + lo[j][e], fm);
       } else if (a.fast) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          r[e] = red_fast(red_fast(hh[j][e], fm) * r16 + red_fast(cr[j][e], fm) * r8 + ll[j][e], fm);
+        for (int e = 0; e < 16; ++e) r[e] = red_fast(red_fast(hi[j][e], fm) * 256 + lo[j][e], fm);
       } else {
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          r[e] = reduce_generic(reduce_generic(hh[j][e], a, res) * r16 + reduce_generic(cr[j][e], a, res) * r8 +
-                                    reduce_generic(ll[j][e], a, res), a, res);
+          r[e] = reduce_generic(reduce_generic(hi[j][e], a, res) * 256 + reduce_generic(lo[j][e], a, res), a, res);
       }
       const int col = col0 + c0 + 16 * j;
       if (row_ok && col < a.Kp) store16(out_row + col, r);
@@ -226,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto stage_a = [&](int s, int pl) { return smem + s * Cfg::kStageBytes + pl * Cfg::kAPlaneBytes; };
   auto stage_b = [&](int s, int pl) {
     return smem + s * Cfg::kStageBytes + MAXPL * Cfg::kAPlaneBytes + pl * Cfg::kBPlaneBytes;
-  };
+  };  // B planes: [0] u_lo, [1] u_hi, [2] u'_lo, [3] u'_hi (16-bit) or [0] u
 
   if (warp == 0) {
     if (lane == 0) {
@@ -242,15 +240,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pos = (int)(rest % args.npos);
         const int res = (int)(rest / args.npos);
         const int pl = args.planes[res];
-        const uint32_t bytes = (uint32_t)(pl * (Cfg::kAPlaneBytes + Cfg::kBPlaneBytes));
+        const int upl = pl == 2 ? 4 : 1;
+        const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
         for (int kc = 0; kc < args.nkc; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], bytes);
-          for (int a = 0; a < pl; ++a) {
-            const int slab = (args.plane_base[res] + a) * args.npos + pos;
-            tma_load_3d(stage_a(stage, a), &tmV, &full[stage], kc * BC, pb * kBlockM, slab);
-            tma_load_3d(stage_b(stage, a), &tmU, &full[stage], kc * BC, kb * BN, slab);
-          }
+          for (int a = 0; a < pl; ++a)
+            tma_load_3d(stage_a(stage, a), &tmV, &full[stage], kc * BC, pb * kBlockM,
+                        (args.plane_base[res] + a) * args.npos + pos);
+          for (int b = 0; b < upl; ++b)
+            tma_load_3d(stage_b(stage, b), &tmU, &full[stage], kc * BC, kb * BN,
+                        (args.uplane_base[res] + b) * args.npos + pos);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -287,11 +287,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_i8(d0, da_lo, db_lo, idesc, acc);
             } else {
               const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
-              const uint64_t db_hi = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);
-              mma_i8(d0, da_hi, db_hi, idesc, acc);
-              mma_i8(d0 + BN, da_hi, db_lo, idesc, acc);
-              mma_i8(d0 + BN, da_lo, db_hi, idesc, 1u);
-              mma_i8(d0 + 2 * BN, da_lo, db_lo, idesc, acc);
+              const uint64_t db_uhi = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);
+              const uint64_t db_plo = umma_desc_kmajor(b0 + 2 * Cfg::kBPlaneBytes + 32 * k, BC);
+              const uint64_t db_phi = umma_desc_kmajor(b0 + 3 * Cfg::kBPlaneBytes + 32 * k, BC);
+              mma_i8(d0, da_hi, db_phi, idesc, acc);       // A256 = v_hi*u'_hi
+              mma_i8(d0, da_lo, db_uhi, idesc, 1u);        //      + v_lo*u_hi
+              mma_i8(d0 + BN, da_hi, db_plo, idesc, acc);  // A1   = v_hi*u'_lo
+              mma_i8(d0 + BN, da_lo, db_lo, idesc, 1u);    //      + v_lo*u_lo
             }
           }
           mma_commit(&empty[stage]);
@@ -366,11 +368,12 @@ bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t 
 int g_num_sms = 0;
 
 template <int BN, int BC, int MAXPL>
-cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, cudaStream_t s) {
+cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
+                     cudaStream_t s) {
   using Cfg = GemmConfig<BN, BC, MAXPL>;
   CUtensorMap tmV, tmU;
   if (!make_tmap(&tmV, V, a.Cp, a.P, (int64_t)n_planes * a.npos, BC, kBlockM)) return cudaErrorInvalidValue;
-  if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_planes * a.npos, BC, BN)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_uplanes * a.npos, BC, BN)) return cudaErrorInvalidValue;
   auto kern = winograd_gemm_kernel<BN, BC, MAXPL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
@@ -386,11 +389,12 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
 }
 
 template <int BN, int MAXPL>
-cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes, cudaStream_t s) {
+cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
+                        cudaStream_t s) {
   switch (bc) {
-    case 32: return run_gemm<BN, 32, MAXPL>(a, V, U, n_planes, s);
-    case 64: return run_gemm<BN, 64, MAXPL>(a, V, U, n_planes, s);
-    default: return run_gemm<BN, 128, MAXPL>(a, V, U, n_planes, s);
+    case 32: return run_gemm<BN, 32, MAXPL>(a, V, U, n_planes, n_uplanes, s);
+    case 64: return run_gemm<BN, 64, MAXPL>(a, V, U, n_planes, n_uplanes, s);
+    default: return run_gemm<BN, 128, MAXPL>(a, V, U, n_planes, n_uplanes, s);
   }
 }
 
@@ -412,6 +416,7 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   for (int r = 0; r < d.n_res; ++r) {
     a.planes[r] = d.res[r].planes;
     a.plane_base[r] = d.res[r].plane_base;
+    a.uplane_base[r] = d.res[r].uplane_base;
     a.modulus[r] = d.res[r].modulus;
     a.inv_m[r] = d.res[r].inv_m;
     a.r256[r] = d.res[r].r_256;
@@ -422,16 +427,27 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   }
   a.fast = (d.fast && Cp <= 8192) ? 1 : 0;
   a.fast2 = (a.fast && Cp <= 512) ? 1 : 0;
+  // 16-bit: 2 accumulators per set -> BN up to 128 with double-buffered TMEM;
+  // the channel chunk drops to 64 bytes so 4 pipeline stages fit (A 2 planes +
+  // B 4 planes per stage)
   int bn;
-  if (maxpl == 2) bn = 64;
+  if (maxpl == 2) bn = Kp <= 64 ? 64 : 128;
   else bn = Kp <= 64 ? 64 : (Kp <= 128 ? 128 : 256);
+  if (maxpl == 2 && bc > 64) {
+    bc = 64;
+    a.nkc = Cp / bc;
+  }
   a.num_pb = (int)((P + kBlockM - 1) / kBlockM);
   a.num_kb = (Kp + bn - 1) / bn;
   a.total_tiles = (int64_t)d.n_res * a.npos * a.num_pb * a.num_kb;
-  if (maxpl == 2) return run_gemm_bc<64, 2>(a, bc, V, U, d.n_planes, s);
-  if (bn == 64) return run_gemm_bc<64, 1>(a, bc, V, U, d.n_planes, s);
-  if (bn == 128) return run_gemm_bc<128, 1>(a, bc, V, U, d.n_planes, s);
-  return run_gemm_bc<256, 1>(a, bc, V, U, d.n_planes, s);
+  const int np = d.n_planes, nup = d.n_uplanes;
+  if (maxpl == 2) {
+    if (bn == 64) return run_gemm_bc<64, 2>(a, bc, V, U, np, nup, s);
+    return run_gemm_bc<128, 2>(a, bc, V, U, np, nup, s);
+  }
+  if (bn == 64) return run_gemm_bc<64, 1>(a, bc, V, U, np, nup, s);
+  if (bn == 128) return run_gemm_bc<128, 1>(a, bc, V, U, np, nup, s);
+  return run_gemm_bc<256, 1>(a, bc, V, U, np, nup, s);
 }
 
 }  // namespace rnsw

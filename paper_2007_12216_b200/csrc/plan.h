@@ -11,7 +11,9 @@
 struct ResidueTables {
   int32_t modulus;
   int32_t planes;      // 1: |v| <= 127 fits s8; 2: balanced hi/lo s8 limbs
-  int32_t plane_base;  // first limb-plane index of this residue in V / U
+  int32_t plane_base;  // first limb-plane index of this residue in V
+  int32_t uplanes;     // filter-bank planes: 1, or 4 = {U lo, U hi, U' lo, U' hi} with U' = 256*U mod m
+  int32_t uplane_base; // first plane of this residue in the filter bank U
   float inv_m;         // 1.0f / modulus
   int32_t r_256;       // 256 mod m (symmetric)
   int32_t r_65536;     // 65536 mod m (symmetric)
@@ -31,7 +33,8 @@ struct PlanDevice {
   int32_t r;      // R
   int32_t n;      // N = M + R - 1
   int32_t n_res;
-  int32_t n_planes;  // total limb planes over all residues
+  int32_t n_planes;  // total limb planes over all residues (V)
+  int32_t n_uplanes; // total filter-bank planes over all residues (U)
   int32_t fast;      // 1: tensor-core transform kernels apply (all m < 4500, D < 2^31)
   int64_t dynamic_range;
   int64_t signed_bound;

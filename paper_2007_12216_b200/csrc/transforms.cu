@@ -22,6 +22,23 @@ namespace {
 
 constexpr int kChanBlock = 32;  // channels per CTA in K1 / output channels in K4
 
+// Filter-bank planes of one residue: v itself (1 plane) for m < 256; for
+// 16-bit moduli the limbs of v and of v' = 256*v mod m (4 planes), so the
+// GEMM can form v_x*v_w with two accumulators (see gemm.cu).
+RNSW_DEV void store_uplanes(int8_t* base, int64_t plane_stride, const ResidueTables& t, int32_t v) {
+  if (t.uplanes == 1) {
+    base[0] = (int8_t)v;
+    return;
+  }
+  int8_t lo, hi;
+  split_limbs(v, lo, hi);
+  base[0] = lo;
+  base[plane_stride] = hi;
+  split_limbs(sym_mod(v * 256, t.modulus, t.inv_m), lo, hi);
+  base[2 * plane_stride] = lo;
+  base[3 * plane_stride] = hi;
+}
+
 // Write one symmetric residue as its limb plane(s).
 RNSW_DEV void store_planes(int8_t* base, int64_t plane_stride, int planes, int32_t v) {
   if (planes == 1) {
@@ -64,12 +81,12 @@ __global__ void filter_transform_kernel(const PlanDevice* __restrict__ plan, con
         tg[i * R + v] = sym_mod(s, m, inv);
       }
     const int64_t plane_stride = (int64_t)npos * K * Cp;
-    int8_t* ubase = U + (int64_t)t.plane_base * plane_stride + (int64_t)k * Cp + c;
+    int8_t* ubase = U + (int64_t)t.uplane_base * plane_stride + (int64_t)k * Cp + c;
     for (int i = 0; i < N; ++i)
       for (int j = 0; j < N; ++j) {
         int32_t s = 0;
         for (int v = 0; v < R; ++v) s += tg[i * R + v] * t.g[j * RNSW_MAX_R + v];
-        store_planes(ubase + (int64_t)(i * N + j) * K * Cp, plane_stride, t.planes, sym_mod(s, m, inv));
+        store_uplanes(ubase + (int64_t)(i * N + j) * K * Cp, plane_stride, t, sym_mod(s, m, inv));
       }
   }
 }
@@ -88,7 +105,7 @@ __global__ void filter_import_kernel(const PlanDevice* __restrict__ plan, int re
     const int k = (int)(rest % K);
     const int pos = (int)(rest / K);
     int32_t v = c < C ? sym_mod(src[((int64_t)pos * C + c) * K + k], t.modulus, t.inv_m) : 0;
-    store_planes(U + (int64_t)t.plane_base * plane_stride + idx, plane_stride, t.planes, v);
+    store_uplanes(U + (int64_t)t.uplane_base * plane_stride + idx, plane_stride, t, v);
   }
 }
 

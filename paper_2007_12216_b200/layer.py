@@ -252,10 +252,16 @@ class FilterBank(Mapping):
     def __len__(self) -> int:
         return len(self.moduli)
 
+    @staticmethod
+    def bank_planes(m) -> int:
+        """Planes per residue in the bank: u itself for m < 256; otherwise the
+        limbs of u and of 256*u mod m (consumed by the 2-accumulator GEMM)."""
+        return 1 if m < 256 else 4
+
     def planes_of(self, m) -> tuple[int, int]:
         base = 0
         for mod in self.moduli:
-            pl = 1 if mod < 256 else 2
+            pl = self.bank_planes(mod)
             if mod == m:
                 return base, pl
             base += pl
@@ -265,11 +271,12 @@ class FilterBank(Mapping):
         """(N, N, C, K) int16 symmetric residues of modulus m, on the GPU."""
         torch = _torch()
         n, c, k = self.n, self.c, self.k
-        cp = self.data.numel() // (self.plan.n_planes * n * n * k)
-        u = self.data.view(torch.int8).view(self.plan.n_planes, n * n, k, cp)[..., :c]
+        total = sum(self.bank_planes(mod) for mod in self.moduli)
+        cp = self.data.numel() // (total * n * n * k)
+        u = self.data.view(torch.int8).view(total, n * n, k, cp)[..., :c]
         base, pl = self.planes_of(m)
         v = u[base].to(torch.int16)
-        if pl == 2:
+        if pl > 1:
             v = u[base + 1].to(torch.int16) * 256 + v
         return v.permute(0, 2, 1).reshape(n, n, c, k).contiguous()
 
