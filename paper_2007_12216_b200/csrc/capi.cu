@@ -132,6 +132,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
   if (n < 2) return fail(RNSW_ERR_INVALID, "tile_m + r - 1 must be at least 2");
   if (n > RNSW_MAX_N || r > RNSW_MAX_R)
     return fail(RNSW_ERR_UNSUPPORTED, "F(%d,%d): tile side %d exceeds the device limit %d", tile_m, r, n, RNSW_MAX_N);
+  // (tensor-core transform kernels need N <= 16; larger tiles use the generic kernels)
   if (n_res < 1 || n_res > RNSW_MAX_RES)
     return fail(RNSW_ERR_UNSUPPORTED, "%d moduli: the device path takes 1..%d", n_res, RNSW_MAX_RES);
   for (int i = 0; i < n_res; ++i) {

@@ -3,7 +3,7 @@
 #include <cstdint>
 
 #define RNSW_MAX_RES 4   // residues per system
-#define RNSW_MAX_N 16    // tile side N = M + R - 1
+#define RNSW_MAX_N 24    // tile side N = M + R - 1 (tensor-core transforms: N <= 16)
 #define RNSW_MAX_R 8     // filter side
 
 // Constant tables one residue needs on the device, as int32 so kernels can

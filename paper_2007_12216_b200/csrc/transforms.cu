@@ -178,7 +178,8 @@ __global__ void __launch_bounds__(256) input_transform_kernel(const PlanDevice* 
 // K4-K6: output transform + MRC + scatter.  CTA = (tile p, 32 output channels).
 __global__ void __launch_bounds__(256) output_transform_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                const int16_t* __restrict__ Mw,
-                                                               int32_t* __restrict__ y, int16_t* __restrict__ y_res) {
+                                                               int32_t* __restrict__ y, int16_t* __restrict__ y_res,
+                                                               int kChanBlock) {
   extern __shared__ int32_t smem[];
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = plan->n_res;
   int32_t* S = smem;                           // [res][pos][k]
@@ -339,7 +340,7 @@ __global__ void requant_pool_vec4_kernel(const int4* __restrict__ y, int B, int 
 // The tensor-core output kernel is instantiated for uniform limb planes:
 // 1-2 residues of 16-bit moduli or 1-4 residues of 8-bit moduli.
 bool tc_output_ok(const PlanDevice& d) {
-  if (!d.fast) return false;
+  if (!d.fast || d.n > 16) return false;
   for (int r = 1; r < d.n_res; ++r)
     if (d.res[r].planes != d.res[0].planes) return false;
   return d.res[0].planes == 1 || d.n_res <= 2;
@@ -389,16 +390,19 @@ cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, con
                                     int16_t* y_res, cudaStream_t s) {
   if (tc_output_ok(plan.dev) && !force_generic()) return launch_output_transform_tc(plan, g, Mw, y, y_res, s);
   const int N = plan.dev.n, M = plan.dev.m_out, nres = plan.dev.n_res;
-  const size_t smem =
-      (size_t)(nres * N * N * kChanBlock + N * M * kChanBlock + nres * M * M * kChanBlock + nres * M * N) *
-      sizeof(int32_t);
+  int kcb = kChanBlock;
+  auto smem_for = [&](int cb) {
+    return (size_t)(nres * N * N * cb + N * M * cb + nres * M * M * cb + nres * M * N) * sizeof(int32_t);
+  };
+  while (kcb > 4 && smem_for(kcb) > 200 * 1024) kcb /= 2;  // large tiles / many residues
+  const size_t smem = smem_for(kcb);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(output_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
-  dim3 grid((unsigned)g.P, (g.K + kChanBlock - 1) / kChanBlock);
-  output_transform_kernel<<<grid, 256, smem, s>>>(plan.d_plan, g, Mw, y, y_res);
+  dim3 grid((unsigned)g.P, (g.K + kcb - 1) / kcb);
+  output_transform_kernel<<<grid, 256, smem, s>>>(plan.d_plan, g, Mw, y, y_res, kcb);
   return cudaGetLastError();
 }
 

@@ -186,3 +186,42 @@ def vgg16_bounds(weights, moduli=SYS16) -> list[int]:
 
     sb = (math.prod(moduli) - 1) // 2
     return [min(weight_bound(w, 127), sb) for w in weights]
+
+
+# ---------------------------------------------------------------------------
+# The reference's verification sweep (rw/cli.py:259-314): 12 (tile, filter)
+# shapes x 3 moduli sets x 7 seeded geometries, minus combinations whose
+# transform denominators share a factor with a modulus.
+
+VERIFY_SYSTEMS = ((253, 251, 247), (251, 241, 239), (4001, 4331))
+VERIFY_SHAPES = ((2, 3), (4, 3), (8, 3), (10, 3), (12, 3), (14, 3),
+                 (2, 5), (4, 5), (8, 5), (10, 5), (12, 5), (14, 5))
+
+
+def verify_cases(seed: int = DEFAULT_SEED) -> list[dict]:
+    from .transforms import cached_transforms, check_modulus_compatibility
+
+    geo = make_rng(seed, "geometry")
+    out = []
+    for tile_m, r in VERIFY_SHAPES:
+        ts = cached_transforms(tile_m, r)
+        for mods in VERIFY_SYSTEMS:
+            if not all(check_modulus_compatibility(ts, m) for m in mods):
+                continue
+            for g in range(7):
+                # draw order matters: h, w, c, k, padding, batch
+                h, w = int(geo.integers(r, 33)), int(geo.integers(r, 33))
+                c, k = int(geo.integers(1, 17)), int(geo.integers(1, 9))
+                pad, batch = int(geo.integers(0, 3)), int(geo.integers(1, 3))
+                out.append(dict(tile_m=tile_m, r=r, moduli=mods, h=h, w=w, c=c, k=k, pad=pad, batch=batch,
+                                entropy=(seed, tile_m, r, *mods, g)))
+    return out
+
+
+def verify_operands(case: dict):
+    """Weights then activations in [-127, 127] from the case's own stream
+    (rw/cli.py:317-322, 97-99)."""
+    rng = make_rng(*case["entropy"])
+    w = rng.integers(-127, 128, size=(case["r"], case["r"], case["c"], case["k"]), dtype=np.int8)
+    x = rng.integers(-127, 128, size=(case["batch"], case["h"], case["w"], case["c"]), dtype=np.int8)
+    return w, x

@@ -164,6 +164,30 @@ def gen_digests():
     return out
 
 
+def gen_verify():
+    """The reference's own 217-case verification sweep (rw/cli.py:278-334):
+    case list and a digest of every layer_conv output (== direct_conv)."""
+    from rnswinograd import cli
+
+    ref_cases = cli.default_verify_cases(2020)
+    mine = W.verify_cases(2020)
+    assert len(ref_cases) == len(mine)
+    out = []
+    for rc, mc in zip(ref_cases, mine):
+        sp = rc.spec
+        assert (sp.tile_m, sp.r, sp.h, sp.w, sp.c, sp.k, sp.padding, sp.batch) == (
+            mc["tile_m"], mc["r"], mc["h"], mc["w"], mc["c"], mc["k"], mc["pad"], mc["batch"])
+        rng = cli.make_rng(*rc.entropy)
+        w = cli.random_int8(rng, sp.weight_shape())
+        x = cli.random_int8(rng, sp.input_shape())
+        wm, xm = W.verify_operands(mc)
+        assert np.array_equal(w, wm) and np.array_equal(x, xm)
+        y = layer.layer_conv(sp, w, x, residue.RnsSystem(rc.moduli))
+        assert np.array_equal(y, layer.direct_conv(sp, w, x))
+        out.append(dict(label=rc.label, y=sha(y)))
+    return out
+
+
 def gen_scalars():
     out = {}
     for mods in [(251, 241, 239), (253, 251, 247), (4001, 4331), (7, 11, 13), (251, 4001)]:
@@ -187,6 +211,7 @@ def main():
     arrays, meta = gen_small()
     np.savez_compressed(HERE / "small_cases.npz", **arrays)
     (HERE / "small_cases.json").write_text(json.dumps(meta, indent=1))
+    (HERE / "verify.json").write_text(json.dumps(gen_verify(), indent=0))
     if "--no-digests" not in sys.argv:
         (HERE / "digests.json").write_text(json.dumps(gen_digests(), indent=1))
 

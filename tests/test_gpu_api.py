@@ -139,8 +139,8 @@ def test_errors_are_raised_before_device_work():
     with pytest.raises(rnsw.UnsupportedStride):
         rnsw.winograd_layer_conv(rnsw.LayerSpec(h=8, w=8, c=2, k=2, r=3, padding=1, stride=2, tile_m=4), w, x, sys8)
     with pytest.raises(rnsw.DeviceError):
-        # F(14,5): tile side 18 is outside the device path (N <= 16)
-        s18 = rnsw.LayerSpec(h=20, w=20, c=2, k=2, r=5, padding=2, tile_m=14)
+        # F(21,5): tile side 25 is outside the device path (N <= 24)
+        s18 = rnsw.LayerSpec(h=24, w=24, c=2, k=2, r=5, padding=2, tile_m=21)
         w18, x18 = _operands(s18, 2)
         rnsw.winograd_layer_conv(s18, w18, x18, rnsw.RnsSystem((4001, 4331)), declared_bound=1000)
 

@@ -52,9 +52,9 @@ def test_plan_validation_rejects_bad_arguments_before_device_work():
     rc = lib.rnsw_plan_create(ctypes.byref(h), 4, 3, 2, mods.ctypes.data_as(i32), z16.ctypes.data_as(i16),
                               z16.ctypes.data_as(i16), z16.ctypes.data_as(i16), inv.ctypes.data_as(i32))
     assert rc == 5  # share factor 7 -> RNSW_ERR_NOT_COPRIME
-    rc = lib.rnsw_plan_create(ctypes.byref(h), 16, 3, 1, mods.ctypes.data_as(i32), z16.ctypes.data_as(i16),
+    rc = lib.rnsw_plan_create(ctypes.byref(h), 23, 3, 1, mods.ctypes.data_as(i32), z16.ctypes.data_as(i16),
                               z16.ctypes.data_as(i16), z16.ctypes.data_as(i16), inv.ctypes.data_as(i32))
-    assert rc == 10  # N = 18 > 16 -> RNSW_ERR_UNSUPPORTED
+    assert rc == 10  # N = 25 > 24 -> RNSW_ERR_UNSUPPORTED
     assert b"exceeds" in lib.rnsw_last_error()
 
 

@@ -111,3 +111,21 @@ def test_config1_oracle_matches_reference_digest():
     assert sha(x) == d["x"] and sha(w) == d["w"]
     y = O.winograd_layer(x, w, case.pad, case.tile_m, case.moduli)
     assert sha(y) == d["y"]
+
+
+def test_verify_sweep_generation_and_oracle_sample():
+    """Case generation restates rw/cli.py:278-314 (checked against the
+    reference in make_golden); the oracle port reproduces a sample."""
+    import json
+
+    from golden_util import GOLDEN
+    from paper_2007_12216_b200 import workloads as W
+
+    gold = json.loads((GOLDEN / "verify.json").read_text())
+    cases = W.verify_cases(2020)
+    assert len(cases) == 217
+    for idx in range(0, 217, 23):
+        c = cases[idx]
+        w, x = W.verify_operands(c)
+        y = O.winograd_layer(x, w, c["pad"], c["tile_m"], c["moduli"])
+        assert sha(y) == gold[idx]["y"], gold[idx]["label"]
