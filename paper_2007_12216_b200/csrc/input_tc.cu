@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
     const uint32_t ahi0 = pack4_lo(limb_hi(av[0]), limb_hi(av[1]), limb_hi(av[2]), limb_hi(av[3]));
     const uint32_t ahi1 = pack4_lo(limb_hi(av[4]), limb_hi(av[5]), limb_hi(av[6]), limb_hi(av[7]));
     // pass-2 B: column i = g + 8 ni, k-slot e <-> a = {2t, 2t+1, 8+2t, 9+2t}[e]
-    uint32_t blo[2], bhi[2];
+    uint32_t blo[2], bhi[2], bplo[2], bphi[2];  // BT and BT' = 256*BT mod m (16-bit: 2 accumulators)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) {
       const int i = gq + 8 * ni;
@@ -125,6 +125,12 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       const int32_t v2 = bt[i * 16 + 8 + 2 * tq], v3 = bt[i * 16 + 9 + 2 * tq];
       blo[ni] = pack4_lo(v0, v1, v2, v3);
       bhi[ni] = pack4_lo(limb_hi(v0), limb_hi(v1), limb_hi(v2), limb_hi(v3));
+      if (planes == 2) {
+        const int32_t w0 = red_fast(v0 * 256, fm), w1 = red_fast(v1 * 256, fm);
+        const int32_t w2 = red_fast(v2 * 256, fm), w3 = red_fast(v3 * 256, fm);
+        bplo[ni] = pack4_lo(w0, w1, w2, w3);
+        bphi[ni] = pack4_lo(limb_hi(w0), limb_hi(w1), limb_hi(w2), limb_hi(w3));
+      }
     }
 
     uint32_t outw[2][8][4];  // [plane][position slot][channel word]
@@ -172,13 +178,13 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
           const uint32_t thi1 = pack4_lo(t[0][2] >> 8, t[0][3] >> 8, t[1][2] >> 8, t[1][3] >> 8);
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni) {
-            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {sbias, sbias, sbias, sbias};
-            imma_us(hh, thi0, thi1, bhi[ni]);
-            imma_us(cr, thi0, thi1, blo[ni]);
-            imma_us(cr, tlo0, tlo1, bhi[ni]);
-            imma_us(ll, tlo0, tlo1, blo[ni]);
+            int32_t a256[4] = {0, 0, 0, 0}, a1[4] = {sbias, sbias, sbias, sbias};
+            imma_us(a256, thi0, thi1, bphi[ni]);
+            imma_us(a256, tlo0, tlo1, bhi[ni]);
+            imma_us(a1, thi0, thi1, bplo[ni]);
+            imma_us(a1, tlo0, tlo1, blo[ni]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) v[ni][e] = red_pos_biased(hh[e] * 65536 + cr[e] * 256 + ll[e], fm) - fm.h;
+            for (int e = 0; e < 4; ++e) v[ni][e] = red_pos_biased(a256[e] * 256 + a1[e], fm) - fm.h;
           }
         } else {
 #pragma unroll
