@@ -153,6 +153,38 @@ class VGG16Rns:
             cur = nxt
         return cur
 
+    def graph(self, x):
+        """Capture forward_fused(x) for x's shape into a CUDA graph (buffers
+        are preallocated per batch size, so replays reuse the same pointers).
+        Returns a callable that copies new input into the captured input
+        buffer, replays, and returns the captured output tensor."""
+        torch = _torch()
+        batch = int(x.shape[0])
+        key = ("graph", batch)
+        if key not in self._buffers:
+            static_in = torch.empty_like(x)
+            static_in.copy_(x)
+            # warm up (lazy module loading, attribute setting) outside capture
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                for _ in range(2):
+                    self.forward_fused(static_in)
+            torch.cuda.current_stream().wait_stream(s)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                static_out = self.forward_fused(static_in)
+            self._buffers[key] = (g, static_in, static_out)
+        g, static_in, static_out = self._buffers[key]
+
+        def run(new_x=None):
+            if new_x is not None and new_x.data_ptr() != static_in.data_ptr():
+                static_in.copy_(new_x, non_blocking=True)
+            g.replay()
+            return static_out
+
+        return run
+
     def forward_fused_staged(self, x, record):
         """forward_fused() with a CUDA event pair around every kernel."""
         torch = _torch()
