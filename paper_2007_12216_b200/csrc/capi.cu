@@ -209,6 +209,11 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
       }
       d.mrc_inv[j][i] = inv;
     }
+  for (int j = 0; j < n_res; ++j)
+    for (int i = j - 1; i >= 0; --i) {
+      const int64_t mj = moduli[j], next = i == j - 1 ? 1 : d.mrc_w[j][i + 1];
+      d.mrc_w[j][i] = (int32_t)(((next * (d.mrc_inv[j][i] % mj)) % mj + mj) % mj);
+    }
   cudaError_t e = cudaGetDevice(&plan->host.device);
   if (e == cudaSuccess) e = cudaMalloc(&plan->host.d_plan, sizeof(PlanDevice));
   if (e == cudaSuccess) e = cudaMemcpy(plan->host.d_plan, &d, sizeof(d), cudaMemcpyHostToDevice);

@@ -2,7 +2,8 @@
 // every residue, mixed-radix reconstruction and crop/scatter, in one kernel
 // (rw/kernel.py:50-53, rw/residue.py:180-206, rw/layer.py:374-388).
 //
-// CTA = one tile p x 32 output channels, 4 warps x 8 channels.  The GEMM
+// CTA = a run of consecutive tiles p x 32 output channels, 4 warps x 8
+// channels; the transform constants are built once per CTA.  The GEMM
 // output Mw[p][res][pos][k] (int16 residues) is staged through shared memory
 // transposed to [res][k][pos] so each warp can feed one channel's 16x16
 // transform-domain tile straight into mma.sync fragments:
@@ -36,67 +37,43 @@ struct Requant {
   int pool;
 };
 
-// Both forms of the biased reduction give identical results; ptxas
-// schedules the fused instance better with n - q*m and the int32 instance
-// with q*(-m) + n (measured, profiles/r01_*).
-template <int kMode>
-RNSW_DEV int32_t red_k4(int32_t n, const FastMod& f) {
-  if constexpr (kMode == 1) return red_pos_biased_sub(n, f);
-  else return red_pos_biased(n, f);
-}
-
+// Reduction of the pass-2 sum for residue r to the mixed-radix digit d_r
+// (rw/residue.py:195-206 expanded): the pass-2 constants of residue r >= 1
+// carry the factor W[r][0], so the sum is y_r*W[r][0] and the digit is
+// (sum - sum_{i<r} d_i*W[r][i]) mod m_r in one reduction.  Bound: the limb
+// sum stays below 1.8e8 and the digit terms below 2.1e7, inside the 2^28
+// window of red_pos_biased for m < 4500.
 // kMode: 0 int32 output, 1 fused requant (int8), 2 per-residue debug output
 template <int NRES, int kPL, int kMode>
 __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                   const int16_t* __restrict__ Mw,
                                                                   int32_t* __restrict__ y,
-                                                                  int16_t* __restrict__ y_res, Requant rq) {
+                                                                  int16_t* __restrict__ y_res, Requant rq,
+                                                                  int tiles_per_cta) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = NRES;
   int16_t* S = reinterpret_cast<int16_t*>(smem_raw);  // [nres][kKB][kRowS]
   const int s_bytes = (nres * kKB * kRowS * 2 + 15) & ~15;
   int32_t* AT16 = reinterpret_cast<int32_t*>(smem_raw + s_bytes);  // [nres][16][16], zero padded
-  uint8_t* O8 = reinterpret_cast<uint8_t*>(AT16 + nres * 256);      // [pixel][kKB] int8 (fused requant)
+  int32_t* ATW16 = AT16 + nres * 256;                               // AT * W[r][0] mod m_r (pass 2)
+  uint8_t* O8 = reinterpret_cast<uint8_t*>(ATW16 + nres * 256);     // [pixel][kKB] int8 (fused requant)
+  constexpr bool kDigits = kMode != 2;  // pass 2 emits mixed-radix digits
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
-  const int64_t p = blockIdx.x;
-  const int k0 = blockIdx.y * kKB;
+  // grid (k-block, tile group): the k-blocks of one tile run side by side, so
+  // the row segments of Mw they split are read from DRAM once
+  const int k0 = blockIdx.x * kKB;
+  const int p_begin = blockIdx.y * tiles_per_cta;
+  const int p_end = min((int)g.P, p_begin + tiles_per_cta);
 
   for (int idx = tid; idx < nres * 256; idx += blockDim.x) {
     const int r = idx >> 8, a = (idx >> 4) & 15, j = idx & 15;
-    AT16[idx] = (a < M && j < N) ? plan->res[r].at[a * RNSW_MAX_N + j] : 0;
+    const int32_t at = (a < M && j < N) ? plan->res[r].at[a * RNSW_MAX_N + j] : 0;
+    AT16[idx] = at;
+    ATW16[idx] = (kDigits && r > 0) ? red_fast(at * plan->mrc_w[r][0], fast_mod_of(plan->res[r])) : at;
   }
-  if (N < 16) {
+  if (N < 16)  // staging never writes the padding rows/columns
     for (int idx = tid; idx < nres * kKB * kRowS / 2; idx += blockDim.x) reinterpret_cast<int32_t*>(S)[idx] = 0;
-    __syncthreads();
-  }
-  // stage: 16 B (8 channels) per load, 4 loads per (res, pos) row segment;
-  // idx walks the padded 16x16 grid so all index math is shifts.  Each
-  // thread issues its loads in batches of 8 before the transposing stores,
-  // so the global latency is paid once per batch, not once per load.
-  constexpr int kBatch = 8;
-  for (int base = tid; base < nres * 1024; base += kBatch * 128) {
-    int4 v[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int idx = base + u * 128;
-      const int kc = idx & 3, j = (idx >> 2) & 15, i = (idx >> 6) & 15, r = idx >> 10;
-      v[u] = make_int4(0, 0, 0, 0);
-      if (idx < nres * 1024 && i < N && j < N && k0 + 8 * kc < g.Kp)
-        v[u] = __ldg(reinterpret_cast<const int4*>(Mw + ((p * nres + r) * npos + i * N + j) * (int64_t)g.Kp + k0 +
-                                                   8 * kc));
-    }
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int idx = base + u * 128;
-      const int kc = idx & 3, j = (idx >> 2) & 15, i = (idx >> 6) & 15, r = idx >> 10;
-      if (idx >= nres * 1024 || i >= N || j >= N) continue;
-      const int16_t* e = reinterpret_cast<const int16_t*>(&v[u]);
-      int16_t* dst = S + (r * kKB + 8 * kc) * kRowS + stage_off(i, j);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) dst[q * kRowS] = e[q];
-    }
-  }
   __syncthreads();
 
   // Per-residue constants, built once per CTA: reduction parameters, the
@@ -106,14 +83,15 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   FastMod fmr[NRES];
   int plr[NRES];
   uint32_t A1lo[NRES][2], A1hi[NRES][2], B2lo[NRES][2], B2hi[NRES][2];
-  int32_t minv[NRES][NRES];
+  int32_t mw[NRES][NRES];
 #pragma unroll
   for (int r = 0; r < NRES; ++r) {
-        fmr[r] = fast_mod_of(plan->res[r]);
+    fmr[r] = fast_mod_of(plan->res[r]);
     plr[r] = plan->res[r].planes;
 #pragma unroll
-    for (int i2 = 0; i2 < NRES; ++i2) minv[r][i2] = i2 < r ? (int32_t)plan->mrc_inv[r][i2] : 0;
+    for (int i2 = 0; i2 < NRES; ++i2) mw[r][i2] = i2 < r ? plan->mrc_w[r][i2] : 0;
     const int32_t* at = AT16 + r * 256;
+    const int32_t* atw = ATW16 + r * 256;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int row = gq + 8 * h;
@@ -121,179 +99,232 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
       const int32_t v2 = at[row * 16 + 4 * tq + 2], v3 = at[row * 16 + 4 * tq + 3];
       A1lo[r][h] = pack4_lo(v0, v1, v2, v3);
       A1hi[r][h] = pack4_lo(limb_hi(v0), limb_hi(v1), limb_hi(v2), limb_hi(v3));
-      const int32_t u0 = at[row * 16 + 2 * tq], u1 = at[row * 16 + 2 * tq + 1];
-      const int32_t u2 = at[row * 16 + 8 + 2 * tq], u3 = at[row * 16 + 9 + 2 * tq];
+      const int32_t u0 = atw[row * 16 + 2 * tq], u1 = atw[row * 16 + 2 * tq + 1];
+      const int32_t u2 = atw[row * 16 + 8 + 2 * tq], u3 = atw[row * 16 + 9 + 2 * tq];
       B2lo[r][h] = pack4_lo(u0, u1, u2, u3);
       B2hi[r][h] = pack4_lo(limb_hi(u0), limb_hi(u1), limb_hi(u2), limb_hi(u3));
     }
   }
-  const int64_t signed_bound = plan->signed_bound, dyn_range = plan->dynamic_range;
+  const uint32_t signed_bound = (uint32_t)plan->signed_bound, dyn_range = (uint32_t)plan->dynamic_range;
 
-  const int b_img = (int)(p / (g.th * g.tw));
-  const int ti = (int)((p / g.tw) % g.th);
-  const int tj = (int)(p % g.tw);
   const int b_lo = gq, b_hi = gq + 8;  // pass-2 C rows = output column offset b
-  // Output addressing is fixed per lane: slot q -> pixel (a, b).  32-bit
-  // offsets from the tile origin (channel k0); -1 marks pixels outside the
-  // output plane.
-  int32_t out_off[8];
   const int32_t kstride = g.layout == 0 ? 1 : g.Ho * g.Wo;
-  int32_t* ytile = nullptr;
-  if (kMode == 0)
-    ytile = y + (g.layout == 0 ? (((int64_t)b_img * g.Ho + ti * M) * g.Wo + tj * M) * g.K + k0
-                               : (((int64_t)b_img * g.K + k0) * g.Ho + ti * M) * g.Wo + tj * M);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
-    const int b = (q & 2) ? b_hi : b_lo;
-    const bool ok = a < M && b < M && ti * M + a < g.Ho && tj * M + b < g.Wo;
-    out_off[q] = !ok ? -1 : (g.layout == 0 ? (a * g.Wo + b) * g.K : a * g.Wo + b);
-  }
-  for (int kk = 0; kk < kKB / 4; ++kk) {
-    const int k = warp * (kKB / 4) + kk;
-    const bool kvalid = k0 + k < g.K;
-    int32_t yv[NRES][8];
-#pragma unroll
+
+  // staging slots of this thread (see the staging loop)
+  const int st_kc = tid & 3, st_j = (tid >> 2) & 15, st_i0 = tid >> 6;
+  const bool st_j_in = st_j < N;
+  const bool st_ok = st_j_in && k0 + 8 * st_kc < g.Kp;
+  const int st_urows = (N - st_i0 + 1) >> 1;  // rows i0 + 2u < N
+  const int st_src = (st_i0 * N + st_j) * g.Kp + k0 + 8 * st_kc;
+  int16_t* st_dst = S + 8 * st_kc * kRowS + stage_off(st_i0, st_j);
+
+  for (int p = p_begin; p < p_end; ++p) {
+    // stage: 16 B (8 channels) per load.  Thread t owns channel group
+    // kc = t & 3 and column j = (t >> 2) & 15 of rows i = (t >> 6) + 2u,
+    // u = 0..7, for every residue, so all addressing is per-thread constants
+    // plus compile-time offsets.  Loads go out in groups of 4 ahead of their
+    // transposing stores.
+    const int16_t* src = Mw + (int64_t)p * nres * npos * g.Kp + st_src;
+#pragma unroll 1
     for (int r = 0; r < NRES; ++r) {
-            const int16_t* row = S + (r * kKB + k) * kRowS;
-      const FastMod fm = fmr[r];
-      int32_t z[2][4];
-      if (kPL == 2) {
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          const int i = gq + 8 * ni;
-          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq));
-          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq) + 2);
-          const uint32_t blo = __byte_perm(w0, w1, 0x6420);  // u8 low bytes
-          const uint32_t bhi = __byte_perm(w0, w1, 0x7531);  // s8 high bytes
-          const int32_t bias = pos_bias(fm);
-          int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {bias, bias, bias, bias};
-          imma_ss(hh, A1hi[r][0], A1hi[r][1], bhi);
-          imma_su(cr, A1hi[r][0], A1hi[r][1], blo);
-          imma_ss(cr, A1lo[r][0], A1lo[r][1], bhi);
-          imma_su(ll, A1lo[r][0], A1lo[r][1], blo);
+      for (int half = 0; half < 2; ++half) {
+        int4 v[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) z[ni][e] = red_k4<kMode>(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+        for (int w = 0; w < 4; ++w) {
+          const int u = 4 * half + w;
+          v[w] = make_int4(0, 0, 0, 0);
+          if (st_ok && u < st_urows) v[w] = __ldg(reinterpret_cast<const int4*>(src + (r * npos + 2 * u * N) * g.Kp));
         }
-      } else {
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          const int i = gq + 8 * ni;
-          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq));
-          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq) + 2);
-          const uint32_t b = __byte_perm(w0, w1, 0x6420);  // residues fit s8
-          const int32_t bias = pos_bias(fm);
-          int32_t acc[4] = {bias, bias, bias, bias};
-          imma_ss(acc, A1lo[r][0], A1lo[r][1], b);
+        for (int w = 0; w < 4; ++w) {
+          const int u = 4 * half + w;
+          if (!(st_j_in && u < st_urows)) continue;
+          const int16_t* e = reinterpret_cast<const int16_t*>(&v[w]);
+          int16_t* dst = st_dst + r * kKB * kRowS + 32 * u + 2 * (u >> 1);  // stage_off(i0 + 2u, j)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) z[ni][e] = red_k4<kMode>(acc[e], fm);
-        }
-      }
-      // pass 2: A = Z^T (rows b = g / g+8; k-slots <- columns i of pass 1)
-      if (kPL == 2) {
-        // z in [0, m): u8 low byte, high part z >> 8 in [0, 23]
-        const uint32_t zlo0 = pack4_lo(z[0][0], z[0][1], z[1][0], z[1][1]);
-        const uint32_t zlo1 = pack4_lo(z[0][2], z[0][3], z[1][2], z[1][3]);
-        const uint32_t zhi0 = pack4_lo(z[0][0] >> 8, z[0][1] >> 8, z[1][0] >> 8, z[1][1] >> 8);
-        const uint32_t zhi1 = pack4_lo(z[0][2] >> 8, z[0][3] >> 8, z[1][2] >> 8, z[1][3] >> 8);
-        const int32_t bias = pos_bias(fm);
-#pragma unroll
-        for (int na = 0; na < 2; ++na) {
-          int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {bias, bias, bias, bias};
-          imma_us(hh, zhi0, zhi1, B2hi[r][na]);
-          imma_us(cr, zhi0, zhi1, B2lo[r][na]);
-          imma_us(cr, zlo0, zlo1, B2hi[r][na]);
-          imma_us(ll, zlo0, zlo1, B2lo[r][na]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_k4<kMode>(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
-        }
-      } else {
-        // z in [0, m < 256): u8
-        const uint32_t za0 = pack4_lo(z[0][0], z[0][1], z[1][0], z[1][1]);
-        const uint32_t za1 = pack4_lo(z[0][2], z[0][3], z[1][2], z[1][3]);
-        const int32_t bias = pos_bias(fm);
-#pragma unroll
-        for (int na = 0; na < 2; ++na) {
-          int32_t acc[4] = {bias, bias, bias, bias};
-          imma_us(acc, za0, za1, B2lo[r][na]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) yv[r][4 * na + e] = red_k4<kMode>(acc[e], fm);
+          for (int q = 0; q < 8; ++q) dst[q * kRowS] = e[q];
         }
       }
     }
-    // yv[r][4*na + e]: a = 8*na + 2t + (e & 1), b = g + 8*(e >> 1)
-    int32_t qv[8];
+    __syncthreads();
+
+    const int b_img = p / (g.th * g.tw);
+    const int ti = (p / g.tw) % g.th;
+    const int tj = p % g.tw;
+    // Output addressing is fixed per lane: slot q -> pixel (a, b).  32-bit
+    // offsets from the tile origin (channel k0); -1 marks pixels outside the
+    // output plane.
+    int32_t out_off[8];
+    int32_t* ytile = nullptr;
+    if (kMode == 0)
+      ytile = y + (g.layout == 0 ? (((int64_t)b_img * g.Ho + ti * M) * g.Wo + tj * M) * g.K + k0
+                                 : (((int64_t)b_img * g.K + k0) * g.Ho + ti * M) * g.Wo + tj * M);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      if constexpr (kMode == 2) {
-        const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
-        const int b = (q & 2) ? b_hi : b_lo;
-        if (a < M && b < M && k0 + k < g.K) {
+      const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
+      const int b = (q & 2) ? b_hi : b_lo;
+      const bool ok = a < M && b < M && ti * M + a < g.Ho && tj * M + b < g.Wo;
+      out_off[q] = !ok ? -1 : (g.layout == 0 ? (a * g.Wo + b) * g.K : a * g.Wo + b);
+    }
+    for (int kk = 0; kk < kKB / 4; ++kk) {
+      const int k = warp * (kKB / 4) + kk;
+      const bool kvalid = k0 + k < g.K;
+      int32_t yv[NRES][8];
 #pragma unroll
-          for (int r = 0; r < NRES; ++r) {
-            const int32_t v = yv[r][q] > fmr[r].h ? yv[r][q] - fmr[r].m : yv[r][q];
-            y_res[(((int64_t)r * g.P + p) * g.K + k0 + k) * M * M + a * M + b] = (int16_t)v;
+      for (int r = 0; r < NRES; ++r) {
+      const int16_t* row = S + (r * kKB + k) * kRowS;
+        const FastMod fm = fmr[r];
+        int32_t z[2][4];
+        if (kPL == 2) {
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            const int i = gq + 8 * ni;
+            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq));
+            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq) + 2);
+            const uint32_t blo = __byte_perm(w0, w1, 0x6420);  // u8 low bytes
+            const uint32_t bhi = __byte_perm(w0, w1, 0x7531);  // s8 high bytes
+            const int32_t bias = pos_bias(fm);
+            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {bias, bias, bias, bias};
+            imma_ss(hh, A1hi[r][0], A1hi[r][1], bhi);
+            imma_su(cr, A1hi[r][0], A1hi[r][1], blo);
+            imma_ss(cr, A1lo[r][0], A1lo[r][1], bhi);
+            imma_su(ll, A1lo[r][0], A1lo[r][1], blo);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+          }
+        } else {
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            const int i = gq + 8 * ni;
+            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq));
+            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq) + 2);
+            const uint32_t b = __byte_perm(w0, w1, 0x6420);  // residues fit s8
+            const int32_t bias = pos_bias(fm);
+            int32_t acc[4] = {bias, bias, bias, bias};
+            imma_ss(acc, A1lo[r][0], A1lo[r][1], b);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased(acc[e], fm);
           }
         }
-      } else {
-        // mixed-radix reconstruction (rw/residue.py:195-206) from digits in
-        // [0, m_j) (yv holds y mod m_j), exact in uint32 for D < 2^31
-        uint32_t x = (uint32_t)yv[0][q], radix = (uint32_t)fmr[0].m;
-        int32_t d[NRES];
-        d[0] = yv[0][q];
+        // pass 2: A = Z^T (rows b = g / g+8; k-slots <- columns i of pass 1)
+        if (kPL == 2) {
+          // z in [0, m): u8 low byte, high part z >> 8 in [0, 23]
+          const uint32_t zlo0 = pack4_lo(z[0][0], z[0][1], z[1][0], z[1][1]);
+          const uint32_t zlo1 = pack4_lo(z[0][2], z[0][3], z[1][2], z[1][3]);
+          const uint32_t zhi0 = pack4_lo(z[0][0] >> 8, z[0][1] >> 8, z[1][0] >> 8, z[1][1] >> 8);
+          const uint32_t zhi1 = pack4_lo(z[0][2] >> 8, z[0][3] >> 8, z[1][2] >> 8, z[1][3] >> 8);
+          const int32_t bias = pos_bias(fm);
 #pragma unroll
-        for (int j = 1; j < NRES; ++j) {
-          int32_t t = yv[j][q];
+          for (int na = 0; na < 2; ++na) {
+            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {bias, bias, bias, bias};
+            imma_us(hh, zhi0, zhi1, B2hi[r][na]);
+            imma_us(cr, zhi0, zhi1, B2lo[r][na]);
+            imma_us(cr, zlo0, zlo1, B2hi[r][na]);
+            imma_us(ll, zlo0, zlo1, B2lo[r][na]);
 #pragma unroll
-          for (int i2 = 0; i2 < j; ++i2) t = red_pos((t - d[i2]) * minv[j][i2], fmr[j]);
-          d[j] = t;
-          x += radix * (uint32_t)t;
-          radix *= (uint32_t)fmr[j].m;
+            for (int e = 0; e < 4; ++e) {
+              int32_t n = hh[e] * 65536 + cr[e] * 256 + ll[e];
+              if constexpr (kDigits) {
+#pragma unroll
+                for (int i2 = 0; i2 < r; ++i2) n -= yv[i2][4 * na + e] * mw[r][i2];
+              }
+              yv[r][4 * na + e] = red_pos_biased(n, fm);
+            }
+          }
+        } else {
+          // z in [0, m < 256): u8
+          const uint32_t za0 = pack4_lo(z[0][0], z[0][1], z[1][0], z[1][1]);
+          const uint32_t za1 = pack4_lo(z[0][2], z[0][3], z[1][2], z[1][3]);
+          const int32_t bias = pos_bias(fm);
+#pragma unroll
+          for (int na = 0; na < 2; ++na) {
+            int32_t acc[4] = {bias, bias, bias, bias};
+            imma_us(acc, za0, za1, B2lo[r][na]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              int32_t n = acc[e];
+              if constexpr (kDigits) {
+#pragma unroll
+                for (int i2 = 0; i2 < r; ++i2) n -= yv[i2][4 * na + e] * mw[r][i2];
+              }
+              yv[r][4 * na + e] = red_pos_biased(n, fm);
+            }
+          }
         }
-        const int32_t v = (int64_t)x > signed_bound ? (int32_t)((int64_t)x - dyn_range) : (int32_t)x;
-        if constexpr (kMode == 1) {
-          qv[q] = min(v > 0 ? v >> rq.shift : 0, 127);
-        } else if (out_off[q] >= 0 && kvalid) {
-          // direct store: over this warp's 8 channels each pixel receives one
-          // complete 32-byte sector (NHWC), merged in L2
-          ytile[out_off[q] + k * kstride] = v;
+      }
+      // yv[r][4*na + e]: a = 8*na + 2t + (e & 1), b = g + 8*(e >> 1)
+      int32_t qv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if constexpr (kMode == 2) {
+          const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
+          const int b = (q & 2) ? b_hi : b_lo;
+          if (a < M && b < M && k0 + k < g.K) {
+#pragma unroll
+            for (int r = 0; r < NRES; ++r) {
+              const int32_t v = yv[r][q] > fmr[r].h ? yv[r][q] - fmr[r].m : yv[r][q];
+              y_res[(((int64_t)r * g.P + p) * g.K + k0 + k) * M * M + a * M + b] = (int16_t)v;
+            }
+          }
+        } else {
+          // mixed-radix reconstruction (rw/residue.py:195-206): yv holds the
+          // digits d_j in [0, m_j); x = sum d_j prod_{i<j} m_i is exact in
+          // uint32 for D < 2^31
+          uint32_t x = (uint32_t)yv[0][q], radix = (uint32_t)fmr[0].m;
+#pragma unroll
+          for (int j = 1; j < NRES; ++j) {
+            x += radix * (uint32_t)yv[j][q];
+            radix *= (uint32_t)fmr[j].m;
+          }
+          const bool neg = x > signed_bound;
+          const int32_t v = (int32_t)(neg ? x - dyn_range : x);
+          if constexpr (kMode == 1) {
+            qv[q] = neg ? 0 : min((int32_t)(x >> rq.shift), 127);  // relu, >> shift, clip
+          } else if (out_off[q] >= 0 && kvalid) {
+            // direct store: over this warp's 8 channels each pixel receives one
+            // complete 32-byte sector (NHWC), merged in L2
+            ytile[out_off[q] + k * kstride] = v;
+          }
+        }
+      }
+      if (kMode == 1) {
+        if (rq.pool) {
+          // pairs along a (q, q^1) share a lane; pairs along b are lanes 4 apart
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            int32_t m2 = max(qv[2 * h], qv[2 * h + 1]);
+            m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 4));
+            const int a = 8 * (h >> 1) + 2 * tq;  // even row of the pair
+            const int b = (h & 1) ? b_hi : b_lo;
+            if ((gq & 1) == 0 && a < M && b < M) O8[((a >> 1) * (M >> 1) + (b >> 1)) * kKB + k] = (uint8_t)m2;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
+            const int b = (q & 2) ? b_hi : b_lo;
+            if (a < M && b < M) O8[(a * M + b) * kKB + k] = (uint8_t)qv[q];
+          }
         }
       }
     }
     if (kMode == 1) {
-      if (rq.pool) {
-        // pairs along a (q, q^1) share a lane; pairs along b are lanes 4 apart
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          int32_t m2 = max(qv[2 * h], qv[2 * h + 1]);
-          m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 4));
-          const int a = 8 * (h >> 1) + 2 * tq;  // even row of the pair
-          const int b = (h & 1) ? b_hi : b_lo;
-          if ((gq & 1) == 0 && a < M && b < M) O8[((a >> 1) * (M >> 1) + (b >> 1)) * kKB + k] = (uint8_t)m2;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int a = 8 * (q >> 2) + 2 * tq + (q & 1);
-          const int b = (q & 2) ? b_hi : b_lo;
-          if (a < M && b < M) O8[(a * M + b) * kKB + k] = (uint8_t)qv[q];
-        }
+      __syncthreads();
+      // int8 NHWC rows of kKB channels (4-byte words)
+      const int side = rq.pool ? (M >> 1) : M;
+      const int Ho = rq.pool ? g.Ho / 2 : g.Ho, Wo = rq.pool ? g.Wo / 2 : g.Wo;
+      const int kw = min(kKB, g.K - k0);
+      for (int idx = tid; idx < side * side * (kKB / 4); idx += blockDim.x) {
+        const int wq = idx % (kKB / 4), pix = idx / (kKB / 4);
+        const int a = pix / side, b = pix - a * side;
+        const int ho = ti * side + a, wo = tj * side + b;
+        if (ho >= Ho || wo >= Wo || 4 * wq >= kw) continue;
+        const uint32_t word = *reinterpret_cast<const uint32_t*>(O8 + pix * kKB + 4 * wq);
+        *reinterpret_cast<uint32_t*>(rq.out + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 4 * wq) = word;
       }
-    }
-  }
-  if (kMode == 1) {
-    __syncthreads();
-    // int8 NHWC rows of kKB channels (4-byte words)
-    const int side = rq.pool ? (M >> 1) : M;
-    const int Ho = rq.pool ? g.Ho / 2 : g.Ho, Wo = rq.pool ? g.Wo / 2 : g.Wo;
-    const int kw = min(kKB, g.K - k0);
-    for (int idx = tid; idx < side * side * (kKB / 4); idx += blockDim.x) {
-      const int wq = idx % (kKB / 4), pix = idx / (kKB / 4);
-      const int a = pix / side, b = pix - a * side;
-      const int ho = ti * side + a, wo = tj * side + b;
-      if (ho >= Ho || wo >= Wo || 4 * wq >= kw) continue;
-      const uint32_t word = *reinterpret_cast<const uint32_t*>(O8 + pix * kKB + 4 * wq);
-      *reinterpret_cast<uint32_t*>(rq.out + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 4 * wq) = word;
+    } else {
+      __syncthreads();  // S is restaged for the next tile
     }
   }
 }
@@ -301,17 +332,22 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
 }  // namespace
 
 size_t output_tc_smem(const PlanDevice& d) {
-  return (size_t)((d.n_res * kKB * kRowS * 2 + 15) & ~15) + d.n_res * 256 * 4 + (size_t)d.m_out * d.m_out * kKB;
+  return (size_t)((d.n_res * kKB * kRowS * 2 + 15) & ~15) + d.n_res * 512 * 4 + (size_t)d.m_out * d.m_out * kKB;
 }
 
 cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
                                        int16_t* y_res, cudaStream_t s, int8_t* out8, int shift, int pool) {
   const Requant rq{out8, shift, pool};
   const size_t smem = output_tc_smem(plan.dev);
-  dim3 grid((unsigned)g.P, (g.K + kKB - 1) / kKB);
+  // a few tiles per CTA amortise the per-CTA constant set-up, keeping at
+  // least ~4 waves of 4 CTAs per SM
+  const int kblocks = (g.K + kKB - 1) / kKB;
+  const int64_t units = g.P * kblocks;
+  const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(8, units / (148 * 4 * 4)));
+  dim3 grid(kblocks, (unsigned)((g.P + tpc - 1) / tpc));
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res, rq);
+    kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res, rq, tpc);
     return 0;
   };
   const int mode = y_res != nullptr ? 2 : (out8 != nullptr ? 1 : 0);

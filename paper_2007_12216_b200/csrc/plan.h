@@ -39,5 +39,8 @@ struct PlanDevice {
   int64_t dynamic_range;
   int64_t signed_bound;
   int64_t mrc_inv[RNSW_MAX_RES][RNSW_MAX_RES];  // m_i^-1 mod m_j, i < j
+  // Expanded mixed-radix weights: digit d_j = y_j*W[j][0] - sum_{i<j} d_i*W[j][i]
+  // (mod m_j), W[j][i] = prod_{k=i}^{j-1} m_k^-1 mod m_j, in [0, m_j).
+  int32_t mrc_w[RNSW_MAX_RES][RNSW_MAX_RES];
   ResidueTables res[RNSW_MAX_RES];
 };
