@@ -11,6 +11,8 @@
  *                              (rw/layer.py:161-174, rw/kernel.py:38-41)
  *   rnsw_input_transform    <- _modulus_pass part 1: residue_encode_array +
  *                              input_transform_mod  (rw/layer.py:278-283)
+ *   rnsw_input_transform_compact, rnsw_small_channel_product
+ *                           <- the same two steps for C <= 4 input channels
  *   rnsw_winograd_gemm      <- _modulus_pass GEMM loop / _modular_gemm
  *                              (rw/layer.py:251-263, 285-291)
  *   rnsw_output_residues    <- _modulus_pass part 2: backward_transform_mod
@@ -94,6 +96,17 @@ int rnsw_filter_import(const rnsw_plan* plan, int res, const int16_t* u_nnck, in
 /* Stage 1: V = BT d B mod m_i for every tile and channel -> [plane][N*N][P][Cp]. */
 int rnsw_input_transform(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C,
                          int pad, int layout, void* V, size_t V_bytes, void* stream);
+/* Small-channel stages 1 + 2 (C <= 4 on a tensor-core plan, e.g. VGG16
+ * conv1_1): the split rnsw_conv_forward takes for such layers.  Stage 1
+ * writes compact symmetric residues V16[n_res][P][N*N][4] int16
+ * (n_res * P * N*N * 8 bytes; same math as rnsw_input_transform,
+ * rw/layer.py:278-283); stage 2 forms M = sum_c V U mod m_i on the CUDA cores
+ * into the rnsw_winograd_gemm output layout (rw/layer.py:366-372).
+ * RNSW_ERR_UNSUPPORTED when C > 4 or the plan is not a tensor-core plan. */
+int rnsw_input_transform_compact(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C,
+                                 int pad, int layout, void* V16, size_t V16_bytes, void* stream);
+int rnsw_small_channel_product(const rnsw_plan* plan, const void* V16, const void* U, int64_t P, int C,
+                               int K, void* Mw, size_t Mw_bytes, void* stream);
 /* Stage 2: per (residue, position) GEMM on tcgen05 kind::i8, reduced mod m_i
  * -> Winograd-domain product residues [P][n_res][N*N][Kp] int16. */
 int rnsw_winograd_gemm(const rnsw_plan* plan, const void* V, const void* U, int64_t P, int C,

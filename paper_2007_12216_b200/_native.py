@@ -37,6 +37,10 @@ _SIGNATURES = {
     "rnsw_filter_import": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p]),
     "rnsw_input_transform": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                      c_size_t, c_void_p]),
+    "rnsw_input_transform_compact": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                                             c_void_p, c_size_t, c_void_p]),
+    "rnsw_small_channel_product": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p,
+                                           c_size_t, c_void_p]),
     "rnsw_winograd_gemm": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_size_t,
                                    c_void_p]),
     "rnsw_output_transform": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,

@@ -175,6 +175,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
       t.red_shift = sh;
       const int64_t L = ((1LL << 28) + m - 1) / m;
       t.red_off = (int32_t)(half + m * L);
+      t.red_negm = (uint32_t)(-(int64_t)m);
     }
     auto load = [&](const int16_t* src, int rows, int cols, int stride, int32_t* dst) -> bool {
       for (int a = 0; a < rows; ++a)
@@ -296,6 +297,41 @@ int rnsw_input_transform(const rnsw_plan* plan, const int8_t* x, int B, int H, i
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "input_transform");
 }
 
+int rnsw_input_transform_compact(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int pad,
+                                 int layout, void* V16, size_t V16_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (x == nullptr || V16 == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, C, 1, pad, layout, &g)) return rc;
+  if (!rnsw::smallc_ok(plan->host.dev, g))
+    return fail(RNSW_ERR_UNSUPPORTED, "compact transform needs C <= 4 and a tensor-core plan (C=%d)", C);
+  if (V16_bytes < rnsw::smallc_v16_bytes(plan->host.dev, g)) return fail(RNSW_ERR_WORKSPACE, "V16 buffer too small");
+  cudaError_t e = rnsw::launch_input_transform_compact(plan->host, g, x, static_cast<int16_t*>(V16),
+                                                       (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "input_transform_compact");
+}
+
+int rnsw_small_channel_product(const rnsw_plan* plan, const void* V16, const void* U, int64_t P, int C, int K,
+                               void* Mw, size_t Mw_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (V16 == nullptr || U == nullptr || Mw == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (P < 1 || P > 2147483647LL || C < 1 || K < 1) return fail(RNSW_ERR_SHAPE, "bad product shape P=%lld C=%d K=%d",
+                                                          (long long)P, C, K);
+  rnsw::Geometry g{};
+  g.P = P;
+  g.C = C;
+  g.K = K;
+  g.Cp = padded_channels(C);
+  g.Kp = (int)round_up(K, 16);
+  if (!rnsw::smallc_ok(plan->host.dev, g))
+    return fail(RNSW_ERR_UNSUPPORTED, "small-channel product needs C <= 4 and a tensor-core plan (C=%d)", C);
+  if (Mw_bytes < m_bytes(plan->host.dev, P, g.Kp)) return fail(RNSW_ERR_WORKSPACE, "Mw buffer too small");
+  cudaError_t e = rnsw::launch_smallc_product(plan->host, g, static_cast<const int16_t*>(V16),
+                                              static_cast<const int8_t*>(U), static_cast<int16_t*>(Mw),
+                                              (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "small_channel_product");
+}
+
 int rnsw_winograd_gemm(const rnsw_plan* plan, const void* V, const void* U, int64_t P, int C, int K, void* Mw,
                        size_t Mw_bytes, void* stream) {
   if (int rc = check_plan(plan)) return rc;
@@ -340,6 +376,26 @@ int rnsw_output_residues(const rnsw_plan* plan, const void* Mw, int64_t P, int K
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_residues");
 }
 
+namespace {
+// K1 + K3 of a whole-layer call: the tensor-core GEMM path, or for C <= 4
+// the compact transform + CUDA-core product (smallc.cu), into Mw.
+int transform_and_product(const rnsw_plan* plan, const rnsw::Geometry& g, const int8_t* x, const void* U, int8_t* V,
+                          int16_t* Mw, cudaStream_t s) {
+  cudaError_t e;
+  if (rnsw::smallc_ok(plan->host.dev, g) && !rnsw::force_generic()) {
+    int16_t* V16 = reinterpret_cast<int16_t*>(V);
+    e = rnsw::launch_input_transform_compact(plan->host, g, x, V16, s);
+    if (e != cudaSuccess) return cuda_fail(e, "input_transform_compact");
+    e = rnsw::launch_smallc_product(plan->host, g, V16, static_cast<const int8_t*>(U), Mw, s);
+    return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "smallc_product");
+  }
+  e = rnsw::launch_input_transform(plan->host, g, x, V, s);
+  if (e != cudaSuccess) return cuda_fail(e, "input_transform");
+  e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, g.K, g.Kp, g.bc, Mw, s);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "winograd_gemm");
+}
+}  // namespace
+
 int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad, int layout,
                       const void* U, int32_t* y, void* workspace, size_t workspace_bytes, void* stream) {
   if (int rc = check_plan(plan)) return rc;
@@ -354,11 +410,8 @@ int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int 
   int8_t* V = static_cast<int8_t*>(workspace);
   int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = rnsw::launch_input_transform(plan->host, g, x, V, s);
-  if (e != cudaSuccess) return cuda_fail(e, "input_transform");
-  e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, K, g.Kp, g.bc, Mw, s);
-  if (e != cudaSuccess) return cuda_fail(e, "winograd_gemm");
-  e = rnsw::launch_output_transform(plan->host, g, Mw, y, nullptr, s);
+  if (int rc = transform_and_product(plan, g, x, U, V, Mw, s)) return rc;
+  cudaError_t e = rnsw::launch_output_transform(plan->host, g, Mw, y, nullptr, s);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform");
 }
 
@@ -383,11 +436,8 @@ int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int
   int8_t* V = static_cast<int8_t*>(workspace);
   int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
   cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = rnsw::launch_input_transform(plan->host, g, x, V, s);
-  if (e != cudaSuccess) return cuda_fail(e, "input_transform");
-  e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, K, g.Kp, g.bc, Mw, s);
-  if (e != cudaSuccess) return cuda_fail(e, "winograd_gemm");
-  e = rnsw::launch_output_transform_tc(plan->host, g, Mw, nullptr, nullptr, s, out, shift, pool);
+  if (int rc = transform_and_product(plan, g, x, U, V, Mw, s)) return rc;
+  cudaError_t e = rnsw::launch_output_transform_tc(plan->host, g, Mw, nullptr, nullptr, s, out, shift, pool);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant");
 }
 

@@ -54,7 +54,7 @@ struct FastMod {
 };
 
 RNSW_DEV FastMod fast_mod_of(const ResidueTables& t) {
-  return FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half, (uint32_t)(-t.modulus)};
+  return FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half, t.red_negm};
 }
 
 RNSW_DEV int32_t red_fast(int32_t x, const FastMod& f) {

@@ -34,7 +34,10 @@ RNSW_DEV void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, u
 
 RNSW_DEV uint32_t word_of(const uint4& v, int u) { return u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w; }
 
-template <int kPL>
+// kCompact (C <= 4, the small-channel path of smallc.cu): each warp owns one
+// tile and writes its 4 channels as symmetric int16 residues to
+// V16[res][P][pos][4] instead of the GEMM limb planes.
+template <int kPL, bool kCompact>
 __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                  const int8_t* __restrict__ x,
                                                                  int8_t* __restrict__ V) {
@@ -42,14 +45,15 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = plan->n_res;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   const int ncb = (g.Cp + kCTAChannels - 1) / kCTAChannels;
-  const int64_t p = blockIdx.x / ncb;  // channel blocks of one tile are adjacent in launch order
-  const int c_base = (int)(blockIdx.x % ncb) * kCTAChannels + warp * 16;
+  // channel blocks of one tile are adjacent in launch order
+  const int64_t p = kCompact ? (int64_t)blockIdx.x * 4 + warp : blockIdx.x / ncb;
+  const int c_base = kCompact ? 0 : (int)(blockIdx.x % ncb) * kCTAChannels + warp * 16;
   for (int idx = tid; idx < nres * 256; idx += blockDim.x) {
     const int r = idx >> 8, a = (idx >> 4) & 15, b = idx & 15;
     BT16[idx] = (a < N && b < N) ? plan->res[r].bt[a * RNSW_MAX_N + b] : 0;
   }
   __syncthreads();
-  if (c_base >= g.Cp) return;
+  if (kCompact ? p >= g.P : c_base >= g.Cp) return;
   const int b_img = (int)(p / (g.th * g.tw));
   const int ti = (int)((p / g.tw) % g.th);
   const int tj = (int)(p % g.tw);
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       raw[ni][e] = v;
     }
 
-  if (c_base >= g.C) {
+  if (!kCompact && c_base >= g.C) {
     // all 16 channels of this warp are Cp padding: V = BT 0 BT^T = 0
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -134,8 +138,11 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
     }
 
     uint32_t outw[2][8][4];  // [plane][position slot][channel word]
+    uint32_t outc[8][2];     // kCompact: [position slot][channel pair] int16 x 2
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int s = 0; s < 8; ++s) outc[s][0] = outc[s][1] = 0u;
+#pragma unroll
+    for (int u = 0; u < (kCompact ? 1 : 4); ++u) {
       uint32_t din[2][4];
       transpose4x4(word_of(raw[0][0], u), word_of(raw[0][1], u), word_of(raw[0][2], u), word_of(raw[0][3], u),
                    din[0]);
@@ -195,11 +202,21 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
             for (int e = 0; e < 4; ++e) v[ni][e] = red_pos_biased(acc[e], fm) - fm.h;
           }
         }
+        if constexpr (kCompact) {
+          const uint32_t hsel = (q & 1) ? 0x5410u : 0x3254u;  // int16 into the high / low half
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const int32_t val = v[s >> 2][s & 3];
-          outw[0][s][u] = __byte_perm(outw[0][s][u], (uint32_t)val, bsel);
-          if (planes == 2) outw[1][s][u] = __byte_perm(outw[1][s][u], (uint32_t)limb_hi(val), bsel);
+          for (int s = 0; s < 8; ++s) {
+            const uint32_t val = (uint32_t)v[s >> 2][s & 3];
+            if (q < 2) outc[s][0] = __byte_perm(outc[s][0], val, hsel);
+            else outc[s][1] = __byte_perm(outc[s][1], val, hsel);
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const int32_t val = v[s >> 2][s & 3];
+            outw[0][s][u] = __byte_perm(outw[0][s][u], (uint32_t)val, bsel);
+            if (planes == 2) outw[1][s][u] = __byte_perm(outw[1][s][u], (uint32_t)limb_hi(val), bsel);
+          }
         }
       }
     }
@@ -210,6 +227,10 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       const int j = gq + 8 * (e >> 1), i = 8 * ni + 2 * tq + (e & 1);
       if (i >= N || j >= N) continue;
       const int pos = i * N + j;
+      if constexpr (kCompact) {
+        *reinterpret_cast<uint2*>(V + ((((int64_t)r * g.P + p) * npos + pos) << 3)) = make_uint2(outc[s][0], outc[s][1]);
+        continue;
+      }
       int8_t* dst = V + ((int64_t)tb.plane_base * npos + pos) * g.P * g.Cp + p * g.Cp + c_base;
       *reinterpret_cast<uint4*>(dst) = make_uint4(outw[0][s][0], outw[0][s][1], outw[0][s][2], outw[0][s][3]);
       if (planes == 2)
@@ -225,9 +246,21 @@ cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, c
                                       cudaStream_t s) {
   dim3 grid((unsigned)(g.P * ((g.Cp + kCTAChannels - 1) / kCTAChannels)));
   if (plan.dev.res[0].planes == 2)
-    input_transform_tc_kernel<2><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+    input_transform_tc_kernel<2, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
   else
-    input_transform_tc_kernel<1><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+    input_transform_tc_kernel<1, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_input_transform_compact(const PlanHost& plan, const Geometry& g, const int8_t* x, int16_t* V16,
+                                           cudaStream_t s) {
+  if (g.C > 4) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((g.P + 3) / 4));
+  int8_t* V = reinterpret_cast<int8_t*>(V16);
+  if (plan.dev.res[0].planes == 2)
+    input_transform_tc_kernel<2, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+  else
+    input_transform_tc_kernel<1, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
   return cudaGetLastError();
 }
 

@@ -43,6 +43,14 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s);
 bool tc_output_ok(const PlanDevice& d);
+bool force_generic();
+// Small-channel path (C <= 4): compact input transform + CUDA-core product (smallc.cu)
+bool smallc_ok(const PlanDevice& d, const Geometry& g);
+size_t smallc_v16_bytes(const PlanDevice& d, const Geometry& g);
+cudaError_t launch_input_transform_compact(const PlanHost& plan, const Geometry& g, const int8_t* x, int16_t* V16,
+                                           cudaStream_t s);
+cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const int16_t* V16, const int8_t* U,
+                                  int16_t* Mw, cudaStream_t s);
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
 size_t direct_weight_bytes(int R, int C, int K);
 cudaError_t launch_pack_weights(const int8_t* w, int R, int C, int K, int layout, int8_t* w2, cudaStream_t s);

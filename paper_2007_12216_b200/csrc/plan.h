@@ -22,6 +22,9 @@ struct ResidueTables {
   uint32_t red_mul;
   int32_t red_shift;
   int32_t red_off;
+  // (uint32)(-m), stored rather than derived so the compiler keeps
+  // q*negm + n as one IMAD instead of negating q and multiplying by m
+  uint32_t red_negm;
   int32_t half;        // (m - 1) / 2
   int32_t at[RNSW_MAX_N * RNSW_MAX_N];  // AT (M x N), row-major, stride N
   int32_t bt[RNSW_MAX_N * RNSW_MAX_N];  // BT (N x N)

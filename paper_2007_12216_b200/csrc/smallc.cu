@@ -1,0 +1,111 @@
+// Small-channel layers (C <= 4, e.g. VGG16 conv1_1 with C = 3): the
+// Winograd-domain product M = sum_c V[c] * U[c][k] mod m (rw/layer.py:366-372,
+// rw/gemm.py:91-97) on the CUDA cores.
+//
+// A tensor-core GEMM would pad the 3-channel contraction to K = 32 and
+// stream 10x more V than the layer has, so for C <= 4 the input transform
+// writes compact int16 residues V16[res][P][pos][4] (input_tc.cu, kCompact)
+// and this kernel forms the product directly into the output transform's
+// input layout Mw[P][res][pos][Kp].  Each thread keeps the filter residues
+// of one (residue, position, 8 output channels) in registers for a run of
+// tiles: per tile it loads 8 bytes of V16 (shared by 8 threads), does
+// 4 x 8 exact int32 products and 8 division-free reductions, and stores one
+// 16-byte row segment of Mw.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rnsw {
+namespace {
+
+// kPL == 2 (16-bit moduli): Mw holds y mod m in [0, m), which the output
+// transform's limb split accepts (its bound analysis covers [0, m)).
+// kPL == 1: symmetric residues (the s8 fragments of the output transform).
+template <int kPL>
+__global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* __restrict__ plan, int P, int K,
+                                                             int Kp, int Cp, const int16_t* __restrict__ V16,
+                                                             const int8_t* __restrict__ U, int16_t* __restrict__ Mw,
+                                                             int tiles_per_cta) {
+  const int N = plan->n, npos = N * N, nres = plan->n_res;
+  const int kgroups = Kp >> 3;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= npos * kgroups) return;
+  const int pos = slot / kgroups, kg = slot - pos * kgroups;
+  const int r = blockIdx.y;
+  const ResidueTables& t = plan->res[r];
+  const FastMod fm = fast_mod_of(t);
+
+  // filter residues u[k][c] = lo + 256 hi from the bank's limb planes
+  // [plane][pos][K][Cp] (transforms.cu store_uplanes)
+  const int64_t plane_stride = (int64_t)npos * K * Cp;
+  int32_t u[8][4];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const int k = kg * 8 + kk;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      int32_t v = 0;
+      if (k < K) {
+        const int8_t* b = U + (int64_t)t.uplane_base * plane_stride + ((int64_t)pos * K + k) * Cp + c;
+        v = b[0];
+        if (kPL == 2) v += 256 * (int32_t)b[plane_stride];
+      }
+      u[kk][c] = v;
+    }
+  }
+  const int32_t bias = kPL == 2 ? pos_bias(fm) : fm.off;
+  const int p_begin = blockIdx.z * tiles_per_cta, p_end = min(P, p_begin + tiles_per_cta);
+  const uint2* src = reinterpret_cast<const uint2*>(V16) + ((int64_t)r * P + p_begin) * npos + pos;
+  uint4* dst = reinterpret_cast<uint4*>(Mw + (((int64_t)p_begin * nres + r) * npos + pos) * Kp) + kg;
+  const int64_t dst_step = (int64_t)nres * npos * Kp / 8;  // uint4 per tile
+  // two tiles of V16 in flight ahead of the one being reduced
+  uint2 wa = p_begin < p_end ? __ldg(src) : make_uint2(0, 0);
+  uint2 wb = p_begin + 1 < p_end ? __ldg(src + npos) : make_uint2(0, 0);
+  for (int p = p_begin; p < p_end; ++p, src += npos, dst += dst_step) {
+    const uint2 w = wa;
+    wa = wb;
+    if (p + 2 < p_end) wb = __ldg(src + 2 * npos);
+    const int32_t v0 = (int32_t)(w.x << 16) >> 16, v1 = (int32_t)w.x >> 16;
+    const int32_t v2 = (int32_t)(w.y << 16) >> 16, v3 = (int32_t)w.y >> 16;
+    uint32_t o[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      int32_t y[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int kk = 2 * h + e;
+        // |sum| <= 4 h^2 < 2^28 for m < 4500
+        const int32_t n = bias + v0 * u[kk][0] + v1 * u[kk][1] + v2 * u[kk][2] + v3 * u[kk][3];
+        y[e] = kPL == 2 ? red_pos_biased(n, fm) : red_pos_biased(n, fm) - fm.h;
+      }
+      o[h] = __byte_perm((uint32_t)y[0], (uint32_t)y[1], 0x5410);
+    }
+    *dst = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+}  // namespace
+
+bool smallc_ok(const PlanDevice& d, const Geometry& g) { return g.C <= 4 && tc_output_ok(d); }
+
+size_t smallc_v16_bytes(const PlanDevice& d, const Geometry& g) {
+  return (size_t)d.n_res * g.P * d.n * d.n * 4 * sizeof(int16_t);
+}
+
+cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const int16_t* V16, const int8_t* U,
+                                  int16_t* Mw, cudaStream_t s) {
+  const PlanDevice& d = plan.dev;
+  const int npos = d.n * d.n, slots = npos * (g.Kp / 8);
+  const int bx = (slots + 255) / 256;
+  // enough CTAs for ~4 waves of 8 per SM, each amortising its register-held
+  // filter residues over up to 64 tiles
+  const int64_t per_tile = (int64_t)bx * d.n_res;
+  const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, g.P * per_tile / (148 * 8 * 4)));
+  dim3 grid(bx, d.n_res, (unsigned)((g.P + tpc - 1) / tpc));
+  if (d.res[0].planes == 2)
+    smallc_product_kernel<2><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+  else
+    smallc_product_kernel<1><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+  return cudaGetLastError();
+}
+
+}  // namespace rnsw

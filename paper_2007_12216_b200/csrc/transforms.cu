@@ -296,14 +296,6 @@ __global__ void requant_pool_kernel(const int32_t* __restrict__ y, int B, int H,
   }
 }
 
-bool force_generic() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("RNSW_FORCE_GENERIC");
-    v = (e != nullptr && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
 
 // Vectorised glue for C % 4 == 0: four channels per thread (int4 loads,
 // one 32-bit store of four int8).
@@ -336,6 +328,17 @@ __global__ void requant_pool_vec4_kernel(const int4* __restrict__ y, int B, int 
 }
 
 }  // namespace
+
+// RNSW_FORCE_GENERIC=1 routes every stage to the generic CUDA-core kernels
+// (test hook for the cross-check of the two paths).
+bool force_generic() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RNSW_FORCE_GENERIC");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 
 // The tensor-core output kernel is instantiated for uniform limb planes:
 // 1-2 residues of 16-bit moduli or 1-4 residues of 8-bit moduli.

@@ -87,9 +87,28 @@ class VGG16Rns:
                 "output_transform_bytes": len(self.cfg.moduli) * npos * tiles * k * 2 + (
                     batch * oside * oside * k if fused else batch * side * side * k * 4),
                 "glue_bytes": batch * side * side * k * 4 + batch * oside * oside * k,
+                # C <= 4 layers run the CUDA-core product (csrc/smallc.cu): V16 in, Mw out
+                "product_bytes": len(self.cfg.moduli) * npos * tiles * (8 + 2 * k),
                 "direct_ops": 2 * batch * side * side * c * k * 9,
             })
         return out
+
+    def _staged_product(self, timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, mb, s):
+        """Stages 1-2 of one layer as rnsw_conv_forward runs them: the
+        tensor-core GEMM split, or for C <= 4 the compact transform + CUDA-core
+        product (kind "product")."""
+        l = _native.lib()
+        vp = _native.c_void_p
+        if c <= 4:
+            timed("input_transform", i, lambda: l.rnsw_input_transform_compact(
+                self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
+            timed("product", i, lambda: l.rnsw_small_channel_product(
+                self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), mb, s))
+            return
+        timed("input_transform", i, lambda: l.rnsw_input_transform(
+            self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
+        timed("gemm", i, lambda: l.rnsw_winograd_gemm(
+            self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), mb, s))
 
     def forward_staged(self, x, record):
         """Same launches as forward(), one C-ABI stage call per kernel with a
@@ -116,10 +135,7 @@ class VGG16Rns:
             tiles = batch * math.ceil(side / self.cfg.tile_m) ** 2
             vb = (l.rnsw_v_bytes(self.plan.handle, tiles, c) + 255) // 256 * 256
             v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
-            timed("input_transform", i, lambda: l.rnsw_input_transform(
-                self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
-            timed("gemm", i, lambda: l.rnsw_winograd_gemm(
-                self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), ws.numel() - vb, s))
+            self._staged_product(timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, ws.numel() - vb, s)
             timed("output_transform", i, lambda: l.rnsw_output_transform(
                 self.plan.handle, vp(m_ptr), batch, side, side, k, 1, _native.LAYOUT_NHWC, vp(y.data_ptr()), s))
             oside = side // 2 if pool else side
@@ -211,10 +227,7 @@ class VGG16Rns:
             oside = side // 2 if pool else side
             nxt = bufs["out"] if i == nl - 1 else \
                 bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
-            timed("input_transform", i, lambda: l.rnsw_input_transform(
-                self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
-            timed("gemm", i, lambda: l.rnsw_winograd_gemm(
-                self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), ws.numel() - vb, s))
+            self._staged_product(timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, ws.numel() - vb, s)
             timed("output_transform", i, lambda: l.rnsw_output_transform_requant(
                 self.plan.handle, vp(m_ptr), batch, side, side, k, 1, self.cfg.shifts[i], 1 if pool else 0,
                 vp(nxt.data_ptr()), s))

@@ -163,6 +163,46 @@ def test_random_geometry_sweep(seed):
     assert np.array_equal(got, oracle.direct_conv_c(x, w, spec.padding))
 
 
+SMALL_C = [
+    # h, w, c, k, r, pad, batch, tile_m, moduli, layout -- C <= 4 runs the compact
+    # transform + CUDA-core product path (csrc/smallc.cu)
+    (224, 224, 3, 64, 3, 1, 1, 14, (4001, 4331), "nhwc"),   # VGG16 conv1_1
+    (30, 26, 1, 5, 3, 1, 2, 8, (251, 241, 239), "nhwc"),     # K not a multiple of 8
+    (17, 19, 2, 33, 5, 2, 3, 12, (4001, 4331), "nchw"),      # N = 16 with R = 5, NCHW
+    (20, 20, 4, 16, 3, 0, 2, 2, (251, 241, 239, 233), "nhwc"),  # four residues
+    (40, 40, 3, 130, 3, 1, 1, 6, (253, 251, 247), "nchw"),   # 3 residues, Kp = 144
+]
+
+
+@pytest.mark.parametrize("case", SMALL_C, ids=lambda c: "x".join(map(str, c[:8])) + c[9])
+def test_small_channel_path(case):
+    rnsw = _rnsw()
+    h, w, c, k, r, pad, batch, tm, mods, layout = case
+    spec = rnsw.LayerSpec(h=h, w=w, c=c, k=k, r=r, padding=pad, batch=batch, tile_m=tm)
+    system = rnsw.RnsSystem(mods)
+    wt, x = _operands(spec, c * 31 + k)
+    want = O.winograd_layer(x, wt, pad, tm, mods)
+    if layout == "nhwc":
+        got = rnsw.winograd_layer_conv(spec, wt, x, system, declared_bound=system.signed_bound)
+    else:
+        got = rnsw.conv2d_rns(np.ascontiguousarray(x.transpose(0, 3, 1, 2)),
+                              np.ascontiguousarray(wt.transpose(3, 2, 0, 1)), mods, tile_m=tm, padding=pad,
+                              declared_bound=system.signed_bound)
+        got = np.asarray(got).transpose(0, 2, 3, 1)
+    assert np.array_equal(got, want)
+
+
+def test_small_channel_wraps_like_the_reference():
+    """A false declared bound wraps modulo D on the small-channel path too."""
+    rnsw = _rnsw()
+    spec = rnsw.LayerSpec(h=12, w=12, c=3, k=8, r=3, padding=1, tile_m=6)
+    mods = (7, 11, 13)
+    system = rnsw.RnsSystem(mods)
+    wt, x = _operands(spec, 5)
+    got = rnsw.winograd_layer_conv(spec, wt, x, system, declared_bound=10)
+    assert np.array_equal(got, O.winograd_layer(x, wt, 1, 6, mods))
+
+
 DIRECT = [
     # b, h, w, c, k, r, pad, stride
     (1, 56, 56, 64, 64, 3, 1, 1),

@@ -30,9 +30,10 @@ for B in batches:
     print(f"B={B} total {tot:.3f} ms  " + "  ".join(f"{k} {v:.3f}" for k, v in per.items()))
     for i, r in rows.items():
         wk = work[i]
+        mid = (f"  gemm {wk['gemm_ops']/r['gemm']/1e9:6.0f} TOPS" if "gemm" in r else
+               f"  prod {wk['product_bytes']/r['product']/1e6:6.0f} GB/s")
         print(f"  {wk['name']:8s} " + " ".join(f"{k[:6]} {v:7.3f}" for k, v in r.items()) +
-              f"  in {wk['input_transform_bytes']/r['input_transform']/1e6:6.0f} GB/s"
-              f"  gemm {wk['gemm_ops']/r['gemm']/1e9:6.0f} TOPS"
+              f"  in {wk['input_transform_bytes']/r['input_transform']/1e6:6.0f} GB/s" + mid +
               f"  out {wk['output_transform_bytes']/r['output_transform']/1e6:6.0f} GB/s")
     print(f"  direct-equiv {sum(w['direct_ops'] for w in work)/tot/1e9:.1f} TOPS")
     for _ in range(2):  # warm-up: lazy module loading of the fused instances
