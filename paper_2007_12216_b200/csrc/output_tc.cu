@@ -11,9 +11,11 @@
 //   pass 2  Y^T = Z^T * AT^T      (A = pass-1 C registers, no shuffles: the
 //                                  contraction index i is permuted so the C
 //                                  fragment columns land on the A k-slots)
-// 16-bit moduli use two s8 limbs on each side (4 MMAs per product, 3
-// accumulators) whose exact int32 recombination stays below 2^28 for
-// m < 4500, so each value needs a single division-free reduction.
+// 16-bit moduli use two s8 limbs on each side (4 MMAs per product) and the
+// limbs of X' = 256 X mod m for the constant side, so the product is
+// 256 * acc256 + acc1 with two accumulators; the exact int32 recombination
+// stays below 2^28 for m < 4500, so each value needs a single division-free
+// reduction.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -56,7 +58,9 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   const int s_bytes = (nres * kKB * kRowS * 2 + 15) & ~15;
   int32_t* AT16 = reinterpret_cast<int32_t*>(smem_raw + s_bytes);  // [nres][16][16], zero padded
   int32_t* ATW16 = AT16 + nres * 256;                               // AT * W[r][0] mod m_r (pass 2)
-  uint8_t* O8 = reinterpret_cast<uint8_t*>(ATW16 + nres * 256);     // [pixel][kKB] int8 (fused requant)
+  int32_t* ATP16 = ATW16 + nres * 256;   // 256 * AT mod m (16-bit limb trick, pass 1)
+  int32_t* ATWP16 = ATP16 + nres * 256;  // 256 * ATW mod m (pass 2)
+  uint8_t* O8 = reinterpret_cast<uint8_t*>(ATWP16 + nres * 256);    // [pixel][kKB] int8 (fused requant)
   constexpr bool kDigits = kMode != 2;  // pass 2 emits mixed-radix digits
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
@@ -69,8 +73,14 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   for (int idx = tid; idx < nres * 256; idx += blockDim.x) {
     const int r = idx >> 8, a = (idx >> 4) & 15, j = idx & 15;
     const int32_t at = (a < M && j < N) ? plan->res[r].at[a * RNSW_MAX_N + j] : 0;
+    const FastMod f = fast_mod_of(plan->res[r]);
+    const int32_t atw = (kDigits && r > 0) ? red_fast(at * plan->mrc_w[r][0], f) : at;
     AT16[idx] = at;
-    ATW16[idx] = (kDigits && r > 0) ? red_fast(at * plan->mrc_w[r][0], fast_mod_of(plan->res[r])) : at;
+    ATW16[idx] = atw;
+    if (kPL == 2) {
+      ATP16[idx] = red_fast(at * 256, f);
+      ATWP16[idx] = red_fast(atw * 256, f);
+    }
   }
   if (N < 16)  // staging never writes the padding rows/columns
     for (int idx = tid; idx < nres * kKB * kRowS / 2; idx += blockDim.x) reinterpret_cast<int32_t*>(S)[idx] = 0;
@@ -83,6 +93,9 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   FastMod fmr[NRES];
   int plr[NRES];
   uint32_t A1lo[NRES][2], A1hi[NRES][2], B2lo[NRES][2], B2hi[NRES][2];
+  // 16-bit moduli: limbs of X' = 256 X mod m, so a product with a two-limb
+  // operand needs two accumulators (256 * hi-part + lo-part) instead of three
+  uint32_t A1plo[NRES][2], A1phi[NRES][2], B2plo[NRES][2], B2phi[NRES][2];
   int32_t mw[NRES][NRES];
 #pragma unroll
   for (int r = 0; r < NRES; ++r) {
@@ -103,6 +116,18 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
       const int32_t u2 = atw[row * 16 + 8 + 2 * tq], u3 = atw[row * 16 + 9 + 2 * tq];
       B2lo[r][h] = pack4_lo(u0, u1, u2, u3);
       B2hi[r][h] = pack4_lo(limb_hi(u0), limb_hi(u1), limb_hi(u2), limb_hi(u3));
+      if (kPL == 2) {
+        const int32_t* atp = ATP16 + r * 256;
+        const int32_t* atwp = ATWP16 + r * 256;
+        const int32_t p0 = atp[row * 16 + 4 * tq], p1 = atp[row * 16 + 4 * tq + 1];
+        const int32_t p2 = atp[row * 16 + 4 * tq + 2], p3 = atp[row * 16 + 4 * tq + 3];
+        A1plo[r][h] = pack4_lo(p0, p1, p2, p3);
+        A1phi[r][h] = pack4_lo(limb_hi(p0), limb_hi(p1), limb_hi(p2), limb_hi(p3));
+        const int32_t q0 = atwp[row * 16 + 2 * tq], q1 = atwp[row * 16 + 2 * tq + 1];
+        const int32_t q2 = atwp[row * 16 + 8 + 2 * tq], q3 = atwp[row * 16 + 9 + 2 * tq];
+        B2plo[r][h] = pack4_lo(q0, q1, q2, q3);
+        B2phi[r][h] = pack4_lo(limb_hi(q0), limb_hi(q1), limb_hi(q2), limb_hi(q3));
+      }
     }
   }
   const uint32_t signed_bound = (uint32_t)plan->signed_bound, dyn_range = (uint32_t)plan->dynamic_range;
@@ -184,14 +209,15 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
             const uint32_t w1 = *reinterpret_cast<const uint32_t*>(row + stage_off(i, 4 * tq) + 2);
             const uint32_t blo = __byte_perm(w0, w1, 0x6420);  // u8 low bytes
             const uint32_t bhi = __byte_perm(w0, w1, 0x7531);  // s8 high bytes
+            // Mat = 256 hi + lo: AT Mat = AT' hi + AT lo (mod m)
             const int32_t bias = pos_bias(fm);
-            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {bias, bias, bias, bias};
-            imma_ss(hh, A1hi[r][0], A1hi[r][1], bhi);
-            imma_su(cr, A1hi[r][0], A1hi[r][1], blo);
-            imma_ss(cr, A1lo[r][0], A1lo[r][1], bhi);
-            imma_su(ll, A1lo[r][0], A1lo[r][1], blo);
+            int32_t a256[4] = {0, 0, 0, 0}, a1[4] = {bias, bias, bias, bias};
+            imma_ss(a256, A1phi[r][0], A1phi[r][1], bhi);
+            imma_su(a256, A1hi[r][0], A1hi[r][1], blo);
+            imma_ss(a1, A1plo[r][0], A1plo[r][1], bhi);
+            imma_su(a1, A1lo[r][0], A1lo[r][1], blo);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased(hh[e] * 65536 + cr[e] * 256 + ll[e], fm);
+            for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased(a256[e] * 256 + a1[e], fm);
           }
         } else {
 #pragma unroll
@@ -217,14 +243,14 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           const int32_t bias = pos_bias(fm);
 #pragma unroll
           for (int na = 0; na < 2; ++na) {
-            int32_t hh[4] = {0, 0, 0, 0}, cr[4] = {0, 0, 0, 0}, ll[4] = {bias, bias, bias, bias};
-            imma_us(hh, zhi0, zhi1, B2hi[r][na]);
-            imma_us(cr, zhi0, zhi1, B2lo[r][na]);
-            imma_us(cr, zlo0, zlo1, B2hi[r][na]);
-            imma_us(ll, zlo0, zlo1, B2lo[r][na]);
+            int32_t a256[4] = {0, 0, 0, 0}, a1[4] = {bias, bias, bias, bias};
+            imma_us(a256, zhi0, zhi1, B2phi[r][na]);
+            imma_us(a256, zlo0, zlo1, B2hi[r][na]);
+            imma_us(a1, zhi0, zhi1, B2plo[r][na]);
+            imma_us(a1, zlo0, zlo1, B2lo[r][na]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              int32_t n = hh[e] * 65536 + cr[e] * 256 + ll[e];
+              int32_t n = a256[e] * 256 + a1[e];
               if constexpr (kDigits) {
 #pragma unroll
                 for (int i2 = 0; i2 < r; ++i2) n -= yv[i2][4 * na + e] * mw[r][i2];
@@ -332,7 +358,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
 }  // namespace
 
 size_t output_tc_smem(const PlanDevice& d) {
-  return (size_t)((d.n_res * kKB * kRowS * 2 + 15) & ~15) + d.n_res * 512 * 4 + (size_t)d.m_out * d.m_out * kKB;
+  return (size_t)((d.n_res * kKB * kRowS * 2 + 15) & ~15) + d.n_res * 1024 * 4 + (size_t)d.m_out * d.m_out * kKB;
 }
 
 cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
