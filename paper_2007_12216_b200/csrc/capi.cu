@@ -391,7 +391,8 @@ int transform_and_product(const rnsw_plan* plan, const rnsw::Geometry& g, const 
   }
   e = rnsw::launch_input_transform(plan->host, g, x, V, s);
   if (e != cudaSuccess) return cuda_fail(e, "input_transform");
-  e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, g.K, g.Kp, g.bc, Mw, s);
+  e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, g.K, g.Kp, g.bc, Mw, s,
+                                 rnsw::tc_output_ok(plan->host.dev) && !rnsw::force_generic());
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "winograd_gemm");
 }
 }  // namespace

@@ -62,6 +62,8 @@ struct GemmArgs {
   FastMod fm[RNSW_MAX_RES];
   int fast;   // exact division-free reductions apply (plan.fast and C <= 8192)
   int fast2;  // additionally C <= 512: 256*A256 + A1 needs a single reduction
+  int pos_out;  // fast2 16-bit residues written as y mod m in [0, m) (the output
+                // transform's limb split accepts it; saves the symmetric shift)
   int16_t* Mw;
 };
 
@@ -138,8 +140,14 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
       int32_t r[16];
       if (a.fast2) {
         // C <= 512, m < 4500: |256*A256 + A1| <= 512*(9*9+128*9)*256 + 512*(9*128+128*128) < 2^28
+        if (a.pos_out) {
+          const int32_t pb = pos_bias(fm);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) r[e] = red_fast(hi[j][e] * 256 + lo[j][e], fm);
+          for (int e = 0; e < 16; ++e) r[e] = red_pos_biased(hi[j][e] * 256 + lo[j][e] + pb, fm);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) r[e] = red_fast(hi[j][e] * 256 + lo[j][e], fm);
+        }
       } else if (a.fast) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) r[e] = red_fast(red_fast(hi[j][e], fm) * 256 + lo[j][e], fm);
@@ -401,7 +409,7 @@ cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t
 }  // namespace
 
 cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp, int K,
-                                 int Kp, int bc, int16_t* Mw, cudaStream_t s) {
+                                 int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out) {
   const PlanDevice& d = plan.dev;
   GemmArgs a{};
   a.P = P;
@@ -412,6 +420,7 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   a.n_res = d.n_res;
   a.nkc = Cp / bc;
   a.Mw = Mw;
+  a.pos_out = pos_out ? 1 : 0;
   int maxpl = 1;
   for (int r = 0; r < d.n_res; ++r) {
     a.planes[r] = d.res[r].planes;

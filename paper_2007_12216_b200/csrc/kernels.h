@@ -33,8 +33,10 @@ cudaError_t launch_filter_import(const PlanHost& plan, int res, const int16_t* u
                                  int8_t* U, cudaStream_t s);
 cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                    cudaStream_t s);
+// pos_out: 16-bit residues as y mod m in [0, m) instead of symmetric (whole-layer
+// path only; the stage API keeps the reference's symmetric residues)
 cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp,
-                                 int K, int Kp, int bc, int16_t* Mw, cudaStream_t s);
+                                 int K, int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out = false);
 cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
                                     int16_t* y_res, cudaStream_t s);
 cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
