@@ -252,6 +252,15 @@ RNSW_DEV uint32_t pack4_lo(int32_t x0, int32_t x1, int32_t x2, int32_t x3) {
   return __byte_perm(a, b, 0x5410);
 }
 
+// Byte k (0..3) of four words packed into one (pack4_lo is k = 0).
+template <int k>
+RNSW_DEV uint32_t pack4_byte(int32_t x0, int32_t x1, int32_t x2, int32_t x3) {
+  constexpr uint32_t sel = ((4u + k) << 4) | k;
+  const uint32_t a = __byte_perm((uint32_t)x0, (uint32_t)x1, sel);
+  const uint32_t b = __byte_perm((uint32_t)x2, (uint32_t)x3, sel);
+  return __byte_perm(a, b, 0x5410);
+}
+
 // High limb of the balanced split v = 256*hi + lo, lo in [-128, 127].
 RNSW_DEV int32_t limb_hi(int32_t v) { return (v + 128) >> 8; }
 

@@ -9,11 +9,16 @@
 //   pass 1  T^T = BT * D^T    (A = BT constants, B = patch bytes)
 //   pass 2  V^T = T^T * BT^T  (A = pass-1 C registers with the contraction
 //                              index permuted onto the k-slots, B = BT^T)
+// 16-bit moduli: pass 1 keeps T exact (|T| < 2^23) as three byte limbs
+// T = 65536 T2 + 256 T1 + T0 instead of reducing it, and pass 2 multiplies
+// them by BT, BT' = 256 BT and BT'' = 65536 BT (mod m), each in two limbs,
+// into two accumulators (256 * acc256 + acc1).  The output limbs come from
+// w = v + 128: hi = w >> 8 and lo = (w & 255) ^ 0x80.
 // Each lane ends up holding 8 transform positions x 16 channels, i.e. one
 // 16-byte row segment of V per position and plane, stored with one vector
-// store.  16-bit moduli: BT and T are split into two s8 limbs; the exact
-// int32 recombination stays below 2^28 (m < 4500) so one division-free
-// reduction per value suffices.
+// store.  16-bit moduli: BT is split into two s8 limbs (see below); every
+// exact int32 sum stays below 2^28 (m < 4500), so one division-free
+// reduction per output value suffices.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -121,7 +126,8 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
     const uint32_t ahi0 = pack4_lo(limb_hi(av[0]), limb_hi(av[1]), limb_hi(av[2]), limb_hi(av[3]));
     const uint32_t ahi1 = pack4_lo(limb_hi(av[4]), limb_hi(av[5]), limb_hi(av[6]), limb_hi(av[7]));
     // pass-2 B: column i = g + 8 ni, k-slot e <-> a = {2t, 2t+1, 8+2t, 9+2t}[e]
-    uint32_t blo[2], bhi[2], bplo[2], bphi[2];  // BT and BT' = 256*BT mod m (16-bit: 2 accumulators)
+    // BT, BT' = 256 BT and BT'' = 65536 BT (mod m) (16-bit: 2 accumulators)
+    uint32_t blo[2], bhi[2], bplo[2], bphi[2], bpplo[2], bpphi[2];
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) {
       const int i = gq + 8 * ni;
@@ -134,6 +140,10 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
         const int32_t w2 = red_fast(v2 * 256, fm), w3 = red_fast(v3 * 256, fm);
         bplo[ni] = pack4_lo(w0, w1, w2, w3);
         bphi[ni] = pack4_lo(limb_hi(w0), limb_hi(w1), limb_hi(w2), limb_hi(w3));
+        const int32_t x0 = red_fast(w0 * 256, fm), x1 = red_fast(w1 * 256, fm);
+        const int32_t x2 = red_fast(w2 * 256, fm), x3 = red_fast(w3 * 256, fm);
+        bpplo[ni] = pack4_lo(x0, x1, x2, x3);
+        bpphi[ni] = pack4_lo(limb_hi(x0), limb_hi(x1), limb_hi(x2), limb_hi(x3));
       }
     }
 
@@ -158,42 +168,53 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
         const uint32_t dq0 = q == 0 ? din[0][0] : q == 1 ? din[0][1] : q == 2 ? din[0][2] : din[0][3];
         const uint32_t dq1 = q == 0 ? din[1][0] : q == 1 ? din[1][1] : q == 2 ? din[1][2] : din[1][3];
         const uint32_t bsel = (0x3210u & ~(0xFu << (4 * q))) | (0x4u << (4 * q));  // insert at byte q
-        // pass 1 -> T in [0, m): the reduction bias rides in the accumulator
-        int32_t t[2][4];
+        int32_t v[2][4];
+        if (planes == 2) {
+          // pass 1: T exact, as byte limbs (see the header)
+          int32_t t[2][4];
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          int32_t acc[4] = {pbias, pbias, pbias, pbias};
-          if (planes == 2) {
-            int32_t hi[4] = {0, 0, 0, 0};
+          for (int ni = 0; ni < 2; ++ni) {
+            int32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
             imma_ss(hi, ahi0, ahi1, ni ? dq1 : dq0);
-            imma_ss(acc, alo0, alo1, ni ? dq1 : dq0);
+            imma_ss(lo, alo0, alo1, ni ? dq1 : dq0);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) t[ni][e] = red_pos_biased(hi[e] * 256 + acc[e], fm);
-          } else {
+            for (int e = 0; e < 4; ++e) t[ni][e] = hi[e] * 256 + lo[e];
+          }
+          // pass 2: A rows j = g / g+8, k-slots = {2t, 2t+1, 8+2t, 9+2t}
+          const uint32_t t0a = pack4_byte<0>(t[0][0], t[0][1], t[1][0], t[1][1]);
+          const uint32_t t0b = pack4_byte<0>(t[0][2], t[0][3], t[1][2], t[1][3]);
+          const uint32_t t1a = pack4_byte<1>(t[0][0], t[0][1], t[1][0], t[1][1]);
+          const uint32_t t1b = pack4_byte<1>(t[0][2], t[0][3], t[1][2], t[1][3]);
+          const uint32_t t2a = pack4_byte<2>(t[0][0], t[0][1], t[1][0], t[1][1]);
+          const uint32_t t2b = pack4_byte<2>(t[0][2], t[0][3], t[1][2], t[1][3]);
+          // kCompact wants v itself, the limb planes w = v + 128
+          const int32_t vshift = kCompact ? -fm.h : 128 - fm.h;
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            int32_t a256[4] = {0, 0, 0, 0}, a1[4] = {sbias, sbias, sbias, sbias};
+            imma_ss(a256, t2a, t2b, bpphi[ni]);
+            imma_us(a256, t1a, t1b, bphi[ni]);
+            imma_us(a256, t0a, t0b, bhi[ni]);
+            imma_ss(a1, t2a, t2b, bpplo[ni]);
+            imma_us(a1, t1a, t1b, bplo[ni]);
+            imma_us(a1, t0a, t0b, blo[ni]);
+            // |256 a256 + a1| < 2^25
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[ni][e] = red_pos_biased(a256[e] * 256 + a1[e], fm) + vshift;
+          }
+        } else {
+          // pass 1 -> T in [0, m): the reduction bias rides in the accumulator
+          int32_t t[2][4];
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            int32_t acc[4] = {pbias, pbias, pbias, pbias};
             imma_ss(acc, alo0, alo1, ni ? dq1 : dq0);
 #pragma unroll
             for (int e = 0; e < 4; ++e) t[ni][e] = red_pos_biased(acc[e], fm);
           }
-        }
-        // pass 2: A rows j = g / g+8, k-slots = {2t, 2t+1, 8+2t, 9+2t}; T is
-        // non-negative, so its low limb is the u8 low byte and the high limb T >> 8
-        const uint32_t tlo0 = pack4_lo(t[0][0], t[0][1], t[1][0], t[1][1]);
-        const uint32_t tlo1 = pack4_lo(t[0][2], t[0][3], t[1][2], t[1][3]);
-        int32_t v[2][4];
-        if (planes == 2) {
-          const uint32_t thi0 = pack4_lo(t[0][0] >> 8, t[0][1] >> 8, t[1][0] >> 8, t[1][1] >> 8);
-          const uint32_t thi1 = pack4_lo(t[0][2] >> 8, t[0][3] >> 8, t[1][2] >> 8, t[1][3] >> 8);
-#pragma unroll
-          for (int ni = 0; ni < 2; ++ni) {
-            int32_t a256[4] = {0, 0, 0, 0}, a1[4] = {sbias, sbias, sbias, sbias};
-            imma_us(a256, thi0, thi1, bphi[ni]);
-            imma_us(a256, tlo0, tlo1, bhi[ni]);
-            imma_us(a1, thi0, thi1, bplo[ni]);
-            imma_us(a1, tlo0, tlo1, blo[ni]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) v[ni][e] = red_pos_biased(a256[e] * 256 + a1[e], fm) - fm.h;
-          }
-        } else {
+          // pass 2: T in [0, m < 256) is one u8 limb
+          const uint32_t tlo0 = pack4_lo(t[0][0], t[0][1], t[1][0], t[1][1]);
+          const uint32_t tlo1 = pack4_lo(t[0][2], t[0][3], t[1][2], t[1][3]);
 #pragma unroll
           for (int ni = 0; ni < 2; ++ni) {
             int32_t acc[4] = {sbias, sbias, sbias, sbias};
@@ -213,11 +234,21 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
         } else {
 #pragma unroll
           for (int s = 0; s < 8; ++s) {
-            const int32_t val = v[s >> 2][s & 3];
+            const int32_t val = v[s >> 2][s & 3];  // 16-bit: w = v + 128
             outw[0][s][u] = __byte_perm(outw[0][s][u], (uint32_t)val, bsel);
-            if (planes == 2) outw[1][s][u] = __byte_perm(outw[1][s][u], (uint32_t)limb_hi(val), bsel);
+            if (planes == 2) outw[1][s][u] = __byte_perm(outw[1][s][u], (uint32_t)(val >> 8), bsel);
           }
         }
+      }
+    }
+    if (planes == 2 && !kCompact) {
+      // low limb = (w & 255) ^ 0x80, on the real channels only
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int nv = min(max(g.C - (c_base + 4 * u), 0), 4);
+        const uint32_t flip = nv >= 4 ? 0x80808080u : (0x80808080u & ((1u << (8 * nv)) - 1u));
+#pragma unroll
+        for (int s = 0; s < 8; ++s) outw[0][s][u] ^= flip;
       }
     }
     // slot s = 4 ni + e: row j = g + 8 (e >> 1), column i = 8 ni + 2t + (e & 1)
