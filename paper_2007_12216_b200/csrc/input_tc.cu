@@ -43,10 +43,13 @@ RNSW_DEV uint32_t word_of(const uint4& v, int u) { return u == 0 ? v.x : u == 1 
 // tile and writes its 4 channels as symmetric int16 residues to
 // V16[res][P][pos][4] instead of the GEMM limb planes.
 template <int kPL, bool kCompact>
-__global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
+__global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                  const int8_t* __restrict__ x,
                                                                  int8_t* __restrict__ V) {
   __shared__ int32_t BT16[RNSW_MAX_RES * 256];
+  // per-warp output staging [slot][plane][u][lane] words: the finished 4-channel
+  // words leave registers after each u, keeping the kernel at 4 CTAs per SM
+  __shared__ uint32_t OW[4][8][2][4][32];
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = plan->n_res;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   const int ncb = (g.Cp + kCTAChannels - 1) / kCTAChannels;
@@ -147,7 +150,8 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       }
     }
 
-    uint32_t outw[2][8][4];  // [plane][position slot][channel word]
+    uint32_t outw[2][8];     // [plane][position slot] word of 4 channels (this u)
+    uint32_t (*ow)[2][4][32] = OW[warp];
     uint32_t outc[8][2];     // kCompact: [position slot][channel pair] int16 x 2
 #pragma unroll
     for (int s = 0; s < 8; ++s) outc[s][0] = outc[s][1] = 0u;
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
       transpose4x4(word_of(raw[1][0], u), word_of(raw[1][1], u), word_of(raw[1][2], u), word_of(raw[1][3], u),
                    din[1]);
 #pragma unroll
-      for (int s = 0; s < 8; ++s) outw[0][s][u] = outw[1][s][u] = 0u;
+      for (int s = 0; s < 8; ++s) outw[0][s] = outw[1][s] = 0u;
       // channels of this word: a rolled loop keeps the kernel inside the
       // instruction cache (the fully unrolled body missed in L0/L1.5)
 #pragma unroll 1
@@ -235,22 +239,27 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
 #pragma unroll
           for (int s = 0; s < 8; ++s) {
             const int32_t val = v[s >> 2][s & 3];  // 16-bit: w = v + 128
-            outw[0][s][u] = __byte_perm(outw[0][s][u], (uint32_t)val, bsel);
-            if (planes == 2) outw[1][s][u] = __byte_perm(outw[1][s][u], (uint32_t)(val >> 8), bsel);
+            outw[0][s] = __byte_perm(outw[0][s], (uint32_t)val, bsel);
+            if (planes == 2) outw[1][s] = __byte_perm(outw[1][s], (uint32_t)(val >> 8), bsel);
           }
         }
       }
-    }
-    if (planes == 2 && !kCompact) {
-      // low limb = (w & 255) ^ 0x80, on the real channels only
+      if constexpr (!kCompact) {
+        if (planes == 2) {
+          // low limb = (w & 255) ^ 0x80, on the real channels only
+          const int nv = min(max(g.C - (c_base + 4 * u), 0), 4);
+          const uint32_t flip = nv >= 4 ? 0x80808080u : (0x80808080u & ((1u << (8 * nv)) - 1u));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int nv = min(max(g.C - (c_base + 4 * u), 0), 4);
-        const uint32_t flip = nv >= 4 ? 0x80808080u : (0x80808080u & ((1u << (8 * nv)) - 1u));
+          for (int s = 0; s < 8; ++s) outw[0][s] ^= flip;
+        }
 #pragma unroll
-        for (int s = 0; s < 8; ++s) outw[0][s][u] ^= flip;
+        for (int s = 0; s < 8; ++s) {
+          ow[s][0][u][lane] = outw[0][s];
+          if (planes == 2) ow[s][1][u][lane] = outw[1][s];
+        }
       }
     }
+    // (each lane only ever touches its own OW column: no synchronisation)
     // slot s = 4 ni + e: row j = g + 8 (e >> 1), column i = 8 ni + 2t + (e & 1)
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -263,10 +272,10 @@ __global__ void __launch_bounds__(128) input_transform_tc_kernel(const PlanDevic
         continue;
       }
       int8_t* dst = V + ((int64_t)tb.plane_base * npos + pos) * g.P * g.Cp + p * g.Cp + c_base;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(outw[0][s][0], outw[0][s][1], outw[0][s][2], outw[0][s][3]);
+      *reinterpret_cast<uint4*>(dst) = make_uint4(ow[s][0][0][lane], ow[s][0][1][lane], ow[s][0][2][lane], ow[s][0][3][lane]);
       if (planes == 2)
         *reinterpret_cast<uint4*>(dst + plane_stride) =
-            make_uint4(outw[1][s][0], outw[1][s][1], outw[1][s][2], outw[1][s][3]);
+            make_uint4(ow[s][1][0][lane], ow[s][1][1][lane], ow[s][1][2][lane], ow[s][1][3][lane]);
     }
   }
 }

@@ -1,5 +1,5 @@
 # A/B the fused stack: RNSW_LIB=ab/A.so vs ab/B.so, alternating, 3 rounds
-for i in 1 2 3; do
+for i in 1 2; do
   for v in A B; do
     echo -n "$v: "; RNSW_LIB=ab/$v.so python tools/probe_vgg.py 256 2>&1 | grep "fused total"
   done
