@@ -125,6 +125,21 @@ def sandwich(left: np.ndarray, t: np.ndarray, right: np.ndarray, m: int) -> np.n
     return fold(a @ right.astype(np.int32), m).astype(narrow(m))
 
 
+def tile_conv_mod(g: np.ndarray, d: np.ndarray, m_out: int, r: int, modulus: int) -> np.ndarray:
+    """rw/kernel.py:56-70: G g G^T, BT d BT^T, elementwise product, AT . AT^T,
+    each reduced mod ``modulus`` (stacked tiles broadcast over leading dims)."""
+    at, gm, bt = modular_matrices(m_out, r, modulus)
+    u = sandwich(gm, g, gm.T, modulus).astype(np.int64)
+    v = sandwich(bt, d, bt.T, modulus).astype(np.int64)
+    return sandwich(at, fold(u * v, modulus), at.T, modulus)
+
+
+def rns_tile_conv(g: np.ndarray, d: np.ndarray, m_out: int, r: int, moduli) -> np.ndarray:
+    """rw/kernel.py:73-105: tile_conv_mod per modulus, then MRC."""
+    outs = [tile_conv_mod(encode(g, q), encode(d, q), m_out, r, q) for q in moduli]
+    return mrc(outs, moduli).astype(np.int32)
+
+
 def encode(a: np.ndarray, m: int) -> np.ndarray:
     return fold(a.astype(np.int32), m).astype(narrow(m))
 

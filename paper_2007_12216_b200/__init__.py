@@ -34,6 +34,8 @@ from .layer import (
     winograd_layer_conv,
 )
 from .residue import RnsSystem, mod_inverse, mod_reduce
+from .tensor_io import QTNS_MAGIC, QTNS_VERSION, read_tensor, write_tensor
+from .tiles import rns_tile_conv, tile_conv_mod
 from .transforms import (
     INF,
     ExactTransformSet,
@@ -60,5 +62,6 @@ __all__ = [
     "LayerSpec", "RangeReport", "StageTimings", "FilterBank", "range_check", "count_operations",
     "precompute_filter_transforms", "precompute_filters_oihw", "winograd_layer_conv", "layer_conv", "conv2d_rns",
     "direct_conv", "DirectWeights",
+    "read_tensor", "write_tensor", "QTNS_MAGIC", "QTNS_VERSION", "tile_conv_mod", "rns_tile_conv",
     "__version__",
 ]

@@ -93,6 +93,9 @@ def lib():
     return _lib
 
 
+RNSW_OK = 0
+
+
 def check(rc: int) -> None:
     if rc != 0:
         l = lib()

@@ -357,11 +357,20 @@ def _run_layer(plan, x_dev, b, h, w, c, k, pad, layout, bank, timings: StageTimi
     v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ev[0].record()
-    _native.check(l.rnsw_input_transform(plan.handle, vp(x_dev.data_ptr()), b, h, w, c, pad, layout, vp(v_ptr),
-                                         vb, s))
-    ev[1].record()
-    _native.check(l.rnsw_winograd_gemm(plan.handle, vp(v_ptr), vp(bank.data_ptr()), p, c, k, vp(m_ptr),
-                                       ws_bytes - vb, s))
+    # the same kernels rnsw_conv_forward picks: for C <= 4 on a tensor-core
+    # plan the compact transform + CUDA-core product (csrc/smallc.cu)
+    compact = c <= 4 and l.rnsw_input_transform_compact(plan.handle, vp(x_dev.data_ptr()), b, h, w, c, pad, layout,
+                                                        vp(v_ptr), vb, s) == _native.RNSW_OK
+    if compact:
+        ev[1].record()
+        _native.check(l.rnsw_small_channel_product(plan.handle, vp(v_ptr), vp(bank.data_ptr()), p, c, k, vp(m_ptr),
+                                                   ws_bytes - vb, s))
+    else:
+        _native.check(l.rnsw_input_transform(plan.handle, vp(x_dev.data_ptr()), b, h, w, c, pad, layout,
+                                             vp(v_ptr), vb, s))
+        ev[1].record()
+        _native.check(l.rnsw_winograd_gemm(plan.handle, vp(v_ptr), vp(bank.data_ptr()), p, c, k, vp(m_ptr),
+                                           ws_bytes - vb, s))
     ev[2].record()
     _native.check(l.rnsw_output_transform(plan.handle, vp(m_ptr), b, h, w, k, pad, layout, vp(y.data_ptr()), s))
     ev[3].record()

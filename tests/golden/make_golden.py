@@ -16,6 +16,11 @@ Outputs
                     configs (1, 3, 5 and VGG16 batch 1, every layer) computed
                     by the reference
   scalars.json      known answers: MRC inverses, signed bounds, chunk sizes
+  tiles.npz         single-tile API: kernel.tile_conv_mod / rns_tile_conv on
+                    seeded (stacked) tiles, 8- and 16-bit moduli
+  qtns.json         layer.write_tensor bytes (hex) of seeded int8 / int32 tensors
+
+``--only tiles,qtns`` regenerates just the named fixtures.
 """
 from __future__ import annotations
 
@@ -205,13 +210,75 @@ def gen_scalars():
     return out
 
 
+def gen_tiles():
+    """kernel.tile_conv_mod on residue tiles and kernel.rns_tile_conv on int8
+    tiles, with leading stack dims and a broadcast filter."""
+    arrays, meta = {}, []
+    cases = [(2, 3, 251, (5,)), (8, 3, 4331, (3, 2)), (4, 5, 241, (4,)), (14, 3, 4001, (2,)), (6, 3, 7, (3,))]
+    for i, (m, r, q, lead) in enumerate(cases):
+        rng = W.make_rng(2020, "tiles", i)
+        n = m + r - 1
+        mt = transforms.reduce_transforms_mod(transforms.cached_transforms(m, r), q)
+        h = (q - 1) // 2
+        g = rng.integers(-h, h + 1, lead + (r, r)).astype(np.int32)
+        d = rng.integers(-h, h + 1, lead + (n, n)).astype(np.int32)
+        y = kernel.tile_conv_mod(g, d, mt)
+        arrays.update({f"mod{i}_g": g, f"mod{i}_d": d, f"mod{i}_y": np.asarray(y)})
+        meta.append({"kind": "mod", "i": i, "m": m, "r": r, "modulus": q})
+    systems = [(2, 3, (251, 241, 239), (6,), False), (8, 3, (4001, 4331), (2, 3), True), (4, 5, (251, 241, 239), (3,), False)]
+    for i, (m, r, mods, lead, bcast) in enumerate(systems):
+        rng = W.make_rng(2020, "rns_tiles", i)
+        n = m + r - 1
+        system = residue.RnsSystem(mods)
+        mts = transforms.reduce_for_system(transforms.cached_transforms(m, r), system)
+        g = rng.integers(-128, 128, ((r, r) if bcast else lead + (r, r))).astype(np.int8)
+        d = rng.integers(-128, 128, lead + (n, n)).astype(np.int8)
+        y = kernel.rns_tile_conv(g, d, system, mts)
+        arrays.update({f"rns{i}_g": g, f"rns{i}_d": d, f"rns{i}_y": np.asarray(y)})
+        meta.append({"kind": "rns", "i": i, "m": m, "r": r, "moduli": list(mods)})
+    return arrays, meta
+
+
+def gen_qtns(tmp: Path):
+    out = []
+    rng = W.make_rng(2020, "qtns")
+    tensors = [rng.integers(-128, 128, (2, 3, 4, 5)).astype(np.int8),
+               rng.integers(-2**31, 2**31, (3, 7)).astype(np.int32),
+               np.array(-5, dtype=np.int32), np.zeros((0, 4), dtype=np.int8)]
+    for i, a in enumerate(tensors):
+        path = tmp / f"t{i}.qtns"
+        layer.write_tensor(path, a)
+        out.append({"dtype": str(a.dtype), "shape": list(a.shape), "values": a.reshape(-1).tolist(),
+                    "bytes_hex": path.read_bytes().hex()})
+    return out
+
+
 def main():
+    if "--only" in sys.argv:
+        only = set(sys.argv[sys.argv.index("--only") + 1].split(","))
+        if "tiles" in only:
+            arrays, meta = gen_tiles()
+            np.savez_compressed(HERE / "tiles.npz", **arrays)
+            (HERE / "tiles.json").write_text(json.dumps(meta, indent=1))
+        if "qtns" in only:
+            import tempfile
+
+            with tempfile.TemporaryDirectory() as td:
+                (HERE / "qtns.json").write_text(json.dumps(gen_qtns(Path(td)), indent=0))
+        return
     (HERE / "transforms.json").write_text(json.dumps(gen_transforms()))
     (HERE / "scalars.json").write_text(json.dumps(gen_scalars(), indent=1))
     arrays, meta = gen_small()
     np.savez_compressed(HERE / "small_cases.npz", **arrays)
     (HERE / "small_cases.json").write_text(json.dumps(meta, indent=1))
     (HERE / "verify.json").write_text(json.dumps(gen_verify(), indent=0))
+    arrays, meta = gen_tiles()
+    np.savez_compressed(HERE / "tiles.npz", **arrays)
+    (HERE / "tiles.json").write_text(json.dumps(meta, indent=1))
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        (HERE / "qtns.json").write_text(json.dumps(gen_qtns(Path(td)), indent=0))
     if "--no-digests" not in sys.argv:
         (HERE / "digests.json").write_text(json.dumps(gen_digests(), indent=1))
 
