@@ -41,15 +41,17 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
     const int k = kg * 8 + kk;
+    // channels 0..3 of one (plane, pos, k) row are 4 contiguous bytes (Cp >= 32)
+    uint32_t lo4 = 0, hi4 = 0;
+    if (k < K) {
+      const int8_t* b = U + (int64_t)t.uplane_base * plane_stride + ((int64_t)pos * K + k) * Cp;
+      lo4 = __ldg(reinterpret_cast<const uint32_t*>(b));
+      if (kPL == 2) hi4 = __ldg(reinterpret_cast<const uint32_t*>(b + plane_stride));
+    }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      int32_t v = 0;
-      if (k < K) {
-        const int8_t* b = U + (int64_t)t.uplane_base * plane_stride + ((int64_t)pos * K + k) * Cp + c;
-        v = b[0];
-        if (kPL == 2) v += 256 * (int32_t)b[plane_stride];
-      }
-      u[kk][c] = v;
+      const int32_t lo = (int32_t)(lo4 << (24 - 8 * c)) >> 24, hi = (int32_t)(hi4 << (24 - 8 * c)) >> 24;
+      u[kk][c] = kPL == 2 ? lo + 256 * hi : lo;
     }
   }
   const int32_t bias = kPL == 2 ? pos_bias(fm) : fm.off;
@@ -96,10 +98,10 @@ cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const
   const PlanDevice& d = plan.dev;
   const int npos = d.n * d.n, slots = npos * (g.Kp / 8);
   const int bx = (slots + 255) / 256;
-  // enough CTAs for ~4 waves of 8 per SM, each amortising its register-held
-  // filter residues over up to 64 tiles
+  // about 4 CTAs per SM in total, each amortising its register-held filter
+  // residues over up to 64 tiles (also at batch 1)
   const int64_t per_tile = (int64_t)bx * d.n_res;
-  const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, g.P * per_tile / (148 * 8 * 4)));
+  const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, g.P * per_tile / (148 * 4)));
   dim3 grid(bx, d.n_res, (unsigned)((g.P + tpc - 1) / tpc));
   if (d.res[0].planes == 2)
     smallc_product_kernel<2><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
