@@ -337,6 +337,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int16_t* out_row = args.Mw + ((p * args.n_res + res) * args.npos + pos) * (int64_t)args.Kp;
       const int col0 = kb * BN + half * kHalf;
       const bool row_ok = p < args.P;
+      if ((int64_t)pb * kBlockM + q * 32 >= args.P) {
+        // every row of this warp's lane quadrant is past the last tile (small
+        // or ragged P): nothing to reduce or store, just free the accumulator
+        release_acc(&tempty[as], lane);
+        continue;
+      }
       if (MAXPL == 2 && pl == 2) {
         epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane);
       } else {
