@@ -83,6 +83,26 @@ RNSW_DEV int32_t red_pos_biased_sub(int32_t n, const FastMod& f) {
   return (int32_t)((uint32_t)n - q * (uint32_t)f.m);
 }
 
+// Exact unsigned division by a runtime constant d for n < 2^31:
+// s = floor(log2 d), mul = ceil(2^(32+s) / d) as a 33-bit value (mul_hi:mul_lo);
+// floor(n/d) = (umulhi(n, mul_lo) + (mul_hi ? n : 0)) >> s.  The rounding
+// error n*(mul*d - 2^(32+s)) / (d*2^(32+s)) < n / 2^(32+s) < 1/d.
+struct FastDiv {
+  uint32_t mul_lo, mul_hi, shift, d;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t s = 0;
+  while ((2ull << s) <= d) ++s;
+  const unsigned long long num = 1ull << (32 + s);
+  const unsigned long long mul = (num + d - 1) / d;  // <= 2^32
+  return FastDiv{(uint32_t)mul, (uint32_t)(mul >> 32), s, d};
+}
+
+RNSW_DEV uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (__umulhi(n, f.mul_lo) + (f.mul_hi ? n : 0u)) >> f.shift;
+}
+
 // 64-bit exact symmetric reduction (used for the mixed-radix digits).
 RNSW_DEV int64_t sym_mod64(int64_t x, int64_t m) {
   int64_t r = x % m;

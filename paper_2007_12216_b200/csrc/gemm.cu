@@ -65,7 +65,26 @@ struct GemmArgs {
   int pos_out;  // fast2 16-bit residues written as y mod m in [0, m) (the output
                 // transform's limb split accepts it; saves the symmetric shift)
   int16_t* Mw;
+  FastDiv div_kb, div_pb, div_pos;  // work-tile index decomposition (total_tiles < 2^31)
 };
+
+// work tile t -> (kb fastest, pb, pos, res) without 64-bit divisions
+struct TileCoord {
+  int kb, pb, pos, res;
+};
+RNSW_DEV TileCoord tile_coord(uint32_t t, const GemmArgs& a) {
+  TileCoord c;
+  uint32_t q = fdiv(t, a.div_kb);
+  c.kb = (int)(t - q * a.div_kb.d);
+  t = q;
+  q = fdiv(t, a.div_pb);
+  c.pb = (int)(t - q * a.div_pb.d);
+  t = q;
+  q = fdiv(t, a.div_pos);
+  c.pos = (int)(t - q * a.div_pos.d);
+  c.res = (int)q;
+  return c;
+}
 
 template <int BN, int MAXPL>
 struct GemmTraits {
@@ -240,13 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
-        int64_t rest = t;
-        const int kb = (int)(rest % args.num_kb);
-        rest /= args.num_kb;
-        const int pb = (int)(rest % args.num_pb);
-        rest /= args.num_pb;
-        const int pos = (int)(rest % args.npos);
-        const int res = (int)(rest / args.npos);
+        const TileCoord tc = tile_coord((uint32_t)t, args);
+        const int kb = tc.kb, pb = tc.pb, pos = tc.pos, res = tc.res;
         const int pl = args.planes[res];
         const int upl = pl == 2 ? 4 : 1;
         const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
@@ -274,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
-        const int res = (int)(t / ((int64_t)args.num_kb * args.num_pb * args.npos));
+        const int res = tile_coord((uint32_t)t, args).res;
         const int pl = args.planes[res];
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
@@ -320,13 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kHalf = BN / 2;
     int it = 0;
     for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
-      int64_t rest = t;
-      const int kb = (int)(rest % args.num_kb);
-      rest /= args.num_kb;
-      const int pb = (int)(rest % args.num_pb);
-      rest /= args.num_pb;
-      const int pos = (int)(rest % args.npos);
-      const int res = (int)(rest / args.npos);
+      const TileCoord tc = tile_coord((uint32_t)t, args);
+      const int kb = tc.kb, pb = tc.pb, pos = tc.pos, res = tc.res;
       const int pl = args.planes[res];
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
@@ -455,6 +464,10 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   a.num_pb = (int)((P + kBlockM - 1) / kBlockM);
   a.num_kb = (Kp + bn - 1) / bn;
   a.total_tiles = (int64_t)d.n_res * a.npos * a.num_pb * a.num_kb;
+  if (a.total_tiles >= (1ll << 31)) return cudaErrorInvalidValue;  // FastDiv range
+  a.div_kb = make_fastdiv((uint32_t)a.num_kb);
+  a.div_pb = make_fastdiv((uint32_t)a.num_pb);
+  a.div_pos = make_fastdiv((uint32_t)a.npos);
   const int np = d.n_planes, nup = d.n_uplanes;
   if (maxpl == 2) {
     if (bn == 64) return run_gemm_bc<64, 2>(a, bc, V, U, np, nup, s);
