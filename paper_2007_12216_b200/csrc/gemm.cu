@@ -9,7 +9,7 @@
 //   warp 0      TMA producer: V and U limb planes -> 128B/64B/32B-swizzled smem
 //   warp 1      MMA issuer:   tcgen05.mma.cta_group::1.kind::i8, s32 in TMEM
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue:     tcgen05.ld -> limb recombination -> mod m -> int16
+//   warps 4-11  epilogue:     tcgen05.ld -> limb recombination -> mod m -> int16
 // TMEM holds two accumulator sets so the epilogue of tile i overlaps the
 // MMAs of tile i+1.
 //
