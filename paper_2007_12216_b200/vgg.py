@@ -169,17 +169,22 @@ class VGG16Rns:
             cur = nxt
         return cur
 
-    def graph(self, x):
+    def graph(self, x, bind: bool = False):
         """Capture forward_fused(x) for x's shape into a CUDA graph (buffers
         are preallocated per batch size, so replays reuse the same pointers).
         Returns a callable that copies new input into the captured input
-        buffer, replays, and returns the captured output tensor."""
+        buffer, replays, and returns the captured output tensor.  With
+        ``bind`` the graph reads ``x`` itself (no input copy; one graph per
+        input buffer)."""
         torch = _torch()
         batch = int(x.shape[0])
-        key = ("graph", batch)
+        key = ("graph", batch, x.data_ptr() if bind else None)
         if key not in self._buffers:
-            static_in = torch.empty_like(x)
-            static_in.copy_(x)
+            if bind:
+                static_in = x
+            else:
+                static_in = torch.empty_like(x)
+                static_in.copy_(x)
             # warm up (lazy module loading, attribute setting) outside capture
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
@@ -200,6 +205,60 @@ class VGG16Rns:
             return static_out
 
         return run
+
+    def run_stream(self, host_batches, host_outs, post=None) -> None:
+        """Serve a sequence of pinned host batches (B, 224, 224, 3) int8 into
+        pinned host outputs: each batch's H2D copy and the previous batch's
+        D2H copy run on a copy stream while the current batch computes (two
+        device input / output buffers, one CUDA graph per input buffer).
+        ``post`` maps the (B, 7, 7, 512) device result before it is copied
+        out (e.g. the multi-GPU gather); a None output entry skips the D2H.
+        Enqueues everything on the current stream and returns; the caller
+        synchronizes."""
+        torch = _torch()
+        n = len(host_batches)
+        if n == 0:
+            return
+        if len(host_outs) != n:
+            raise ValueError("one output buffer per batch")
+        shape = tuple(host_batches[0].shape)
+        comp = torch.cuda.current_stream()
+        key = ("stream", shape)
+        if key not in self._buffers:
+            dev_in = [torch.empty(shape, dtype=torch.int8, device="cuda") for _ in range(2)]
+            runs = [self.graph(d, bind=True) for d in dev_in]
+            self._buffers[key] = (dev_in, [None, None], runs, torch.cuda.Stream())
+        dev_in, dev_out, runs, copy = self._buffers[key]
+        ev = lambda: torch.cuda.Event()
+        h2d, done, d2h = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+        copy.wait_stream(comp)
+        with torch.cuda.stream(copy):
+            dev_in[0].copy_(host_batches[0], non_blocking=True)
+            h2d[0].record(copy)
+        for i in range(n):
+            j = i % 2
+            if i + 1 < n:
+                with torch.cuda.stream(copy):
+                    if i >= 1:
+                        copy.wait_event(done[1 - j])  # step i-1 has finished reading dev_in[1-j]
+                    dev_in[1 - j].copy_(host_batches[i + 1], non_blocking=True)
+                    h2d[1 - j].record(copy)
+            comp.wait_event(h2d[j])
+            if i >= 2:
+                comp.wait_event(d2h[j])  # dev_out[j] of step i-2 has left the device
+            y = runs[j]()
+            if post is not None:
+                y = post(y)
+            if dev_out[j] is None or dev_out[j].shape != y.shape:
+                dev_out[j] = torch.empty_like(y)
+            dev_out[j].copy_(y, non_blocking=True)
+            done[j].record(comp)
+            with torch.cuda.stream(copy):
+                copy.wait_event(done[j])
+                if host_outs[i] is not None:
+                    host_outs[i].copy_(dev_out[j], non_blocking=True)
+                d2h[j].record(copy)
+        comp.wait_stream(copy)
 
     def forward_fused_staged(self, x, record):
         """forward_fused() with a CUDA event pair around every kernel."""

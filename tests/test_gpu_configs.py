@@ -110,6 +110,23 @@ def test_vgg16_fused_glue_matches_unfused():
     assert sha(one) == digests()["vgg16/final"]["y"]
 
 
+def test_vgg16_streamed_serving_matches_forward():
+    """VGG16Rns.run_stream (copies overlapped with compute, CUDA graphs bound
+    to two input buffers) returns the same maps as forward_fused per batch."""
+    import torch
+    from paper_2007_12216_b200 import workloads as W
+    from paper_2007_12216_b200.vgg import VGG16Rns
+
+    net = VGG16Rns()
+    batches = [torch.from_numpy(W.vgg16_images(2, start=2 * i)).pin_memory() for i in range(4)]
+    outs = [torch.empty((2, 7, 7, 512), dtype=torch.int8).pin_memory() for _ in range(4)]
+    net.run_stream(batches, outs)
+    torch.cuda.synchronize()
+    for b, o in zip(batches, outs):
+        assert torch.equal(o, net.forward_fused(b.cuda()).cpu())
+    assert sha(outs[0][:1].numpy()) == digests()["vgg16/final"]["y"]
+
+
 def test_fused_requant_single_layers():
     import torch
     from oracle.vgg_ref import requant_pool
