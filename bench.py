@@ -4,9 +4,10 @@
 Workload (BASELINE.json config 4; config 2 at --batch 1): the 13 3x3 conv
 layers of VGG16 on 224x224x3 int8 images, every layer an exact int32
 RNS-Winograd convolution F(14x14,3x3) over RNS(4001,4331) plus the device
-glue (relu, >> shift, clip, 2x2 max-pool).  The batch is sharded by image
-over the ranks (one process per GPU); the only collective is one all-gather
-of the final (B/N,7,7,512) int8 maps.
+glue (relu, >> shift, clip, 2x2 max-pool).  Weak scaling: each rank (one
+process per GPU) serves its own shard of --batch images (default 256), so the
+global batch is 256 x N; the only collective is one all-gather of the final
+(B,7,7,512) int8 maps.
 
 Metric: direct-conv-equivalent INT8 TOPS = sum over layers of
 2*B*Ho*Wo*C*K*9 divided by the stack latency (whole job, all ranks).
@@ -42,7 +43,8 @@ def parse_args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256, help="global batch (images), sharded over ranks")
+    ap.add_argument("--batch", type=int, default=256,
+                    help="images per GPU (weak scaling: the global batch is batch x N, one shard per rank)")
     ap.add_argument("--impl", default="rnsw", choices=["rnsw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-images", type=int, default=1)
@@ -145,7 +147,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded PCG64, rw/cli.py:82-94 convention)",
         "config": {"workload": "VGG16 13x conv3x3 stack, 224x224x3, F(14x14,3x3), RNS(4001,4331), CPU sample",
                    "images_per_step": procs},
@@ -256,13 +258,16 @@ def run_gpu_arm(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    start, shard = parallel.shard_range(args.batch, world, rank)
+    # weak scaling: every rank serves its own shard of `batch` images (global
+    # batch = batch x N); the ranks meet once, in the final all-gather
+    global_batch = args.batch * world
+    start, shard = parallel.shard_range(global_batch, world, rank)
     net = VGG16Rns()
     x_host = W.vgg16_images(shard, start=start)
     x_pinned = torch.from_numpy(x_host).pin_memory()
     x_dev = x_pinned.cuda()
-    gathered = torch.empty((args.batch, 7, 7, 512), dtype=torch.int8, device="cuda") if world > 1 else None
-    out_pinned = torch.empty((args.batch if rank == 0 else shard, 7, 7, 512), dtype=torch.int8).pin_memory()
+    gathered = torch.empty((global_batch, 7, 7, 512), dtype=torch.int8, device="cuda") if world > 1 else None
+    out_pinned = torch.empty((global_batch if rank == 0 else shard, 7, 7, 512), dtype=torch.int8).pin_memory()
 
     fwd = net.forward if args.unfused else net.forward_fused
     if not args.unfused and not args.no_graph:
@@ -311,7 +316,7 @@ def run_gpu_arm(args):
         torch.cuda.synchronize()
         barrier()
     elapsed = parallel.max_over_ranks(e0.elapsed_time(e1) / 1e3, world, device="cuda")
-    total_ops = W.VGGConfig(batch=args.batch).direct_ops() * args.steps
+    total_ops = W.VGGConfig(batch=global_batch).direct_ops() * args.steps
     value = total_ops / elapsed / 1e12
     ms_per_step = elapsed / args.steps * 1e3
 
@@ -408,13 +413,13 @@ def run_gpu_arm(args):
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": n_warm, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded PCG64 images U{0..127}, weights round(N(0,20^2)) clipped; no dataset)",
-        "config": {"workload": f"BASELINE config 4: VGG16 13x conv3x3 stack, 224x224x3, batch {args.batch} "
-                               f"sharded {shard}/rank, F(14x14,3x3), RNS(4001,4331), relu/shift/maxpool glue "
+        "config": {"workload": f"BASELINE config 4: VGG16 13x conv3x3 stack, 224x224x3, batch {global_batch} "
+                               f"({shard} images per GPU), F(14x14,3x3), RNS(4001,4331), relu/shift/maxpool glue "
                                + ("as a separate kernel (int32 outputs materialised)" if args.unfused else
                                   "fused into each layer's output stage"),
-                   "global_batch": args.batch, "per_rank_batch": shard, "tile": "F(14x14,3x3)",
+                   "global_batch": global_batch, "per_rank_batch": shard, "tile": "F(14x14,3x3)",
                    "moduli": [4001, 4331], "parallelism": f"image-sharded x{world}, one all-gather at the end",
                    "l2": "inputs and intermediates larger than L2 (126 MB)",
                    "layer_ms": layer_ms, "layer_stage_ms": layer_stage_ms,
