@@ -22,6 +22,17 @@
 namespace rnsw {
 namespace {
 
+// tuning knobs (defaults measured best, see tools/variant_build.sh)
+#ifndef RNSW_K4_KK_UNROLL
+#define RNSW_K4_KK_UNROLL 1
+#endif
+#ifndef RNSW_K4_TPC_MAX
+#define RNSW_K4_TPC_MAX 8
+#endif
+#ifndef RNSW_K4_WAVES
+#define RNSW_K4_WAVES 4
+#endif
+
 constexpr int kKB = 32;       // output channels per CTA
 // Staged row for one (residue, channel): the 16x16 transform-domain tile with
 // a 2-element skew every 4 rows (word offset 8i + i/4 + 2t: fragment loads of
@@ -192,6 +203,11 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
       const bool ok = a < M && b < M && ti * M + a < g.Ho && tj * M + b < g.Wo;
       out_off[q] = !ok ? -1 : (g.layout == 0 ? (a * g.Wo + b) * g.K : a * g.Wo + b);
     }
+#if RNSW_K4_KK_UNROLL == 2
+#pragma unroll 2
+#else
+#pragma unroll 1
+#endif
     for (int kk = 0; kk < kKB / 4; ++kk) {
       const int k = warp * (kKB / 4) + kk;
       const bool kvalid = k0 + k < g.K;
@@ -369,7 +385,7 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
   // least ~4 waves of 4 CTAs per SM
   const int kblocks = (g.K + kKB - 1) / kKB;
   const int64_t units = g.P * kblocks;
-  const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(8, units / (148 * 4 * 4)));
+  const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(RNSW_K4_TPC_MAX, units / (148 * 4 * RNSW_K4_WAVES)));
   dim3 grid(kblocks, (unsigned)((g.P + tpc - 1) / tpc));
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
