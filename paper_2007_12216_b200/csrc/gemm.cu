@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -211,7 +212,14 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
   }
 }
 
-template <int BN, int BC, int MAXPL>
+// MC = 2: a cluster of two CTAs works on tile pairs (pb, pb+1) of the same
+// (residue, position, kb).  Each CTA TMA-loads its own V tile and half of
+// the filter-bank planes, multicast into both CTAs' stage, so the filter
+// bytes moved from L2 per MMA halve (the deep layers are bound by L2 -> SM
+// operand traffic, not by the tensor pipe: profiles/r01_gemm_*).  A stage is
+// refilled only after both CTAs' MMAs released it (empty barriers count 2,
+// MMA commits multicast to the pair).
+template <int BN, int BC, int MAXPL, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     winograd_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                          GemmArgs args) {
@@ -228,13 +236,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const int rank = MC == 2 ? (int)cluster_ctarank() : 0;
+  // work units: (kb fastest, pb group of MC tiles, pos, res); this CTA takes
+  // pb = MC * unit_pb + rank of every unit of its cluster
+  const int64_t u_begin = blockIdx.x / MC, u_step = gridDim.x / MC;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmU);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], MC);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -244,7 +256,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 2) tmem_alloc<Tr::kTmemCols>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (MC == 2)
+    cluster_sync();  // the peer multicasts into this CTA's stages and barriers
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -258,9 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+      for (int64_t t = u_begin; t < args.total_tiles; t += u_step) {
         const TileCoord tc = tile_coord((uint32_t)t, args);
-        const int kb = tc.kb, pb = tc.pb, pos = tc.pos, res = tc.res;
+        const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
         const int pl = args.planes[res];
         const int upl = pl == 2 ? 4 : 1;
         const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
@@ -270,9 +285,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int a = 0; a < pl; ++a)
             tma_load_3d(stage_a(stage, a), &tmV, &full[stage], kc * BC, pb * kBlockM,
                         (args.plane_base[res] + a) * args.npos + pos);
-          for (int b = 0; b < upl; ++b)
-            tma_load_3d(stage_b(stage, b), &tmU, &full[stage], kc * BC, kb * BN,
-                        (args.uplane_base[res] + b) * args.npos + pos);
+          if (MC == 2) {
+            // 16-bit only: this CTA's half of the 4 filter planes, to both CTAs
+            for (int b = 2 * rank; b < 2 * rank + 2; ++b)
+              tma_load_3d_mc(stage_b(stage, b), &tmU, &full[stage], kc * BC, kb * BN,
+                             (args.uplane_base[res] + b) * args.npos + pos, (uint16_t)0x3);
+          } else {
+            for (int b = 0; b < upl; ++b)
+              tma_load_3d(stage_b(stage, b), &tmU, &full[stage], kc * BC, kb * BN,
+                          (args.uplane_base[res] + b) * args.npos + pos);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -287,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+      for (int64_t t = u_begin; t < args.total_tiles; t += u_step, ++it) {
         const int res = tile_coord((uint32_t)t, args).res;
         const int pl = args.planes[res];
         const int as = it & 1;
@@ -312,13 +334,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t db_uhi = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);
               const uint64_t db_plo = umma_desc_kmajor(b0 + 2 * Cfg::kBPlaneBytes + 32 * k, BC);
               const uint64_t db_phi = umma_desc_kmajor(b0 + 3 * Cfg::kBPlaneBytes + 32 * k, BC);
+#ifdef RNSW_GEMM_DIAG_HALF_MMA  // timing diagnostic only: wrong results
+              mma_i8(d0, da_hi, db_phi, idesc, acc);
+              mma_i8(d0 + BN, da_lo, db_lo, idesc, acc);
+#else
               mma_i8(d0, da_hi, db_phi, idesc, acc);       // A256 = v_hi*u'_hi
               mma_i8(d0, da_lo, db_uhi, idesc, 1u);        //      + v_lo*u_hi
               mma_i8(d0 + BN, da_hi, db_plo, idesc, acc);  // A1   = v_hi*u'_lo
               mma_i8(d0 + BN, da_lo, db_lo, idesc, 1u);    //      + v_lo*u_lo
+#endif
             }
           }
-          mma_commit(&empty[stage]);
+          if (MC == 2)
+            mma_commit_mc(&empty[stage], (uint16_t)0x3);
+          else
+            mma_commit(&empty[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -333,9 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = (warp - 4) >> 2;       // column half of the accumulator tile
     constexpr int kHalf = BN / 2;
     int it = 0;
-    for (int64_t t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+    for (int64_t t = u_begin; t < args.total_tiles; t += u_step, ++it) {
       const TileCoord tc = tile_coord((uint32_t)t, args);
-      const int kb = tc.kb, pb = tc.pb, pos = tc.pos, res = tc.res;
+      const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
       const int pl = args.planes[res];
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
@@ -366,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<Tr::kTmemCols>(tmem_base);
   }
+  if (MC == 2) cluster_sync();  // no CTA leaves while its peer may still signal it
 }
 
 // ---------------------------------------------------------------------------
@@ -390,14 +421,14 @@ bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t 
 
 int g_num_sms = 0;
 
-template <int BN, int BC, int MAXPL>
+template <int BN, int BC, int MAXPL, int MC>
 cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
                      cudaStream_t s) {
   using Cfg = GemmConfig<BN, BC, MAXPL>;
   CUtensorMap tmV, tmU;
   if (!make_tmap(&tmV, V, a.Cp, a.P, (int64_t)n_planes * a.npos, BC, kBlockM)) return cudaErrorInvalidValue;
   if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_uplanes * a.npos, BC, BN)) return cudaErrorInvalidValue;
-  auto kern = winograd_gemm_kernel<BN, BC, MAXPL>;
+  auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
   if (g_num_sms == 0) {
@@ -405,19 +436,35 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  int64_t grid = a.total_tiles < g_num_sms ? a.total_tiles : g_num_sms;
-  if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kThreads, Cfg::kSmemBytes, s>>>(tmV, tmU, a);
-  return cudaGetLastError();
+  int64_t grid = a.total_tiles * MC < g_num_sms ? a.total_tiles * MC : g_num_sms;
+  grid = grid / MC * MC;
+  if (grid < MC) grid = MC;
+  if (MC == 1) {
+    kern<<<(unsigned)grid, kThreads, Cfg::kSmemBytes, s>>>(tmV, tmU, a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = MC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tmV, tmU, a);
 }
 
-template <int BN, int MAXPL>
+template <int BN, int MAXPL, int MC = 1>
 cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
                         cudaStream_t s) {
   switch (bc) {
-    case 32: return run_gemm<BN, 32, MAXPL>(a, V, U, n_planes, n_uplanes, s);
-    case 64: return run_gemm<BN, 64, MAXPL>(a, V, U, n_planes, n_uplanes, s);
-    default: return run_gemm<BN, 128, MAXPL>(a, V, U, n_planes, n_uplanes, s);
+    case 32: return run_gemm<BN, 32, MAXPL, MC>(a, V, U, n_planes, n_uplanes, s);
+    case 64: return run_gemm<BN, 64, MAXPL, MC>(a, V, U, n_planes, n_uplanes, s);
+    default: return run_gemm<BN, 128, MAXPL, MC>(a, V, U, n_planes, n_uplanes, s);
   }
 }
 
@@ -469,6 +516,17 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   a.div_pb = make_fastdiv((uint32_t)a.num_pb);
   a.div_pos = make_fastdiv((uint32_t)a.npos);
   const int np = d.n_planes, nup = d.n_uplanes;
+  bool all16 = true;
+  for (int r = 0; r < d.n_res; ++r) all16 = all16 && d.res[r].planes == 2;
+  static const bool no_mc = getenv("RNSW_GEMM_NO_MC") != nullptr;  // A/B switch
+  if (maxpl == 2 && all16 && a.num_pb >= 2 && !no_mc) {
+    // CTA pairs over (pb, pb+1) with the filter planes multicast (see the kernel)
+    const int num_pbu = (a.num_pb + 1) / 2;
+    a.total_tiles = (int64_t)d.n_res * a.npos * num_pbu * a.num_kb;
+    a.div_pb = make_fastdiv((uint32_t)num_pbu);
+    if (bn == 64) return run_gemm_bc<64, 2, 2>(a, bc, V, U, np, nup, s);
+    return run_gemm_bc<128, 2, 2>(a, bc, V, U, np, nup, s);
+  }
   if (maxpl == 2) {
     if (bn == 64) return run_gemm_bc<64, 2>(a, bc, V, U, np, nup, s);
     return run_gemm_bc<128, 2>(a, bc, V, U, np, nup, s);
