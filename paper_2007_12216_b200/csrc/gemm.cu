@@ -17,7 +17,8 @@
 // filter bank holds the limbs of u and of u' = 256*u mod m.  Then
 //     v*u = v_hi*256*u + v_lo*u  ==  v_hi*u' + v_lo*u               (mod m)
 //         == 256*(v_hi*u'_hi + v_lo*u_hi) + (v_hi*u'_lo + v_lo*u_lo)
-// so each chunk issues 4 MMAs into 2 accumulators (A256, A1); the epilogue
+// so each k-step issues 2 MMAs of N = 2*BN ([u'_hi;u'_lo] and [u_hi;u_lo]
+// stacked in smem) into the adjacent accumulators [A256 | A1]; the epilogue
 // recombines 256*A256 + A1 (< 2^28 for C <= 512) with a single exact
 // reduction.  |acc| <= C * 128^2 < 2^31 for C <= 131071 (host-checked).
 #include <cuda.h>
@@ -266,7 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto stage_a = [&](int s, int pl) { return smem + s * Cfg::kStageBytes + pl * Cfg::kAPlaneBytes; };
   auto stage_b = [&](int s, int pl) {
     return smem + s * Cfg::kStageBytes + MAXPL * Cfg::kAPlaneBytes + pl * Cfg::kBPlaneBytes;
-  };  // B planes: [0] u_lo, [1] u_hi, [2] u'_lo, [3] u'_hi (16-bit) or [0] u
+  };  // B smem slots, 16-bit: [0] u'_hi, [1] u'_lo, [2] u_hi, [3] u_lo (bank plane b -> slot 3 - b),
+     // so slots 0-1 and 2-3 are each one 2*BN-row K-major operand; 8-bit: [0] u
+  auto bslot = [&](int b, int pl) { return (MAXPL == 2 && pl == 2) ? 3 - b : b; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -288,11 +291,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (MC == 2) {
             // 16-bit only: this CTA's half of the 4 filter planes, to both CTAs
             for (int b = 2 * rank; b < 2 * rank + 2; ++b)
-              tma_load_3d_mc(stage_b(stage, b), &tmU, &full[stage], kc * BC, kb * BN,
+              tma_load_3d_mc(stage_b(stage, bslot(b, pl)), &tmU, &full[stage], kc * BC, kb * BN,
                              (args.uplane_base[res] + b) * args.npos + pos, (uint16_t)0x3);
           } else {
             for (int b = 0; b < upl; ++b)
-              tma_load_3d(stage_b(stage, b), &tmU, &full[stage], kc * BC, kb * BN,
+              tma_load_3d(stage_b(stage, bslot(b, pl)), &tmU, &full[stage], kc * BC, kb * BN,
                           (args.uplane_base[res] + b) * args.npos + pos);
           }
           if (++stage == S) {
@@ -306,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc = idesc_i8(kBlockM, BN);
+      constexpr uint32_t idesc2 = idesc_i8(kBlockM, 2 * BN);  // 16-bit: [A256 | A1] in one MMA
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -330,19 +334,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (MAXPL == 1 || pl == 1) {
               mma_i8(d0, da_lo, db_lo, idesc, acc);
             } else {
+              // v*u = 256*(v_hi*u'_hi + v_lo*u_hi) + (v_hi*u'_lo + v_lo*u_lo): the
+              // accumulator columns [A256 | A1] take N = 2*BN rows of B at once
               const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
-              const uint64_t db_uhi = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);
-              const uint64_t db_plo = umma_desc_kmajor(b0 + 2 * Cfg::kBPlaneBytes + 32 * k, BC);
-              const uint64_t db_phi = umma_desc_kmajor(b0 + 3 * Cfg::kBPlaneBytes + 32 * k, BC);
-#ifdef RNSW_GEMM_DIAG_HALF_MMA  // timing diagnostic only: wrong results
-              mma_i8(d0, da_hi, db_phi, idesc, acc);
-              mma_i8(d0 + BN, da_lo, db_lo, idesc, acc);
-#else
-              mma_i8(d0, da_hi, db_phi, idesc, acc);       // A256 = v_hi*u'_hi
-              mma_i8(d0, da_lo, db_uhi, idesc, 1u);        //      + v_lo*u_hi
-              mma_i8(d0 + BN, da_hi, db_plo, idesc, acc);  // A1   = v_hi*u'_lo
-              mma_i8(d0 + BN, da_lo, db_lo, idesc, 1u);    //      + v_lo*u_lo
-#endif
+              const uint64_t db_p = umma_desc_kmajor(b0 + 32 * k, BC);                         // [u'_hi ; u'_lo]
+              const uint64_t db_u = umma_desc_kmajor(b0 + 2 * Cfg::kBPlaneBytes + 32 * k, BC);  // [u_hi ; u_lo]
+              mma_i8(d0, da_hi, db_p, idesc2, acc);
+              mma_i8(d0, da_lo, db_u, idesc2, 1u);
             }
           }
           if (MC == 2)
