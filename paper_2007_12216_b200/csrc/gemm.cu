@@ -272,36 +272,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bslot = [&](int b, int pl) { return (MAXPL == 2 && pl == 2) ? 3 - b : b; };
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t t = u_begin; t < args.total_tiles; t += u_step) {
-        const TileCoord tc = tile_coord((uint32_t)t, args);
-        const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
-        const int pl = args.planes[res];
-        const int upl = pl == 2 ? 4 : 1;
-        const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
-        for (int kc = 0; kc < args.nkc; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          for (int a = 0; a < pl; ++a)
-            tma_load_3d(stage_a(stage, a), &tmV, &full[stage], kc * BC, pb * kBlockM,
-                        (args.plane_base[res] + a) * args.npos + pos);
-          if (MC == 2) {
-            // 16-bit only: this CTA's half of the 4 filter planes, to both CTAs
-            for (int b = 2 * rank; b < 2 * rank + 2; ++b)
-              tma_load_3d_mc(stage_b(stage, bslot(b, pl)), &tmU, &full[stage], kc * BC, kb * BN,
-                             (args.uplane_base[res] + b) * args.npos + pos, (uint16_t)0x3);
-          } else {
-            for (int b = 0; b < upl; ++b)
-              tma_load_3d(stage_b(stage, bslot(b, pl)), &tmU, &full[stage], kc * BC, kb * BN,
-                          (args.uplane_base[res] + b) * args.npos + pos);
-          }
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1;
-          }
+    // ---------------- TMA producer (whole warp) ----------------
+    // lane 0 arms the stage barrier, then lane j issues load j of the chunk
+    // (A planes, then this CTA's filter planes), so the chunk's 4-6 TMA
+    // instructions go out together instead of back to back from one thread
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = u_begin; t < args.total_tiles; t += u_step) {
+      const TileCoord tc = tile_coord((uint32_t)t, args);
+      const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
+      const int pl = args.planes[res];
+      const int upl = pl == 2 ? 4 : 1;
+      const int nb = MC == 2 ? 2 : upl;        // filter planes this CTA loads
+      const int b0 = MC == 2 ? 2 * rank : 0;   // first of them
+      const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
+      for (int kc = 0; kc < args.nkc; ++kc) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+        __syncwarp();
+        if (lane < pl) {
+          tma_load_3d(stage_a(stage, lane), &tmV, &full[stage], kc * BC, pb * kBlockM,
+                      (args.plane_base[res] + lane) * args.npos + pos);
+        } else if (lane < pl + nb) {
+          const int b = b0 + lane - pl;
+          if (MC == 2)
+            tma_load_3d_mc(stage_b(stage, bslot(b, pl)), &tmU, &full[stage], kc * BC, kb * BN,
+                           (args.uplane_base[res] + b) * args.npos + pos, (uint16_t)0x3);
+          else
+            tma_load_3d(stage_b(stage, bslot(b, pl)), &tmU, &full[stage], kc * BC, kb * BN,
+                        (args.uplane_base[res] + b) * args.npos + pos);
+        }
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
