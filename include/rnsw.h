@@ -108,7 +108,9 @@ int rnsw_input_transform_compact(const rnsw_plan* plan, const int8_t* x, int B, 
 int rnsw_small_channel_product(const rnsw_plan* plan, const void* V16, const void* U, int64_t P, int C,
                                int K, void* Mw, size_t Mw_bytes, void* stream);
 /* Stage 2: per (residue, position) GEMM on tcgen05 kind::i8, reduced mod m_i
- * -> Winograd-domain product residues [P][n_res][N*N][Kp] int16. */
+ * -> Winograd-domain product residues, int16, in blocks of 128 tiles:
+ * [ceil(P/128)][n_res][N*N][128][Kp] (tile p of block p/128 at row p%128),
+ * so each GEMM output tile is written as one contiguous run. */
 int rnsw_winograd_gemm(const rnsw_plan* plan, const void* V, const void* U, int64_t P, int C,
                        int K, void* Mw, size_t Mw_bytes, void* stream);
 /* Stage 3: Y = AT M A mod m_i, mixed-radix reconstruction, crop/scatter. */

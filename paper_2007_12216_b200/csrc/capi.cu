@@ -95,8 +95,8 @@ int make_geometry(const rnsw_plan* plan, int B, int H, int W, int C, int K, int 
 }
 
 size_t v_bytes(const PlanDevice& d, int64_t P, int Cp) { return (size_t)d.n_planes * d.n * d.n * P * Cp; }
-size_t m_bytes(const PlanDevice& d, int64_t P, int Kp) {
-  return (size_t)P * d.n_res * d.n * d.n * Kp * sizeof(int16_t);
+size_t m_bytes(const PlanDevice& d, int64_t P, int Kp) {  // blocked layout (kernels.h mw_offset)
+  return (size_t)((P + 127) / 128) * 128 * d.n_res * d.n * d.n * Kp * sizeof(int16_t);
 }
 
 }  // namespace

@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int64_t p = (int64_t)pb * kBlockM + q * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Tr::kAccCols + half * kHalf;
-      int16_t* out_row = args.Mw + ((p * args.n_res + res) * args.npos + pos) * (int64_t)args.Kp;
+      int16_t* out_row = args.Mw + mw_offset(p, res * args.npos + pos, args.n_res * args.npos, args.Kp);
       const int col0 = kb * BN + half * kHalf;
       const bool row_ok = p < args.P;
       if ((int64_t)pb * kBlockM + q * 32 >= args.P) {

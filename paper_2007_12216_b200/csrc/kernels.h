@@ -20,6 +20,15 @@ struct Geometry {
   int bc;              // channel chunk per MMA stage (32 / 64 / 128 bytes)
 };
 
+// Mw (K3 -> K4) layout: blocks of 128 tiles, [ceil(P/128)][res][pos][128][Kp]
+// int16 residues, so every (tile block, residue, position) output tile of the
+// GEMM is one contiguous run of 128*Kp values (its stores stream instead of
+// scattering 128 rows over the whole buffer).  rp = res * npos + pos,
+// nrp = n_res * npos.
+__host__ __device__ inline int64_t mw_offset(int64_t p, int rp, int nrp, int Kp) {
+  return (((p >> 7) * nrp + rp) * 128 + (p & 127)) * (int64_t)Kp;
+}
+
 // Host-side mirror of the plan (kept next to the device copy).
 struct PlanHost {
   PlanDevice dev;         // host copy of the tables

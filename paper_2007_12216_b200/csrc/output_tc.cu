@@ -4,7 +4,7 @@
 //
 // CTA = a run of consecutive tiles p x 32 output channels, 4 warps x 8
 // channels; the transform constants are built once per CTA.  The GEMM
-// output Mw[p][res][pos][k] (int16 residues) is staged through shared memory
+// output Mw (int16 residues, blocked layout of kernels.h) is staged through shared memory
 // transposed to [res][k][pos] so each warp can feed one channel's 16x16
 // transform-domain tile straight into mma.sync fragments:
 //   pass 1  Z^T = AT * Mat^T      (A = AT constants, B = Mat^T from smem)
@@ -151,7 +151,9 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   const bool st_j_in = st_j < N;
   const bool st_ok = st_j_in && k0 + 8 * st_kc < g.Kp;
   const int st_urows = (N - st_i0 + 1) >> 1;  // rows i0 + 2u < N
-  const int st_src = (st_i0 * N + st_j) * g.Kp + k0 + 8 * st_kc;
+  // Mw rows (res, pos) of one tile are 128*Kp apart (blocked layout, kernels.h)
+  const int row_stride = 128 * g.Kp;
+  const int st_src = (st_i0 * N + st_j) * row_stride + k0 + 8 * st_kc;
   int16_t* st_dst = S + 8 * st_kc * kRowS + stage_off(st_i0, st_j);
 
   for (int p = p_begin; p < p_end; ++p) {
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
     // u = 0..7, for every residue, so all addressing is per-thread constants
     // plus compile-time offsets.  Loads go out in groups of 4 ahead of their
     // transposing stores.
-    const int16_t* src = Mw + (int64_t)p * nres * npos * g.Kp + st_src;
+    const int16_t* src = Mw + mw_offset(p, 0, nres * npos, g.Kp) + st_src;
 #pragma unroll 1
     for (int r = 0; r < NRES; ++r) {
 #pragma unroll
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
         for (int w = 0; w < 4; ++w) {
           const int u = 4 * half + w;
           v[w] = make_int4(0, 0, 0, 0);
-          if (st_ok && u < st_urows) v[w] = __ldg(reinterpret_cast<const int4*>(src + (r * npos + 2 * u * N) * g.Kp));
+          if (st_ok && u < st_urows) v[w] = __ldg(reinterpret_cast<const int4*>(src + (r * npos + 2 * u * N) * row_stride));
         }
 #pragma unroll
         for (int w = 0; w < 4; ++w) {

@@ -6,7 +6,7 @@
 // stream 10x more V than the layer has, so for C <= 4 the input transform
 // writes compact int16 residues V16[res][P][pos][4] (input_tc.cu, kCompact)
 // and this kernel forms the product directly into the output transform's
-// input layout Mw[P][res][pos][Kp].  Each thread keeps the filter residues
+// input layout Mw (blocked, kernels.h mw_offset).  Each thread keeps the filter residues
 // of one (residue, position, 8 output channels) in registers for a run of
 // tiles: per tile it loads 8 bytes of V16 (shared by 8 threads), does
 // 4 x 8 exact int32 products and 8 division-free reductions, and stores one
@@ -57,12 +57,12 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
   const int32_t bias = kPL == 2 ? pos_bias(fm) : fm.off;
   const int p_begin = blockIdx.z * tiles_per_cta, p_end = min(P, p_begin + tiles_per_cta);
   const uint2* src = reinterpret_cast<const uint2*>(V16) + ((int64_t)r * P + p_begin) * npos + pos;
-  uint4* dst = reinterpret_cast<uint4*>(Mw + (((int64_t)p_begin * nres + r) * npos + pos) * Kp) + kg;
-  const int64_t dst_step = (int64_t)nres * npos * Kp / 8;  // uint4 per tile
+  const int rp = r * npos + pos, nrp = nres * npos;
   // two tiles of V16 in flight ahead of the one being reduced
   uint2 wa = p_begin < p_end ? __ldg(src) : make_uint2(0, 0);
   uint2 wb = p_begin + 1 < p_end ? __ldg(src + npos) : make_uint2(0, 0);
-  for (int p = p_begin; p < p_end; ++p, src += npos, dst += dst_step) {
+  for (int p = p_begin; p < p_end; ++p, src += npos) {
+    uint4* dst = reinterpret_cast<uint4*>(Mw + mw_offset(p, rp, nrp, Kp)) + kg;
     const uint2 w = wa;
     wa = wb;
     if (p + 2 < p_end) wb = __ldg(src + 2 * npos);

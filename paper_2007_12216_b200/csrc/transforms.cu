@@ -9,7 +9,8 @@
 // Device layouts (all int8 limb planes are s8, see residue.planes_for_modulus):
 //   U  [plane][pos][K][Cp]      pos = i*N + j of the N x N transform domain
 //   V  [plane][pos][P][Cp]      P = B*th*tw tiles, tile p = (b*th + ti)*tw + tj
-//   Mw [P][res][pos][Kp] int16  GEMM output, symmetric residues
+//   Mw [P/128][res][pos][128][Kp] int16  GEMM output, symmetric residues
+//                                          (blocked layout, kernels.h mw_offset)
 #include <cstdio>
 #include <cstdlib>
 
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(256) output_transform_kernel(const PlanDevice*
   }
   for (int idx = tid; idx < nres * npos * kChanBlock; idx += blockDim.x) {
     const int k = idx % kChanBlock, rp = idx / kChanBlock;
-    S[idx] = (k0 + k < g.Kp) ? (int32_t)Mw[(p * nres * npos + rp) * g.Kp + k0 + k] : 0;
+    S[idx] = (k0 + k < g.Kp) ? (int32_t)Mw[mw_offset(p, rp, nres * npos, g.Kp) + k0 + k] : 0;
   }
   __syncthreads();
 

@@ -85,8 +85,11 @@ def winograd_gemm(vbuf, bank, tile_m: int, r: int, system, p: int, c: int, k: in
                                        nbytes, _stream_ptr()))
     kp = (k + 15) // 16 * 16
     n2 = plan.n * plan.n
-    view = mw.view(torch.int16).view(p, len(plan.moduli), n2, kp)[..., :k]
-    return mw, {m: view[:, i].permute(1, 0, 2) for i, m in enumerate(plan.moduli)}
+    # blocked layout [ceil(P/128)][res][pos][128][Kp] (include/rnsw.h)
+    nb = (p + 127) // 128
+    view = mw.view(torch.int16)[: nb * len(plan.moduli) * n2 * 128 * kp].view(nb, len(plan.moduli), n2, 128, kp)
+    view = view.permute(1, 2, 0, 3, 4).reshape(len(plan.moduli), n2, nb * 128, kp)[:, :, :p, :k]
+    return mw, {m: view[i] for i, m in enumerate(plan.moduli)}
 
 
 def output_residues(mw, tile_m: int, r: int, system, p: int, k: int):
