@@ -171,6 +171,27 @@ RNSW_DEV void tma_load_3d(void* dst, const void* desc, uint64_t* bar, int c0, in
       : "memory");
 }
 
+// Bulk tensor store smem -> global (bulk-group completion).
+RNSW_DEV void tma_store_2d(const void* desc, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+RNSW_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N bulk groups still read their shared-memory source
+template <int N>
+RNSW_DEV void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+RNSW_DEV void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+RNSW_DEV void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // The same load delivered to every CTA of the cluster in ctaMask (same smem
 // offset, each CTA's mbarrier at the same offset receives the bytes).
 RNSW_DEV void tma_load_3d_mc(void* dst, const void* desc, uint64_t* bar, int c0, int c1, int c2, uint16_t mask) {

@@ -107,12 +107,31 @@ constexpr int stage_bytes(int bn, int maxpl) {
 template <int BN, int BC, int MAXPL>
 struct GemmConfig {
   static constexpr int kStageBytes = stage_bytes<BC>(BN, MAXPL);
-  static constexpr int kStagesRaw = (200 * 1024) / kStageBytes;
+  // BN <= 128: the epilogue stages each output tile in shared memory (int16,
+  // 128B-swizzled boxes of 64 columns) and writes it with TMA bulk tensor
+  // stores; per-thread 16-byte stores of 128 scattered rows were the GEMM's
+  // bottleneck (profiles/r01_gemm_*).  BN = 256 (8-bit) keeps direct stores.
+  static constexpr bool kTmaStore = BN <= 128;
+  static constexpr int kStoreBytes = kTmaStore ? kBlockM * BN * 2 : 0;
+  static constexpr int kStagesRaw = (224 * 1024 - kStoreBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kAPlaneBytes = kBlockM * BC;
   static constexpr int kBPlaneBytes = BN * BC;
-  static constexpr size_t kSmemBytes = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256 /*barriers*/;
+  static constexpr size_t kSmemBytes =
+      1024 /*align slack*/ + (size_t)kStages * kStageBytes + kStoreBytes + 256 /*barriers*/;
 };
+
+// one output row (tile) of 16 int16 residues into the staging tile: box
+// col / 64, 128-byte rows, 16-byte chunk c at c ^ (row & 7) (TMA SWIZZLE_128B)
+RNSW_DEV void sts16_swz(uint8_t* stg, int row, int col, const int32_t (&r)[16]) {
+  uint32_t w[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) w[e] = __byte_perm((uint32_t)r[2 * e], (uint32_t)r[2 * e + 1], 0x5410);
+  uint8_t* box = stg + (col >> 6) * (kBlockM * 128) + row * 128;
+  const int c = (col & 63) >> 3;
+  *reinterpret_cast<uint4*>(box + (((c) ^ (row & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+  *reinterpret_cast<uint4*>(box + (((c + 1) ^ (row & 7)) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
+}
 
 // Epilogue helpers.  Each thread owns one accumulator row (tile p) and a
 // half of the BN columns.  All TMEM loads of a batch are issued before a
@@ -142,7 +161,7 @@ RNSW_DEV void release_acc(uint64_t* bar, int lane) {
 // 16-bit residues: two accumulators (A256, A1) per column.
 template <int BN, int ACC_COLS>
 RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
-                             uint64_t* tempty, int lane) {
+                             uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 32 ? kHalf : 32;  // 2 x 32 registers in flight
   const FastMod fm = a.fm[res];
@@ -178,7 +197,10 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
           r[e] = reduce_generic(reduce_generic(hi[j][e], a, res) * 256 + reduce_generic(lo[j][e], a, res), a, res);
       }
       const int col = col0 + c0 + 16 * j;
-      if (row_ok && col < a.Kp) store16(out_row + col, r);
+      if (stg != nullptr)
+        sts16_swz(stg, srow, scol0 + c0 + 16 * j, r);
+      else if (row_ok && col < a.Kp)
+        store16(out_row + col, r);
     }
   }
 }
@@ -186,7 +208,7 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
 // 8-bit residues: one accumulator per column.
 template <int BN>
 RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
-                              uint64_t* tempty, int lane) {
+                              uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 64 ? kHalf : 64;
   const FastMod fm = a.fm[res];
@@ -208,7 +230,10 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
         for (int e = 0; e < 16; ++e) r[e] = reduce_generic(v[j][e], a, res);
       }
       const int col = col0 + c0 + 16 * j;
-      if (row_ok && col < a.Kp) store16(out_row + col, r);
+      if (stg != nullptr)
+        sts16_swz(stg, srow, scol0 + c0 + 16 * j, r);
+      else if (row_ok && col < a.Kp)
+        store16(out_row + col, r);
     }
   }
 }
@@ -223,13 +248,14 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
 template <int BN, int BC, int MAXPL, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     winograd_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
-                         GemmArgs args) {
+                         const __grid_constant__ CUtensorMap tmM, GemmArgs args) {
   using Cfg = GemmConfig<BN, BC, MAXPL>;
   using Tr = GemmTraits<BN, MAXPL>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint8_t* stg = smem + S * Cfg::kStageBytes;  // output staging tile (kTmaStore)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStoreBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
@@ -377,18 +403,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       int16_t* out_row = args.Mw + mw_offset(p, res * args.npos + pos, args.n_res * args.npos, args.Kp);
       const int col0 = kb * BN + half * kHalf;
       const bool row_ok = p < args.P;
-      if ((int64_t)pb * kBlockM + q * 32 >= args.P) {
-        // every row of this warp's lane quadrant is past the last tile (small
-        // or ragged P): nothing to reduce or store, just free the accumulator
-        release_acc(&tempty[as], lane);
-        continue;
+      const bool quad_live = (int64_t)pb * kBlockM + q * 32 < args.P;
+      if (Cfg::kTmaStore) {
+        // the previous tile's bulk store must have read the staging tile
+        if (warp == 4 && lane == 0) bulk_wait_read<0>();
+        named_bar_sync(1, 256);
       }
-      if (MAXPL == 2 && pl == 2) {
-        epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane);
+      uint8_t* stg_t = Cfg::kTmaStore ? stg : nullptr;
+      if (!quad_live) {
+        // every row of this warp's lane quadrant is past the last tile (small
+        // or ragged P): nothing to reduce, just free the accumulator
+        release_acc(&tempty[as], lane);
+      } else if (MAXPL == 2 && pl == 2) {
+        epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane, stg_t,
+                                         q * 32 + lane, half * kHalf);
       } else {
-        epilogue_single<BN>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane);
+        epilogue_single<BN>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane, stg_t, q * 32 + lane,
+                            half * kHalf);
+      }
+      if (Cfg::kTmaStore) {
+        fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
+        named_bar_sync(1, 256);
+        if (warp == 4 && lane == 0) {
+          const int row0 = (int)(((int64_t)pb * args.n_res * args.npos + res * args.npos + pos) * kBlockM);
+#pragma unroll
+          for (int bx = 0; bx < (BN + 63) / 64; ++bx) tma_store_2d(&tmM, stg + bx * (kBlockM * 128), kb * BN + 64 * bx, row0);
+          bulk_commit();
+        }
       }
     }
+    if (Cfg::kTmaStore && warp == 4 && lane == 0) bulk_wait<0>();  // stores complete before exit
   }
 
   tc_fence_before();
@@ -402,6 +446,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------------------
 // Host side: tensor maps and dispatch.
+
+// Mw as a 2-D int16 array [rows][Kp] (blocked layout rows), box 64 x 128,
+// 128B swizzle: the epilogue's bulk store target.
+bool make_tmap_mw(CUtensorMap* tm, const void* base, int Kp, int64_t rows) {
+  auto encode = encode_fn();
+  if (encode == nullptr) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)kBlockM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 
 // 3-D view [slabs][rows][Cp] of int8 limb planes; box = (bc bytes, box_rows, 1).
 bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t slabs, int bc, int box_rows) {
@@ -429,6 +488,9 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   CUtensorMap tmV, tmU;
   if (!make_tmap(&tmV, V, a.Cp, a.P, (int64_t)n_planes * a.npos, BC, kBlockM)) return cudaErrorInvalidValue;
   if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_uplanes * a.npos, BC, BN)) return cudaErrorInvalidValue;
+  CUtensorMap tmM;
+  const int64_t mw_rows = (a.P + kBlockM - 1) / kBlockM * (int64_t)a.n_res * a.npos * kBlockM;
+  if (!make_tmap_mw(&tmM, a.Mw, a.Kp, mw_rows)) return cudaErrorInvalidValue;
   auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
@@ -441,7 +503,7 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   grid = grid / MC * MC;
   if (grid < MC) grid = MC;
   if (MC == 1) {
-    kern<<<(unsigned)grid, kThreads, Cfg::kSmemBytes, s>>>(tmV, tmU, a);
+    kern<<<(unsigned)grid, kThreads, Cfg::kSmemBytes, s>>>(tmV, tmU, tmM, a);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -456,7 +518,7 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmV, tmU, a);
+  return cudaLaunchKernelEx(&cfg, kern, tmV, tmU, tmM, a);
 }
 
 template <int BN, int MAXPL, int MC = 1>
