@@ -104,14 +104,14 @@ constexpr int stage_bytes(int bn, int maxpl) {
   return maxpl * kBlockM * BC + (maxpl == 2 ? 4 : 1) * bn * BC;
 }
 
-template <int BN, int BC, int MAXPL>
+template <int BN, int BC, int MAXPL, bool TS = true>
 struct GemmConfig {
   static constexpr int kStageBytes = stage_bytes<BC>(BN, MAXPL);
   // BN <= 128: the epilogue stages each output tile in shared memory (int16,
   // 128B-swizzled boxes of 64 columns) and writes it with TMA bulk tensor
   // stores; per-thread 16-byte stores of 128 scattered rows were the GEMM's
   // bottleneck (profiles/r01_gemm_*).  BN = 256 (8-bit) keeps direct stores.
-  static constexpr bool kTmaStore = BN <= 128;
+  static constexpr bool kTmaStore = TS && BN <= 128;
   static constexpr int kStoreBytes = kTmaStore ? kBlockM * BN * 2 : 0;
   static constexpr int kStagesRaw = (224 * 1024 - kStoreBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
@@ -245,11 +245,11 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
 // operand traffic, not by the tensor pipe: profiles/r01_gemm_*).  A stage is
 // refilled only after both CTAs' MMAs released it (empty barriers count 2,
 // MMA commits multicast to the pair).
-template <int BN, int BC, int MAXPL, int MC>
+template <int BN, int BC, int MAXPL, int MC, bool TS>
 __global__ void __launch_bounds__(kThreads, 1)
     winograd_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                          const __grid_constant__ CUtensorMap tmM, GemmArgs args) {
-  using Cfg = GemmConfig<BN, BC, MAXPL>;
+  using Cfg = GemmConfig<BN, BC, MAXPL, TS>;
   using Tr = GemmTraits<BN, MAXPL>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -481,17 +481,17 @@ bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t 
 
 int g_num_sms = 0;
 
-template <int BN, int BC, int MAXPL, int MC>
+template <int BN, int BC, int MAXPL, int MC, bool TS>
 cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
                      cudaStream_t s) {
-  using Cfg = GemmConfig<BN, BC, MAXPL>;
+  using Cfg = GemmConfig<BN, BC, MAXPL, TS>;
   CUtensorMap tmV, tmU;
   if (!make_tmap(&tmV, V, a.Cp, a.P, (int64_t)n_planes * a.npos, BC, kBlockM)) return cudaErrorInvalidValue;
   if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_uplanes * a.npos, BC, BN)) return cudaErrorInvalidValue;
   CUtensorMap tmM;
   const int64_t mw_rows = (a.P + kBlockM - 1) / kBlockM * (int64_t)a.n_res * a.npos * kBlockM;
   if (!make_tmap_mw(&tmM, a.Mw, a.Kp, mw_rows)) return cudaErrorInvalidValue;
-  auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC>;
+  auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC, TS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
   if (g_num_sms == 0) {
@@ -521,14 +521,25 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   return cudaLaunchKernelEx(&cfg, kern, tmV, tmU, tmM, a);
 }
 
+template <int BN, int MAXPL, int MC, bool TS>
+cudaError_t run_gemm_bc_ts(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes,
+                           int n_uplanes, cudaStream_t s) {
+  switch (bc) {
+    case 32: return run_gemm<BN, 32, MAXPL, MC, TS>(a, V, U, n_planes, n_uplanes, s);
+    case 64: return run_gemm<BN, 64, MAXPL, MC, TS>(a, V, U, n_planes, n_uplanes, s);
+    default: return run_gemm<BN, 128, MAXPL, MC, TS>(a, V, U, n_planes, n_uplanes, s);
+  }
+}
+
+// Bulk-store epilogue unless the last tile block is mostly empty (small
+// batches): a bulk store writes all 128 rows of a block, the per-thread
+// epilogue only the live ones.
 template <int BN, int MAXPL, int MC = 1>
 cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
                         cudaStream_t s) {
-  switch (bc) {
-    case 32: return run_gemm<BN, 32, MAXPL, MC>(a, V, U, n_planes, n_uplanes, s);
-    case 64: return run_gemm<BN, 64, MAXPL, MC>(a, V, U, n_planes, n_uplanes, s);
-    default: return run_gemm<BN, 128, MAXPL, MC>(a, V, U, n_planes, n_uplanes, s);
-  }
+  const int64_t dead_rows = (int64_t)a.num_pb * kBlockM - a.P;
+  if (dead_rows * 8 <= a.P) return run_gemm_bc_ts<BN, MAXPL, MC, true>(a, bc, V, U, n_planes, n_uplanes, s);
+  return run_gemm_bc_ts<BN, MAXPL, MC, false>(a, bc, V, U, n_planes, n_uplanes, s);
 }
 
 }  // namespace
