@@ -178,6 +178,12 @@ RNSW_DEV void tma_store_2d(const void* desc, const void* src, int c0, int c1) {
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+RNSW_DEV void tma_store_3d(const void* desc, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 RNSW_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most N bulk groups still read their shared-memory source
 template <int N>

@@ -19,6 +19,9 @@
 // store.  16-bit moduli: BT is split into two s8 limbs (see below); every
 // exact int32 sum stays below 2^28 (m < 4500), so one division-free
 // reduction per output value suffices.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -42,14 +45,19 @@ RNSW_DEV uint32_t word_of(const uint4& v, int u) { return u == 0 ? v.x : u == 1 
 // kCompact (C <= 4, the small-channel path of smallc.cu): each warp owns one
 // tile and writes its 4 channels as symmetric int16 residues to
 // V16[res][P][pos][4] instead of the GEMM limb planes.
+// Non-compact output: the CTA's V rows of one residue are staged in shared
+// memory as OWT[plane][pos][64 channels] (64-byte rows, 16-byte chunks XOR
+// (pos >> 1) & 3 = TMA SWIZZLE_64B) and written by one TMA bulk tensor store
+// per plane (one 64-byte segment per position) instead of 16-byte stores
+// from four warps.  The finished 4-channel words leave registers after each
+// u, keeping the kernel at 4 CTAs per SM.
 template <int kPL, bool kCompact>
 __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                  const int8_t* __restrict__ x,
-                                                                 int8_t* __restrict__ V) {
+                                                                 int8_t* __restrict__ V,
+                                                                 const __grid_constant__ CUtensorMap tmVout) {
   __shared__ int32_t BT16[RNSW_MAX_RES * 256];
-  // per-warp output staging [slot][plane][u][lane] words: the finished 4-channel
-  // words leave registers after each u, keeping the kernel at 4 CTAs per SM
-  __shared__ uint32_t OW[4][8][2][4][32];
+  __shared__ __align__(1024) uint32_t OWT[2][256][16];
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = plan->n_res;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   const int ncb = (g.Cp + kCTAChannels - 1) / kCTAChannels;
@@ -61,11 +69,13 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
     BT16[idx] = (a < N && b < N) ? plan->res[r].bt[a * RNSW_MAX_N + b] : 0;
   }
   __syncthreads();
-  if (kCompact ? p >= g.P : c_base >= g.Cp) return;
+  if (kCompact && p >= g.P) return;
+  // non-compact: every warp stays for the CTA barriers of the bulk stores;
+  // warps past C compute nothing (their channel loop breaks at once) and
+  // stage zero rows; chunks past Cp are clipped by the store
   const int b_img = (int)(p / (g.th * g.tw));
   const int ti = (int)((p / g.tw) % g.th);
   const int tj = (int)(p % g.tw);
-  const int64_t plane_stride = (int64_t)npos * g.P * g.Cp;
 
   // ---- patch: raw[ni][e] = channels c_base..+15 of pixel (a = g + 8 ni, b = 4t + e)
   uint4 raw[2][4];
@@ -97,19 +107,6 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
       raw[ni][e] = v;
     }
 
-  if (!kCompact && c_base >= g.C) {
-    // all 16 channels of this warp are Cp padding: V = BT 0 BT^T = 0
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int e = s & 3, ni = s >> 2;
-      const int j = gq + 8 * (e >> 1), i = 8 * ni + 2 * tq + (e & 1);
-      if (i >= N || j >= N) continue;
-      for (int pl = 0; pl < plan->n_planes; ++pl)
-        *reinterpret_cast<uint4*>(V + ((int64_t)pl * npos + i * N + j) * g.P * g.Cp + p * g.Cp + c_base) =
-            make_uint4(0, 0, 0, 0);
-    }
-    return;
-  }
   for (int r = 0; r < nres; ++r) {
     const ResidueTables& tb = plan->res[r];
     const FastMod fm = fast_mod_of(tb);
@@ -151,7 +148,6 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
     }
 
     uint32_t outw[2][8];     // [plane][position slot] word of 4 channels (this u)
-    uint32_t (*ow)[2][4][32] = OW[warp];
     uint32_t outc[8][2];     // kCompact: [position slot][channel pair] int16 x 2
 #pragma unroll
     for (int s = 0; s < 8; ++s) outc[s][0] = outc[s][1] = 0u;
@@ -254,28 +250,37 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
         }
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
-          ow[s][0][u][lane] = outw[0][s];
-          if (planes == 2) ow[s][1][u][lane] = outw[1][s];
+          const int e = s & 3, ni = s >> 2;
+          const int j = gq + 8 * (e >> 1), i = 8 * ni + 2 * tq + (e & 1);
+          const int pos = i * N + j;
+          if (i >= N || j >= N) continue;
+          const int w = (((warp ^ (pos >> 1)) & 3) << 2) + u;  // 64B swizzle of chunk `warp`
+          OWT[0][pos][w] = outw[0][s];
+          if (planes == 2) OWT[1][pos][w] = outw[1][s];
         }
       }
     }
-    // (each lane only ever touches its own OW column: no synchronisation)
-    // slot s = 4 ni + e: row j = g + 8 (e >> 1), column i = 8 ni + 2t + (e & 1)
+    if constexpr (kCompact) {
+      // slot s = 4 ni + e: row j = g + 8 (e >> 1), column i = 8 ni + 2t + (e & 1)
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int e = s & 3, ni = s >> 2;
-      const int j = gq + 8 * (e >> 1), i = 8 * ni + 2 * tq + (e & 1);
-      if (i >= N || j >= N) continue;
-      const int pos = i * N + j;
-      if constexpr (kCompact) {
-        *reinterpret_cast<uint2*>(V + ((((int64_t)r * g.P + p) * npos + pos) << 3)) = make_uint2(outc[s][0], outc[s][1]);
-        continue;
+      for (int s = 0; s < 8; ++s) {
+        const int e = s & 3, ni = s >> 2;
+        const int j = gq + 8 * (e >> 1), i = 8 * ni + 2 * tq + (e & 1);
+        if (i >= N || j >= N) continue;
+        *reinterpret_cast<uint2*>(V + ((((int64_t)r * g.P + p) * npos + i * N + j) << 3)) =
+            make_uint2(outc[s][0], outc[s][1]);
       }
-      int8_t* dst = V + ((int64_t)tb.plane_base * npos + pos) * g.P * g.Cp + p * g.Cp + c_base;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(ow[s][0][0][lane], ow[s][0][1][lane], ow[s][0][2][lane], ow[s][0][3][lane]);
-      if (planes == 2)
-        *reinterpret_cast<uint4*>(dst + plane_stride) =
-            make_uint4(ow[s][1][0][lane], ow[s][1][1][lane], ow[s][1][2][lane], ow[s][1][3][lane]);
+    } else {
+      fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
+      __syncthreads();
+      if (tid == 0) {
+        for (int pl = 0; pl < planes; ++pl)
+          tma_store_3d(&tmVout, &OWT[pl][0][0], (int)(blockIdx.x % ncb) * kCTAChannels, (int)p,
+                       (tb.plane_base + pl) * npos);
+        bulk_commit();
+        bulk_wait_read<0>();  // OWT is rewritten by the next residue
+      }
+      __syncthreads();
     }
   }
 }
@@ -285,10 +290,23 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s) {
   dim3 grid((unsigned)(g.P * ((g.Cp + kCTAChannels - 1) / kCTAChannels)));
+  // V as [n_planes * npos][P][Cp] bytes; box = 64 channels x 1 tile x npos positions
+  const int npos = plan.dev.n * plan.dev.n;
+  auto encode = encode_fn();
+  if (encode == nullptr) return cudaErrorInvalidValue;
+  CUtensorMap tm;
+  cuuint64_t dims[3] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P, (cuuint64_t)plan.dev.n_planes * npos};
+  cuuint64_t strides[2] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P * g.Cp};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)npos};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, V, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
   if (plan.dev.res[0].planes == 2)
-    input_transform_tc_kernel<2, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+    input_transform_tc_kernel<2, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
   else
-    input_transform_tc_kernel<1, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+    input_transform_tc_kernel<1, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
   return cudaGetLastError();
 }
 
@@ -297,10 +315,11 @@ cudaError_t launch_input_transform_compact(const PlanHost& plan, const Geometry&
   if (g.C > 4) return cudaErrorInvalidValue;
   dim3 grid((unsigned)((g.P + 3) / 4));
   int8_t* V = reinterpret_cast<int8_t*>(V16);
+  CUtensorMap unused{};
   if (plan.dev.res[0].planes == 2)
-    input_transform_tc_kernel<2, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+    input_transform_tc_kernel<2, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, unused);
   else
-    input_transform_tc_kernel<1, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V);
+    input_transform_tc_kernel<1, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, unused);
   return cudaGetLastError();
 }
 
