@@ -104,7 +104,7 @@ constexpr int stage_bytes(int bn, int maxpl) {
   return maxpl * kBlockM * BC + (maxpl == 2 ? 4 : 1) * bn * BC;
 }
 
-template <int BN, int BC, int MAXPL, bool TS = true>
+template <int BN, int BC, int MAXPL, bool TS = true, int SB = 1>
 struct GemmConfig {
   static constexpr int kStageBytes = stage_bytes<BC>(BN, MAXPL);
   // BN <= 128: the epilogue stages each output tile in shared memory (int16,
@@ -112,7 +112,12 @@ struct GemmConfig {
   // stores; per-thread 16-byte stores of 128 scattered rows were the GEMM's
   // bottleneck (profiles/r01_gemm_*).  BN = 256 (8-bit) keeps direct stores.
   static constexpr bool kTmaStore = TS && BN <= 128;
-  static constexpr int kStoreBytes = kTmaStore ? kBlockM * BN * 2 : 0;
+  // SB staging tiles: with 2, tile i's bulk store drains while tile i+1 is
+  // staged (chosen when a work tile has few K chunks, so the operand stages
+  // it costs matter less)
+  static constexpr int kStoreTile = kBlockM * BN * 2;
+  static constexpr int kStoreBufs = SB;
+  static constexpr int kStoreBytes = kTmaStore ? kStoreBufs * kStoreTile : 0;
   static constexpr int kStagesRaw = (224 * 1024 - kStoreBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kAPlaneBytes = kBlockM * BC;
@@ -245,11 +250,11 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
 // operand traffic, not by the tensor pipe: profiles/r01_gemm_*).  A stage is
 // refilled only after both CTAs' MMAs released it (empty barriers count 2,
 // MMA commits multicast to the pair).
-template <int BN, int BC, int MAXPL, int MC, bool TS>
+template <int BN, int BC, int MAXPL, int MC, bool TS, int SB>
 __global__ void __launch_bounds__(kThreads, 1)
     winograd_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                          const __grid_constant__ CUtensorMap tmM, GemmArgs args) {
-  using Cfg = GemmConfig<BN, BC, MAXPL, TS>;
+  using Cfg = GemmConfig<BN, BC, MAXPL, TS, SB>;
   using Tr = GemmTraits<BN, MAXPL>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -406,10 +411,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool quad_live = (int64_t)pb * kBlockM + q * 32 < args.P;
       if (Cfg::kTmaStore) {
         // the previous tile's bulk store must have read the staging tile
-        if (warp == 4 && lane == 0) bulk_wait_read<0>();
+        // the store that last used this staging tile has read it
+        if (warp == 4 && lane == 0) {
+          if (Cfg::kStoreBufs == 2)
+            bulk_wait_read<1>();
+          else
+            bulk_wait_read<0>();
+        }
         named_bar_sync(1, 256);
       }
-      uint8_t* stg_t = Cfg::kTmaStore ? stg : nullptr;
+      uint8_t* stg_b = stg + (Cfg::kStoreBufs == 2 ? (it & 1) * Cfg::kStoreTile : 0);
+      uint8_t* stg_t = Cfg::kTmaStore ? stg_b : nullptr;
       if (!quad_live) {
         // every row of this warp's lane quadrant is past the last tile (small
         // or ragged P): nothing to reduce, just free the accumulator
@@ -427,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 4 && lane == 0) {
           const int row0 = (int)(((int64_t)pb * args.n_res * args.npos + res * args.npos + pos) * kBlockM);
 #pragma unroll
-          for (int bx = 0; bx < (BN + 63) / 64; ++bx) tma_store_2d(&tmM, stg + bx * (kBlockM * 128), kb * BN + 64 * bx, row0);
+          for (int bx = 0; bx < (BN + 63) / 64; ++bx) tma_store_2d(&tmM, stg_b + bx * (kBlockM * 128), kb * BN + 64 * bx, row0);
           bulk_commit();
         }
       }
@@ -481,17 +493,17 @@ bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t 
 
 int g_num_sms = 0;
 
-template <int BN, int BC, int MAXPL, int MC, bool TS>
+template <int BN, int BC, int MAXPL, int MC, bool TS, int SB>
 cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
                      cudaStream_t s) {
-  using Cfg = GemmConfig<BN, BC, MAXPL, TS>;
+  using Cfg = GemmConfig<BN, BC, MAXPL, TS, SB>;
   CUtensorMap tmV, tmU;
   if (!make_tmap(&tmV, V, a.Cp, a.P, (int64_t)n_planes * a.npos, BC, kBlockM)) return cudaErrorInvalidValue;
   if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_uplanes * a.npos, BC, BN)) return cudaErrorInvalidValue;
   CUtensorMap tmM;
   const int64_t mw_rows = (a.P + kBlockM - 1) / kBlockM * (int64_t)a.n_res * a.npos * kBlockM;
   if (!make_tmap_mw(&tmM, a.Mw, a.Kp, mw_rows)) return cudaErrorInvalidValue;
-  auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC, TS>;
+  auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC, TS, SB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
   if (g_num_sms == 0) {
@@ -524,10 +536,17 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
 template <int BN, int MAXPL, int MC, bool TS>
 cudaError_t run_gemm_bc_ts(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes,
                            int n_uplanes, cudaStream_t s) {
+  if (TS && a.nkc <= 2) {
+    switch (bc) {
+      case 32: return run_gemm<BN, 32, MAXPL, MC, TS, 2>(a, V, U, n_planes, n_uplanes, s);
+      case 64: return run_gemm<BN, 64, MAXPL, MC, TS, 2>(a, V, U, n_planes, n_uplanes, s);
+      default: return run_gemm<BN, 128, MAXPL, MC, TS, 2>(a, V, U, n_planes, n_uplanes, s);
+    }
+  }
   switch (bc) {
-    case 32: return run_gemm<BN, 32, MAXPL, MC, TS>(a, V, U, n_planes, n_uplanes, s);
-    case 64: return run_gemm<BN, 64, MAXPL, MC, TS>(a, V, U, n_planes, n_uplanes, s);
-    default: return run_gemm<BN, 128, MAXPL, MC, TS>(a, V, U, n_planes, n_uplanes, s);
+    case 32: return run_gemm<BN, 32, MAXPL, MC, TS, 1>(a, V, U, n_planes, n_uplanes, s);
+    case 64: return run_gemm<BN, 64, MAXPL, MC, TS, 1>(a, V, U, n_planes, n_uplanes, s);
+    default: return run_gemm<BN, 128, MAXPL, MC, TS, 1>(a, V, U, n_planes, n_uplanes, s);
   }
 }
 
