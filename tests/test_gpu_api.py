@@ -203,6 +203,30 @@ def test_small_channel_wraps_like_the_reference():
     assert np.array_equal(got, O.winograd_layer(x, wt, 1, 6, mods))
 
 
+GEMM_PATHS = [
+    # (batch, side, c, k, tile_m, moduli): P = batch * ceil(side/tile_m)^2 tiles
+    (3, 42, 64, 64, 14, (4001, 4331)),      # P = 27: one partial block, per-thread epilogue stores
+    (16, 42, 64, 64, 14, (4001, 4331)),     # P = 144: 2 blocks, mostly dead -> per-thread stores
+    (128, 28, 128, 256, 14, (4001, 4331)),  # P = 512: CTA pairs, 4 full blocks, bulk stores, num_kb = 2
+    (72, 28, 256, 128, 14, (4001, 4331)),   # P = 288: odd block count (3) -> phantom partner block
+    (64, 30, 32, 300, 10, (251, 241, 239)), # 8-bit: BN = 256 (per-thread stores), Kp = 304
+    (64, 30, 96, 100, 10, (251, 241, 239)), # 8-bit: BN = 128 with bulk stores, Cp = 128
+]
+
+
+@pytest.mark.parametrize("case", GEMM_PATHS, ids=lambda c: "b%d_s%d_c%d_k%d" % c[:4])
+def test_gemm_epilogue_and_pairing_paths(case):
+    """Each GEMM variant (per-thread vs bulk-store epilogue, CTA pairs with an
+    odd block count, 8-bit BN = 256) against the exact direct convolution."""
+    rnsw = _rnsw()
+    batch, side, c, k, tm, mods = case
+    spec = rnsw.LayerSpec(h=side, w=side, c=c, k=k, r=3, padding=1, batch=batch, tile_m=tm)
+    system = rnsw.RnsSystem(mods)
+    wt, x = _operands(spec, batch + c, -40, 40)
+    got = rnsw.winograd_layer_conv(spec, wt, x, system, declared_bound=system.signed_bound)
+    assert np.array_equal(got, oracle.direct_conv_c(x, wt, 1))
+
+
 DIRECT = [
     # b, h, w, c, k, r, pad, stride
     (1, 56, 56, 64, 64, 3, 1, 1),
