@@ -58,30 +58,34 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
   const int p_begin = blockIdx.z * tiles_per_cta, p_end = min(P, p_begin + tiles_per_cta);
   const uint2* src = reinterpret_cast<const uint2*>(V16) + ((int64_t)r * P + p_begin) * npos + pos;
   const int rp = r * npos + pos, nrp = nres * npos;
-  // two tiles of V16 in flight ahead of the one being reduced
-  uint2 wa = p_begin < p_end ? __ldg(src) : make_uint2(0, 0);
-  uint2 wb = p_begin + 1 < p_end ? __ldg(src + npos) : make_uint2(0, 0);
-  for (int p = p_begin; p < p_end; ++p, src += npos) {
-    uint4* dst = reinterpret_cast<uint4*>(Mw + mw_offset(p, rp, nrp, Kp)) + kg;
-    const uint2 w = wa;
-    wa = wb;
-    if (p + 2 < p_end) wb = __ldg(src + 2 * npos);
-    const int32_t v0 = (int32_t)(w.x << 16) >> 16, v1 = (int32_t)w.x >> 16;
-    const int32_t v2 = (int32_t)(w.y << 16) >> 16, v3 = (int32_t)w.y >> 16;
-    uint32_t o[4];
+  // V16 rows of 4 tiles are loaded together ahead of their products
+  for (int p0 = p_begin; p0 < p_end; p0 += 4) {
+    uint2 wv[4];
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      int32_t y[2];
+    for (int i = 0; i < 4; ++i)
+      wv[i] = p0 + i < p_end ? __ldg(src + (int64_t)(p0 - p_begin + i) * npos) : make_uint2(0, 0);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int kk = 2 * h + e;
-        // |sum| <= 4 h^2 < 2^28 for m < 4500
-        const int32_t n = bias + v0 * u[kk][0] + v1 * u[kk][1] + v2 * u[kk][2] + v3 * u[kk][3];
-        y[e] = kPL == 2 ? red_pos_biased(n, fm) : red_pos_biased(n, fm) - fm.h;
+    for (int i = 0; i < 4; ++i) {
+      const int p = p0 + i;
+      if (p >= p_end) break;
+      const uint2 w = wv[i];
+      const int32_t v0 = (int32_t)(w.x << 16) >> 16, v1 = (int32_t)w.x >> 16;
+      const int32_t v2 = (int32_t)(w.y << 16) >> 16, v3 = (int32_t)w.y >> 16;
+      uint32_t o[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        int32_t y[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kk = 2 * h + e;
+          // |sum| <= 4 h^2 < 2^28 for m < 4500
+          const int32_t n = bias + v0 * u[kk][0] + v1 * u[kk][1] + v2 * u[kk][2] + v3 * u[kk][3];
+          y[e] = kPL == 2 ? red_pos_biased(n, fm) : red_pos_biased(n, fm) - fm.h;
+        }
+        o[h] = __byte_perm((uint32_t)y[0], (uint32_t)y[1], 0x5410);
       }
-      o[h] = __byte_perm((uint32_t)y[0], (uint32_t)y[1], 0x5410);
+      *(reinterpret_cast<uint4*>(Mw + mw_offset(p, rp, nrp, Kp)) + kg) = make_uint4(o[0], o[1], o[2], o[3]);
     }
-    *dst = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
