@@ -145,7 +145,7 @@ def test_errors_are_raised_before_device_work():
         rnsw.winograd_layer_conv(s18, w18, x18, rnsw.RnsSystem((4001, 4331)), declared_bound=1000)
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(16))
 def test_random_geometry_sweep(seed):
     rnsw = _rnsw()
     rng = np.random.default_rng(100 + seed)
@@ -201,6 +201,32 @@ def test_small_channel_wraps_like_the_reference():
     wt, x = _operands(spec, 5)
     got = rnsw.winograd_layer_conv(spec, wt, x, system, declared_bound=10)
     assert np.array_equal(got, O.winograd_layer(x, wt, 1, 6, mods))
+
+
+K1_STORES = [
+    # (batch, side, c, k, r, tile_m, moduli, layout): the input transform's bulk
+    # stores for several channel blocks, short tiles (N < 16) and NCHW input
+    (2, 23, 200, 16, 3, 8, (251, 241, 239), "nhwc"),   # Cp = 256: 4 channel blocks, N = 10
+    (3, 19, 40, 24, 5, 6, (4001, 4331), "nchw"),       # Cp = 64 with C = 40, N = 10, NCHW
+    (1, 64, 32, 8, 3, 12, (4001, 4331), "nhwc"),       # Cp = 32 (box wider than the rows), N = 14
+]
+
+
+@pytest.mark.parametrize("case", K1_STORES, ids=lambda c: "c%d_n%d_%s" % (c[2], c[5] + c[4] - 1, c[7]))
+def test_input_transform_bulk_store_layouts(case):
+    rnsw = _rnsw()
+    batch, side, c, k, r, tm, mods, layout = case
+    spec = rnsw.LayerSpec(h=side, w=side, c=c, k=k, r=r, padding=r // 2, batch=batch, tile_m=tm)
+    system = rnsw.RnsSystem(mods)
+    wt, x = _operands(spec, side * c, -50, 50)
+    want = oracle.direct_conv_c(x, wt, r // 2)
+    if layout == "nhwc":
+        got = rnsw.winograd_layer_conv(spec, wt, x, system, declared_bound=system.signed_bound)
+    else:
+        got = np.asarray(rnsw.conv2d_rns(np.ascontiguousarray(x.transpose(0, 3, 1, 2)),
+                                         np.ascontiguousarray(wt.transpose(3, 2, 0, 1)), mods, tile_m=tm,
+                                         padding=r // 2, declared_bound=system.signed_bound)).transpose(0, 2, 3, 1)
+    assert np.array_equal(got, want)
 
 
 GEMM_PATHS = [
