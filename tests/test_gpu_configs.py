@@ -110,6 +110,23 @@ def test_vgg16_fused_glue_matches_unfused():
     assert sha(one) == digests()["vgg16/final"]["y"]
 
 
+def test_vgg16_batch256_matches_single_image_runs():
+    """The bench workload itself (config 4, B=256, fused, CUDA graph): sampled
+    images equal their own batch-1 runs, which are pinned to the reference
+    digests -- no cross-tile / cross-image interference at full scale."""
+    import torch
+    from paper_2007_12216_b200 import workloads as W
+    from paper_2007_12216_b200.vgg import VGG16Rns
+
+    net = VGG16Rns()
+    x = torch.from_numpy(W.vgg16_images(256)).cuda()
+    out = net.graph(x)(x).cpu()
+    for i in (0, 1, 127, 128, 255):
+        one = net.forward_fused(x[i:i + 1].contiguous()).cpu()
+        assert torch.equal(out[i:i + 1], one), i
+    assert sha(out[:1].numpy()) == digests()["vgg16/final"]["y"]
+
+
 def test_vgg16_streamed_serving_matches_forward():
     """VGG16Rns.run_stream (copies overlapped with compute, CUDA graphs bound
     to two input buffers) returns the same maps as forward_fused per batch."""
