@@ -147,10 +147,11 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   const int32_t kstride = g.layout == 0 ? 1 : g.Ho * g.Wo;
 
   // staging slots of this thread (see the staging loop)
-  const int st_kc = tid & 3, st_j = (tid >> 2) & 15, st_i0 = tid >> 6;
-  const bool st_j_in = st_j < N;
-  const bool st_ok = st_j_in && k0 + 8 * st_kc < g.Kp;
-  const int st_urows = (N - st_i0 + 1) >> 1;  // rows i0 + 2u < N
+  const int st_kc = tid & 3, st_jp = (tid >> 2) & 7, st_i0 = tid >> 5;
+  const int st_j = 2 * st_jp;
+  const bool st_c0 = st_j < N, st_c1 = st_j + 1 < N;  // the pair's columns inside the tile
+  const bool st_k = k0 + 8 * st_kc < g.Kp;
+  const int st_urows = (N - st_i0 + 3) >> 2;  // rows i0 + 4u < N
   // Mw rows (res, pos) of one tile are 128*Kp apart (blocked layout, kernels.h)
   const int row_stride = 128 * g.Kp;
   const int st_src = (st_i0 * N + st_j) * row_stride + k0 + 8 * st_kc;
@@ -158,30 +159,32 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
 
   for (int p = p_begin; p < p_end; ++p) {
     // stage: 16 B (8 channels) per load.  Thread t owns channel group
-    // kc = t & 3 and column j = (t >> 2) & 15 of rows i = (t >> 6) + 2u,
-    // u = 0..7, for every residue, so all addressing is per-thread constants
-    // plus compile-time offsets.  Loads go out in groups of 4 ahead of their
-    // transposing stores.
+    // kc = t & 3 and the column pair j = 2 ((t >> 2) & 7), j + 1 of rows
+    // i = (t >> 5) + 4u, u = 0..3, for every residue: the two columns' values
+    // of one channel are packed into one 32-bit transposing store (adjacent
+    // in the staged row; banks 8 kc + pair index are all distinct).
     const int16_t* src = Mw + mw_offset(p, 0, nres * npos, g.Kp) + st_src;
 #pragma unroll 1
     for (int r = 0; r < NRES; ++r) {
+      int4 v[4][2];
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        int4 v[4];
+      for (int u = 0; u < 4; ++u) {
+        const int16_t* row = src + (r * npos + 4 * u * N) * row_stride;
+        const bool rok = st_k && u < st_urows;
+        v[u][0] = (rok && st_c0) ? __ldg(reinterpret_cast<const int4*>(row)) : make_int4(0, 0, 0, 0);
+        v[u][1] = (rok && st_c1) ? __ldg(reinterpret_cast<const int4*>(row + row_stride)) : make_int4(0, 0, 0, 0);
+      }
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int u = 4 * half + w;
-          v[w] = make_int4(0, 0, 0, 0);
-          if (st_ok && u < st_urows) v[w] = __ldg(reinterpret_cast<const int4*>(src + (r * npos + 2 * u * N) * row_stride));
-        }
+      for (int u = 0; u < 4; ++u) {
+        if (!(st_c0 && u < st_urows)) continue;
+        const uint32_t* a = reinterpret_cast<const uint32_t*>(&v[u][0]);
+        const uint32_t* b = reinterpret_cast<const uint32_t*>(&v[u][1]);
+        // stage_off(i0 + 4u, j) = stage_off(i0, j) + 64 u + 2 u
+        uint32_t* dst = reinterpret_cast<uint32_t*>(st_dst + r * kKB * kRowS + 66 * u);
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int u = 4 * half + w;
-          if (!(st_j_in && u < st_urows)) continue;
-          const int16_t* e = reinterpret_cast<const int16_t*>(&v[w]);
-          int16_t* dst = st_dst + r * kKB * kRowS + 32 * u + 2 * (u >> 1);  // stage_off(i0 + 2u, j)
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dst[q * kRowS] = e[q];
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t wa = a[q >> 1], wb = b[q >> 1];
+          dst[q * (kRowS / 2)] = __byte_perm(wa, wb, (q & 1) ? 0x7632 : 0x5410);
         }
       }
     }
