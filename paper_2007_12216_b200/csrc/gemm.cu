@@ -10,8 +10,11 @@
 //   warp 1      MMA issuer:   tcgen05.mma.cta_group::1.kind::i8, s32 in TMEM
 //   warp 2      TMEM allocator
 //   warps 4-11  epilogue:     tcgen05.ld -> limb recombination -> mod m -> int16
+//                             -> swizzled smem staging -> TMA bulk tensor store
 // TMEM holds two accumulator sets so the epilogue of tile i overlaps the
-// MMAs of tile i+1.
+// MMAs of tile i+1.  16-bit plans with >= 2 tile blocks run as CTA pairs
+// (clusters of 2) that multicast the filter-bank planes (see the kernel).
+// Output: Mw in blocks of 128 tiles (kernels.h mw_offset).
 //
 // 16-bit moduli: V residues are two s8 planes v = 256*v_hi + v_lo; the
 // filter bank holds the limbs of u and of u' = 256*u mod m.  Then
