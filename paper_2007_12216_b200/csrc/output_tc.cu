@@ -56,7 +56,8 @@ struct Requant {
 // (sum - sum_{i<r} d_i*W[r][i]) mod m_r in one reduction.  Bound: the limb
 // sum stays below 1.8e8 and the digit terms below 2.1e7, inside the 2^28
 // window of red_pos_biased for m < 4500.
-// kMode: 0 int32 output, 1 fused requant (int8), 2 per-residue debug output
+// kMode: 0 int32 output, 1 fused requant (int8), 3 fused requant + 2x2 pool,
+// 2 per-residue debug output
 template <int NRES, int kPL, int kMode>
 __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                   const int16_t* __restrict__ Mw,
@@ -73,6 +74,8 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   int32_t* ATWP16 = ATP16 + nres * 256;  // 256 * ATW mod m (pass 2)
   uint8_t* O8 = reinterpret_cast<uint8_t*>(ATWP16 + nres * 256);    // [pixel][kKB] int8 (fused requant)
   constexpr bool kDigits = kMode != 2;  // pass 2 emits mixed-radix digits
+  constexpr bool kReq = kMode == 1 || kMode == 3;  // fused requantisation (int8 out)
+  constexpr bool kPool = kMode == 3;                // ... with the 2x2 max-pool
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   // grid (k-block, tile group): the k-blocks of one tile run side by side, so
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           }
           const bool neg = x > signed_bound;
           const int32_t v = (int32_t)(neg ? x - dyn_range : x);
-          if constexpr (kMode == 1) {
+          if constexpr (kReq) {
             qv[q] = neg ? 0 : min((int32_t)(x >> rq.shift), 127);  // relu, >> shift, clip
           } else if (out_off[q] >= 0 && kvalid) {
             // direct store: over this warp's 8 channels each pixel receives one
@@ -335,8 +338,8 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           }
         }
       }
-      if (kMode == 1) {
-        if (rq.pool) {
+      if (kReq) {
+        if (kPool) {
           // pairs along a (q, q^1) share a lane; pairs along b are lanes 4 apart
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
@@ -356,11 +359,11 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
         }
       }
     }
-    if (kMode == 1) {
+    if (kReq) {
       __syncthreads();
       // int8 NHWC rows of kKB channels (4-byte words)
-      const int side = rq.pool ? (M >> 1) : M;
-      const int Ho = rq.pool ? g.Ho / 2 : g.Ho, Wo = rq.pool ? g.Wo / 2 : g.Wo;
+      const int side = kPool ? (M >> 1) : M;
+      const int Ho = kPool ? g.Ho / 2 : g.Ho, Wo = kPool ? g.Wo / 2 : g.Wo;
       const int kw = min(kKB, g.K - k0);
       for (int idx = tid; idx < side * side * (kKB / 4); idx += blockDim.x) {
         const int wq = idx % (kKB / 4), pix = idx / (kKB / 4);
@@ -397,11 +400,12 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
     kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res, rq, tpc);
     return 0;
   };
-  const int mode = y_res != nullptr ? 2 : (out8 != nullptr ? 1 : 0);
+  const int mode = y_res != nullptr ? 2 : (out8 != nullptr ? (pool ? 3 : 1) : 0);
   const bool pl2 = plan.dev.res[0].planes == 2;
 #define RNSW_OT_MODES(NR, PL)                                             \
   (mode == 0 ? launch(output_transform_tc_kernel<NR, PL, 0>)              \
    : mode == 1 ? launch(output_transform_tc_kernel<NR, PL, 1>)            \
+   : mode == 3 ? launch(output_transform_tc_kernel<NR, PL, 3>)            \
                : launch(output_transform_tc_kernel<NR, PL, 2>))
   switch (plan.dev.n_res * (pl2 ? 10 : 1)) {
     case 10: RNSW_OT_MODES(1, 2); break;
