@@ -330,7 +330,9 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           const bool neg = x > signed_bound;
           const int32_t v = (int32_t)(neg ? x - dyn_range : x);
           if constexpr (kReq) {
-            qv[q] = neg ? 0 : min((int32_t)(x >> rq.shift), 127);  // relu, >> shift, clip
+            // relu, >> shift, clip; with the pool the (monotone) shift and clip
+            // are applied once per pooled value, after the max
+            qv[q] = neg ? 0 : (kPool ? (int32_t)x : min((int32_t)(x >> rq.shift), 127));
           } else if (out_off[q] >= 0 && kvalid) {
             // direct store: over this warp's 8 channels each pixel receives one
             // complete 32-byte sector (NHWC), merged in L2
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           for (int h = 0; h < 4; ++h) {
             int32_t m2 = max(qv[2 * h], qv[2 * h + 1]);
             m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 4));
+            m2 = min(m2 >> rq.shift, 127);
             const int a = 8 * (h >> 1) + 2 * tq;  // even row of the pair
             const int b = (h & 1) ? b_hi : b_lo;
             if ((gq & 1) == 0 && a < M && b < M) O8[((a >> 1) * (M >> 1) + (b >> 1)) * kKB + k] = (uint8_t)m2;
