@@ -51,7 +51,9 @@ RNSW_DEV uint32_t word_of(const uint4& v, int u) { return u == 0 ? v.x : u == 1 
 // per plane (one 64-byte segment per position) instead of 16-byte stores
 // from four warps.  The finished 4-channel words leave registers after each
 // u, keeping the kernel at 4 CTAs per SM.
-template <int kPL, bool kCompact>
+// kFull: NHWC with C % 64 == 0 -- 16-byte patch loads, every channel real
+// (no channel-loop exits, no masked limb flips), as a separate instance.
+template <int kPL, bool kCompact, bool kFull = false>
 __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                  const int8_t* __restrict__ x,
                                                                  int8_t* __restrict__ V,
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
 
   // ---- patch: raw[ni][e] = channels c_base..+15 of pixel (a = g + 8 ni, b = 4t + e)
   uint4 raw[2][4];
-  const bool vec = g.layout == 0 && (g.C & 15) == 0;
+  const bool vec = kFull || (g.layout == 0 && (g.C & 15) == 0);
 #pragma unroll
   for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
       // instruction cache (the fully unrolled body missed in L0/L1.5)
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
-        if (c_base + 4 * u + q >= g.C) break;  // padding channels stay 0
+        if (!kFull && c_base + 4 * u + q >= g.C) break;  // padding channels stay 0
         const uint32_t dq0 = q == 0 ? din[0][0] : q == 1 ? din[0][1] : q == 2 ? din[0][2] : din[0][3];
         const uint32_t dq1 = q == 0 ? din[1][0] : q == 1 ? din[1][1] : q == 2 ? din[1][2] : din[1][3];
         const uint32_t bsel = (0x3210u & ~(0xFu << (4 * q))) | (0x4u << (4 * q));  // insert at byte q
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
       if constexpr (!kCompact) {
         if (planes == 2) {
           // low limb = (w & 255) ^ 0x80, on the real channels only
-          const int nv = min(max(g.C - (c_base + 4 * u), 0), 4);
+          const int nv = kFull ? 4 : min(max(g.C - (c_base + 4 * u), 0), 4);
           const uint32_t flip = nv >= 4 ? 0x80808080u : (0x80808080u & ((1u << (8 * nv)) - 1u));
 #pragma unroll
           for (int s = 0; s < 8; ++s) outw[0][s] ^= flip;
@@ -303,10 +305,18 @@ cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, c
              CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  if (plan.dev.res[0].planes == 2)
-    input_transform_tc_kernel<2, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
-  else
-    input_transform_tc_kernel<1, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+  const bool full = g.layout == 0 && (g.C & 63) == 0;
+  if (plan.dev.res[0].planes == 2) {
+    if (full)
+      input_transform_tc_kernel<2, false, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+    else
+      input_transform_tc_kernel<2, false, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+  } else {
+    if (full)
+      input_transform_tc_kernel<1, false, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+    else
+      input_transform_tc_kernel<1, false, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+  }
   return cudaGetLastError();
 }
 
