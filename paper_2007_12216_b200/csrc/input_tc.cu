@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kCTAChannels = 64;
 
+
 // 4x4 byte transpose: in[e] = 4 channels of pixel e -> out[q] = channel q of pixels 0..3.
 RNSW_DEV void transpose4x4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&o)[4]) {
   const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w2, w3, 0x5140);
@@ -162,9 +163,11 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
                    din[1]);
 #pragma unroll
       for (int s = 0; s < 8; ++s) outw[0][s] = outw[1][s] = 0u;
-      // channels of this word: a rolled loop keeps the kernel inside the
-      // instruction cache (the fully unrolled body missed in L0/L1.5)
-#pragma unroll 1
+      // channels of this word: a rolled loop (unrolled by 2 in the full-channel
+      // instance, measured best) keeps the kernel inside the instruction
+      // cache -- the fully unrolled body missed in L0/L1.5
+      constexpr int kQUnroll = kFull ? 2 : 1;
+#pragma unroll kQUnroll
       for (int q = 0; q < 4; ++q) {
         if (!kFull && c_base + 4 * u + q >= g.C) break;  // padding channels stay 0
         const uint32_t dq0 = q == 0 ? din[0][0] : q == 1 ? din[0][1] : q == 2 ? din[0][2] : din[0][3];
