@@ -58,14 +58,16 @@ struct Requant {
 // window of red_pos_biased for m < 4500.
 // kMode: 0 int32 output, 1 fused requant (int8), 3 fused requant + 2x2 pool,
 // 2 per-residue debug output
-template <int NRES, int kPL, int kMode>
+// kF14: the F(14x14, 3x3) tile (N = 16, M = 14) as compile-time constants, so
+// the tile-shape index math and bounds checks fold away; 0: N, M from the plan.
+template <int NRES, int kPL, int kMode, bool kF14 = false>
 __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                   const int16_t* __restrict__ Mw,
                                                                   int32_t* __restrict__ y,
                                                                   int16_t* __restrict__ y_res, Requant rq,
                                                                   int tiles_per_cta) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int N = plan->n, M = plan->m_out, npos = N * N, nres = NRES;
+  const int N = kF14 ? 16 : plan->n, M = kF14 ? 14 : plan->m_out, npos = N * N, nres = NRES;
   int16_t* S = reinterpret_cast<int16_t*>(smem_raw);  // [nres][kKB][kRowS]
   const int s_bytes = (nres * kKB * kRowS * 2 + 15) & ~15;
   int32_t* AT16 = reinterpret_cast<int32_t*>(smem_raw + s_bytes);  // [nres][16][16], zero padded
@@ -405,6 +407,21 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
   };
   const int mode = y_res != nullptr ? 2 : (out8 != nullptr ? (pool ? 3 : 1) : 0);
   const bool pl2 = plan.dev.res[0].planes == 2;
+  if (plan.dev.n == 16 && plan.dev.m_out == 14 && mode != 2) {
+    // F(14x14, 3x3) (BASELINE configs 2, 4, 5): the specialised instances
+    if (pl2 && plan.dev.n_res == 2) {
+      mode == 0 ? launch(output_transform_tc_kernel<2, 2, 0, true>)
+      : mode == 1 ? launch(output_transform_tc_kernel<2, 2, 1, true>)
+                  : launch(output_transform_tc_kernel<2, 2, 3, true>);
+      return cudaGetLastError();
+    }
+    if (!pl2 && plan.dev.n_res == 3) {
+      mode == 0 ? launch(output_transform_tc_kernel<3, 1, 0, true>)
+      : mode == 1 ? launch(output_transform_tc_kernel<3, 1, 1, true>)
+                  : launch(output_transform_tc_kernel<3, 1, 3, true>);
+      return cudaGetLastError();
+    }
+  }
 #define RNSW_OT_MODES(NR, PL)                                             \
   (mode == 0 ? launch(output_transform_tc_kernel<NR, PL, 0>)              \
    : mode == 1 ? launch(output_transform_tc_kernel<NR, PL, 1>)            \
