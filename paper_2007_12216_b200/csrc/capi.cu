@@ -199,6 +199,26 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
     for (int i = 0; i < n_res; ++i) fast = fast && moduli[i] < 4500;  // keeps every limb recombination below 2^28
     d.fast = fast ? 1 : 0;
   }
+  {
+    // K4's unreduced pass 1 (output_tc.cu): the sum over j of AT'[a][j] hi +
+    // AT[a][j] lo, AT' = 256 AT mod m, hi in [-9, 8], lo in [0, 255], must fit
+    // three bytes as a signed value for every row a of every 16-bit residue
+    bool z3 = true;
+    for (int i = 0; i < n_res; ++i) {
+      const ResidueTables& t = d.res[i];
+      if (t.planes != 2) continue;
+      for (int a = 0; a < tile_m; ++a) {
+        int64_t bound = 0;
+        for (int j = 0; j < n; ++j) {
+          const int64_t v = t.at[a * RNSW_MAX_N + j];
+          const int64_t vp = sym(v * 256, t.modulus);
+          bound += 9 * (vp < 0 ? -vp : vp) + 255 * (v < 0 ? -v : v);
+        }
+        z3 = z3 && bound < (1 << 23);
+      }
+    }
+    d.z3 = z3 ? 1 : 0;
+  }
   d.signed_bound = (d.dynamic_range - 1) / 2;
   for (int j = 0; j < n_res; ++j)
     for (int i = 0; i < j; ++i) {

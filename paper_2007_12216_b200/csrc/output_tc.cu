@@ -60,8 +60,15 @@ struct Requant {
 // 2 per-residue debug output
 // kF14: the F(14x14, 3x3) tile (N = 16, M = 14) as compile-time constants, so
 // the tile-shape index math and bounds checks fold away; 0: N, M from the plan.
-template <int NRES, int kPL, int kMode, bool kF14 = false>
-__global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
+// kZ3 (16-bit moduli, plan->z3): pass 1 is not reduced; its exact sum z fits
+// 24-bit signed, and pass 2 takes z as three byte limbs (u8, u8, s8) against
+// AT^T, 256 AT^T and 65536 AT^T mod m: 8 reductions fewer per channel and
+// residue for two more MMAs.
+#ifndef RNSW_K4_MINB
+#define RNSW_K4_MINB 4
+#endif
+template <int NRES, int kPL, int kMode, bool kF14 = false, bool kZ3 = false>
+__global__ void __launch_bounds__(128, RNSW_K4_MINB) output_transform_tc_kernel(const PlanDevice* __restrict__ plan, Geometry g,
                                                                   const int16_t* __restrict__ Mw,
                                                                   int32_t* __restrict__ y,
                                                                   int16_t* __restrict__ y_res, Requant rq,
@@ -112,6 +119,7 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
   // 16-bit moduli: limbs of X' = 256 X mod m, so a product with a two-limb
   // operand needs two accumulators (256 * hi-part + lo-part) instead of three
   uint32_t A1plo[NRES][2], A1phi[NRES][2], B2plo[NRES][2], B2phi[NRES][2];
+  uint32_t B2qlo[kZ3 ? NRES : 1][2], B2qhi[kZ3 ? NRES : 1][2];  // 65536 ATW mod m (kZ3)
   int32_t mw[NRES][NRES];
 #pragma unroll
   for (int r = 0; r < NRES; ++r) {
@@ -143,6 +151,13 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
         const int32_t q2 = atwp[row * 16 + 8 + 2 * tq], q3 = atwp[row * 16 + 9 + 2 * tq];
         B2plo[r][h] = pack4_lo(q0, q1, q2, q3);
         B2phi[r][h] = pack4_lo(limb_hi(q0), limb_hi(q1), limb_hi(q2), limb_hi(q3));
+        if constexpr (kZ3) {
+          const FastMod f = fmr[r];
+          const int32_t w0 = red_fast(q0 * 256, f), w1 = red_fast(q1 * 256, f);
+          const int32_t w2 = red_fast(q2 * 256, f), w3 = red_fast(q3 * 256, f);
+          B2qlo[r][h] = pack4_lo(w0, w1, w2, w3);
+          B2qhi[r][h] = pack4_lo(limb_hi(w0), limb_hi(w1), limb_hi(w2), limb_hi(w3));
+        }
       }
     }
   }
@@ -236,14 +251,15 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
             const uint32_t blo = __byte_perm(w0, w1, 0x6420);  // u8 low bytes
             const uint32_t bhi = __byte_perm(w0, w1, 0x7531);  // s8 high bytes
             // Mat = 256 hi + lo: AT Mat = AT' hi + AT lo (mod m)
-            const int32_t bias = pos_bias(fm);
+            const int32_t bias = kZ3 ? 0 : pos_bias(fm);
             int32_t a256[4] = {0, 0, 0, 0}, a1[4] = {bias, bias, bias, bias};
             imma_ss(a256, A1phi[r][0], A1phi[r][1], bhi);
             imma_su(a256, A1hi[r][0], A1hi[r][1], blo);
             imma_ss(a1, A1plo[r][0], A1plo[r][1], bhi);
             imma_su(a1, A1lo[r][0], A1lo[r][1], blo);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) z[ni][e] = red_pos_biased(a256[e] * 256 + a1[e], fm);
+            for (int e = 0; e < 4; ++e)
+              z[ni][e] = kZ3 ? a256[e] * 256 + a1[e] : red_pos_biased(a256[e] * 256 + a1[e], fm);
           }
         } else {
 #pragma unroll
@@ -260,7 +276,35 @@ __global__ void __launch_bounds__(128, 4) output_transform_tc_kernel(const PlanD
           }
         }
         // pass 2: A = Z^T (rows b = g / g+8; k-slots <- columns i of pass 1)
-        if (kPL == 2) {
+        if (kPL == 2 && kZ3) {
+          // z in [-2^23, 2^23): bytes 0, 1 (u8) and 2 (s8) of each value
+          const uint32_t p0 = __byte_perm(z[0][0], z[0][1], 0x5140), q0 = __byte_perm(z[1][0], z[1][1], 0x5140);
+          const uint32_t p1 = __byte_perm(z[0][2], z[0][3], 0x5140), q1 = __byte_perm(z[1][2], z[1][3], 0x5140);
+          const uint32_t zb00 = __byte_perm(p0, q0, 0x5410), zb10 = __byte_perm(p0, q0, 0x7632);
+          const uint32_t zb01 = __byte_perm(p1, q1, 0x5410), zb11 = __byte_perm(p1, q1, 0x7632);
+          const uint32_t zb20 = __byte_perm(__byte_perm(z[0][0], z[0][1], 0x0062), __byte_perm(z[1][0], z[1][1], 0x0062), 0x5410);
+          const uint32_t zb21 = __byte_perm(__byte_perm(z[0][2], z[0][3], 0x0062), __byte_perm(z[1][2], z[1][3], 0x0062), 0x5410);
+          const int32_t bias = pos_bias(fm);
+#pragma unroll
+          for (int na = 0; na < 2; ++na) {
+            int32_t a256[4] = {0, 0, 0, 0}, a1[4] = {bias, bias, bias, bias};
+            imma_ss(a256, zb20, zb21, B2qhi[r][na]);
+            imma_us(a256, zb10, zb11, B2phi[r][na]);
+            imma_us(a256, zb00, zb01, B2hi[r][na]);
+            imma_ss(a1, zb20, zb21, B2qlo[r][na]);
+            imma_us(a1, zb10, zb11, B2plo[r][na]);
+            imma_us(a1, zb00, zb01, B2lo[r][na]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              int32_t n = a256[e] * 256 + a1[e];
+              if constexpr (kDigits) {
+#pragma unroll
+                for (int i2 = 0; i2 < r; ++i2) n -= yv[i2][4 * na + e] * mw[r][i2];
+              }
+              yv[r][4 * na + e] = red_pos_biased(n, fm);
+            }
+          }
+        } else if (kPL == 2) {
           // z in [0, m): u8 low byte, high part z >> 8 in [0, 23]
           const uint32_t zlo0 = pack4_lo(z[0][0], z[0][1], z[1][0], z[1][1]);
           const uint32_t zlo1 = pack4_lo(z[0][2], z[0][3], z[1][2], z[1][3]);
@@ -409,6 +453,13 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
   const bool pl2 = plan.dev.res[0].planes == 2;
   if (plan.dev.n == 16 && plan.dev.m_out == 14 && mode != 2) {
     // F(14x14, 3x3) (BASELINE configs 2, 4, 5): the specialised instances
+    static const bool no_z3 = getenv("RNSW_K4_NO_Z3") != nullptr;  // A/B switch (tests cover both paths)
+    if (pl2 && plan.dev.n_res == 2 && plan.dev.z3 && !no_z3) {
+      mode == 0 ? launch(output_transform_tc_kernel<2, 2, 0, true, true>)
+      : mode == 1 ? launch(output_transform_tc_kernel<2, 2, 1, true, true>)
+                  : launch(output_transform_tc_kernel<2, 2, 3, true, true>);
+      return cudaGetLastError();
+    }
     if (pl2 && plan.dev.n_res == 2) {
       mode == 0 ? launch(output_transform_tc_kernel<2, 2, 0, true>)
       : mode == 1 ? launch(output_transform_tc_kernel<2, 2, 1, true>)

@@ -39,6 +39,7 @@ struct PlanDevice {
   int32_t n_planes;  // total limb planes over all residues (V)
   int32_t n_uplanes; // total filter-bank planes over all residues (U)
   int32_t fast;      // 1: tensor-core transform kernels apply (all m < 4500, D < 2^31)
+  int32_t z3;        // 1: K4 pass-1 sums of every 16-bit residue fit 24-bit signed (three-limb pass 2)
   int64_t dynamic_range;
   int64_t signed_bound;
   int64_t mrc_inv[RNSW_MAX_RES][RNSW_MAX_RES];  // m_i^-1 mod m_j, i < j

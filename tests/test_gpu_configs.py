@@ -171,3 +171,22 @@ def test_fused_requant_single_layers():
                                                   vp(ws.data_ptr()), ws_bytes, _stream_ptr()))
         want = requant_pool(oracle.direct_conv_c(x, w, 1), shift, bool(pool))
         assert np.array_equal(out.cpu().numpy(), want), (h, c, k, tm, pool)
+
+
+@pytest.mark.skipif(__import__("os").environ.get("RNSW_K4_NO_Z3") is not None, reason="already the alternate path")
+def test_alternate_kernel_paths_in_subprocess():
+    """The A/B switches read once per process (RNSW_K4_NO_Z3: K4 with a
+    reduced pass 1 instead of the three-limb pass 2; RNSW_GEMM_NO_MC: GEMM
+    without CTA pairs) select kernels the default dispatch does not use for
+    the VGG16 shapes: rerun the VGG16 and fused-epilogue checks on them."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, RNSW_K4_NO_Z3="1", RNSW_GEMM_NO_MC="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_configs.py"),
+                        "-k", "vgg16_batch1 or fused_glue or fused_requant or config5_sweep"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
