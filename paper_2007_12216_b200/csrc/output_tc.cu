@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(128, RNSW_K4_MINB) output_transform_tc_kernel(
                                                                   const int16_t* __restrict__ Mw,
                                                                   int32_t* __restrict__ y,
                                                                   int16_t* __restrict__ y_res, Requant rq,
-                                                                  int tiles_per_cta) {
+                                                                  int tiles_per_cta, FastDiv div_img, FastDiv div_tw) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int N = kF14 ? 16 : plan->n, M = kF14 ? 14 : plan->m_out, npos = N * N, nres = NRES;
   int16_t* S = reinterpret_cast<int16_t*>(smem_raw);  // [nres][kKB][kRowS]
@@ -210,9 +210,10 @@ __global__ void __launch_bounds__(128, RNSW_K4_MINB) output_transform_tc_kernel(
     }
     __syncthreads();
 
-    const int b_img = p / (g.th * g.tw);
-    const int ti = (p / g.tw) % g.th;
-    const int tj = p % g.tw;
+    const int b_img = (int)fdiv((uint32_t)p, div_img);  // p = (b_img * th + ti) * tw + tj
+    const int rem = p - b_img * (int)div_img.d;
+    const int ti = (int)fdiv((uint32_t)rem, div_tw);
+    const int tj = rem - ti * g.tw;
     // Output addressing is fixed per lane: slot q -> pixel (a, b).  32-bit
     // offsets from the tile origin (channel k0); -1 marks pixels outside the
     // output plane.
@@ -444,9 +445,11 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
   const int64_t units = g.P * kblocks;
   const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(RNSW_K4_TPC_MAX, units / (148 * 4 * RNSW_K4_WAVES)));
   dim3 grid(kblocks, (unsigned)((g.P + tpc - 1) / tpc));
+  if (g.P >= (1ll << 31)) return cudaErrorInvalidValue;  // FastDiv range
+  const FastDiv div_img = make_fastdiv((uint32_t)(g.th * g.tw)), div_tw = make_fastdiv((uint32_t)g.tw);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res, rq, tpc);
+    kern<<<grid, 128, smem, s>>>(plan.d_plan, g, Mw, y, y_res, rq, tpc, div_img, div_tw);
     return 0;
   };
   const int mode = y_res != nullptr ? 2 : (out8 != nullptr ? (pool ? 3 : 1) : 0);
