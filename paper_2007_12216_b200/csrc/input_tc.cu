@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
         if (!kFull && c_base + 4 * u + q >= g.C) break;  // padding channels stay 0
         const uint32_t dq0 = q == 0 ? din[0][0] : q == 1 ? din[0][1] : q == 2 ? din[0][2] : din[0][3];
         const uint32_t dq1 = q == 0 ? din[1][0] : q == 1 ? din[1][1] : q == 2 ? din[1][2] : din[1][3];
-        const uint32_t bsel = (0x3210u & ~(0xFu << (4 * q))) | (0x4u << (4 * q));  // insert at byte q
+        const uint32_t bsel = (0x3210u & ~(0xFu << (4 * q))) | (0x4u << (4 * q));  // insert byte 0 at byte q
+        const uint32_t bsel1 = (0x3210u & ~(0xFu << (4 * q))) | (0x5u << (4 * q)); // insert byte 1 at byte q
         int32_t v[2][4];
         if (planes == 2) {
           // pass 1: T exact, as byte limbs (see the header)
@@ -186,10 +187,11 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
             for (int e = 0; e < 4; ++e) t[ni][e] = hi[e] * 256 + lo[e];
           }
           // pass 2: A rows j = g / g+8, k-slots = {2t, 2t+1, 8+2t, 9+2t}
-          const uint32_t t0a = pack4_byte<0>(t[0][0], t[0][1], t[1][0], t[1][1]);
-          const uint32_t t0b = pack4_byte<0>(t[0][2], t[0][3], t[1][2], t[1][3]);
-          const uint32_t t1a = pack4_byte<1>(t[0][0], t[0][1], t[1][0], t[1][1]);
-          const uint32_t t1b = pack4_byte<1>(t[0][2], t[0][3], t[1][2], t[1][3]);
+          // bytes 0 and 1 share their first byte-pairing step
+          const uint32_t pa = __byte_perm(t[0][0], t[0][1], 0x5140), qa = __byte_perm(t[1][0], t[1][1], 0x5140);
+          const uint32_t pb = __byte_perm(t[0][2], t[0][3], 0x5140), qb = __byte_perm(t[1][2], t[1][3], 0x5140);
+          const uint32_t t0a = __byte_perm(pa, qa, 0x5410), t1a = __byte_perm(pa, qa, 0x7632);
+          const uint32_t t0b = __byte_perm(pb, qb, 0x5410), t1b = __byte_perm(pb, qb, 0x7632);
           const uint32_t t2a = pack4_byte<2>(t[0][0], t[0][1], t[1][0], t[1][1]);
           const uint32_t t2b = pack4_byte<2>(t[0][2], t[0][3], t[1][2], t[1][3]);
           // kCompact wants v itself, the limb planes w = v + 128
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
           for (int s = 0; s < 8; ++s) {
             const int32_t val = v[s >> 2][s & 3];  // 16-bit: w = v + 128
             outw[0][s] = __byte_perm(outw[0][s], (uint32_t)val, bsel);
-            if (planes == 2) outw[1][s] = __byte_perm(outw[1][s], (uint32_t)(val >> 8), bsel);
+            if (planes == 2) outw[1][s] = __byte_perm(outw[1][s], (uint32_t)val, bsel1);  // byte 1 = w >> 8
           }
         }
       }
