@@ -177,6 +177,18 @@ __global__ void __launch_bounds__(128, RNSW_K4_MINB) output_transform_tc_kernel(
   const int st_src = (st_i0 * N + st_j) * row_stride + k0 + 8 * st_kc;
   int16_t* st_dst = S + 8 * st_kc * kRowS + stage_off(st_i0, st_j);
 
+  // fused requant + pool: this lane's O8 slots, fixed for the whole kernel.
+  // Pooled pair h (rows a = 8 (h >> 1) + 2t, a + 1; columns b = g + 8 (h & 1)
+  // and b + 1 on lane g + 1) goes to pixel (a / 2, b / 2), written by the
+  // even-g lanes; bit h of o8_mask marks the pairs inside the tile.
+  const int o8_base = (tq * (M >> 1) + (gq >> 1)) * kKB;
+  uint32_t o8_mask = 0;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const int a = 8 * (h >> 1) + 2 * tq, b = gq + 8 * (h & 1);
+    if ((gq & 1) == 0 && a < M && b < M) o8_mask |= 1u << h;
+  }
+
   for (int p = p_begin; p < p_end; ++p) {
     // stage: 16 B (8 channels) per load.  Thread t owns channel group
     // kc = t & 3 and the column pair j = 2 ((t >> 2) & 7), j + 1 of rows
@@ -395,9 +407,8 @@ __global__ void __launch_bounds__(128, RNSW_K4_MINB) output_transform_tc_kernel(
             int32_t m2 = max(qv[2 * h], qv[2 * h + 1]);
             m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 4));
             m2 = min(m2 >> rq.shift, 127);
-            const int a = 8 * (h >> 1) + 2 * tq;  // even row of the pair
-            const int b = (h & 1) ? b_hi : b_lo;
-            if ((gq & 1) == 0 && a < M && b < M) O8[((a >> 1) * (M >> 1) + (b >> 1)) * kKB + k] = (uint8_t)m2;
+            // pair h: rows a = 8 (h >> 1) + 2t, columns b = g + 8 (h & 1)
+            if (o8_mask & (1u << h)) O8[o8_base + (4 * (h >> 1) * (M >> 1) + 4 * (h & 1)) * kKB + k] = (uint8_t)m2;
           }
         } else {
 #pragma unroll
