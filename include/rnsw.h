@@ -137,6 +137,24 @@ int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int
 int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, int H, int W, int K, int pad,
                                   int shift, int pool, int8_t* out, void* stream);
 
+/* Mw8 stage variants (the layout the whole-layer path uses when
+ * rnsw_mw8_supported(plan) is 1: F(14x14,3x3) over two 16-bit residues,
+ * output transform on tcgen05).  Mw8 holds the same Winograd-domain product
+ * as Mw, as y mod m in [0, m) split into low/high byte planes:
+ * [ceil(P/128)][n_res][2][N*N][128][Kp] uint8 (rnsw_m_bytes bytes).  The
+ * stage calls mirror rnsw_small_channel_product / rnsw_winograd_gemm /
+ * rnsw_output_transform / rnsw_output_transform_requant; chaining them gives
+ * exactly rnsw_conv_forward(_requant).  RNSW_ERR_UNSUPPORTED for other plans. */
+int rnsw_mw8_supported(const rnsw_plan* plan);
+int rnsw_small_channel_product_mw8(const rnsw_plan* plan, const void* V16, const void* U, int64_t P, int C,
+                                   int K, void* Mw8, size_t Mw8_bytes, void* stream);
+int rnsw_winograd_gemm_mw8(const rnsw_plan* plan, const void* V, const void* U, int64_t P, int C, int K,
+                           void* Mw8, size_t Mw8_bytes, void* stream);
+int rnsw_output_transform_mw8(const rnsw_plan* plan, const void* Mw8, int B, int H, int W, int K, int pad,
+                              int layout, int32_t* y, void* stream);
+int rnsw_output_transform_requant_mw8(const rnsw_plan* plan, const void* Mw8, int B, int H, int W, int K,
+                                      int pad, int shift, int pool, int8_t* out, void* stream);
+
 /* Vectorised MRC of n_res residue arrays ([n_res][count] int16, any congruent
  * representatives) into signed int64. */
 int rnsw_mrc_reconstruct(const rnsw_plan* plan, const int16_t* residues, int64_t count,

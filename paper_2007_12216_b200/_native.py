@@ -52,6 +52,15 @@ _SIGNATURES = {
                                           c_int, c_int, c_void_p, c_void_p, c_size_t, c_void_p]),
     "rnsw_output_transform_requant": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                               c_void_p, c_void_p]),
+    "rnsw_mw8_supported": (c_int, [c_void_p]),
+    "rnsw_small_channel_product_mw8": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p,
+                                               c_size_t, c_void_p]),
+    "rnsw_winograd_gemm_mw8": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_size_t,
+                                       c_void_p]),
+    "rnsw_output_transform_mw8": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                          c_void_p]),
+    "rnsw_output_transform_requant_mw8": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                                                  c_int, c_void_p, c_void_p]),
     "rnsw_direct_weight_bytes": (c_size_t, [c_int, c_int, c_int]),
     "rnsw_direct_pack_weights": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
     "rnsw_direct_conv": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_int, c_int, c_int,

@@ -200,19 +200,21 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
     d.fast = fast ? 1 : 0;
   }
   {
-    // K4's unreduced pass 1 (output_tc.cu): the sum over j of AT'[a][j] hi +
-    // AT[a][j] lo, AT' = 256 AT mod m, hi in [-9, 8], lo in [0, 255], must fit
+    // K4's unreduced pass 1 (output_tc.cu, output_umma.cu): the sum over j of
+    // AT'[a][j] hi + AT[a][j] lo, AT' = 256 AT mod m, with hi, lo the bytes of
+    // y mod m in [0, m) (hi <= (m-1) >> 8, lo <= 255), must fit
     // three bytes as a signed value for every row a of every 16-bit residue
     bool z3 = true;
     for (int i = 0; i < n_res; ++i) {
       const ResidueTables& t = d.res[i];
       if (t.planes != 2) continue;
+      const int64_t hi_max = (t.modulus - 1) >> 8;  // high byte of y mod m in [0, m)
       for (int a = 0; a < tile_m; ++a) {
         int64_t bound = 0;
         for (int j = 0; j < n; ++j) {
           const int64_t v = t.at[a * RNSW_MAX_N + j];
           const int64_t vp = sym(v * 256, t.modulus);
-          bound += 9 * (vp < 0 ? -vp : vp) + 255 * (v < 0 ? -v : v);
+          bound += hi_max * (vp < 0 ? -vp : vp) + 255 * (v < 0 ? -v : v);
         }
         z3 = z3 && bound < (1 << 23);
       }
@@ -399,20 +401,21 @@ int rnsw_output_residues(const rnsw_plan* plan, const void* Mw, int64_t P, int K
 namespace {
 // K1 + K3 of a whole-layer call: the tensor-core GEMM path, or for C <= 4
 // the compact transform + CUDA-core product (smallc.cu), into Mw.
+// planar: leave Mw8 (the byte planes the tcgen05 output transform reads).
 int transform_and_product(const rnsw_plan* plan, const rnsw::Geometry& g, const int8_t* x, const void* U, int8_t* V,
-                          int16_t* Mw, cudaStream_t s) {
+                          int16_t* Mw, cudaStream_t s, bool planar = false) {
   cudaError_t e;
   if (rnsw::smallc_ok(plan->host.dev, g) && !rnsw::force_generic()) {
     int16_t* V16 = reinterpret_cast<int16_t*>(V);
     e = rnsw::launch_input_transform_compact(plan->host, g, x, V16, s);
     if (e != cudaSuccess) return cuda_fail(e, "input_transform_compact");
-    e = rnsw::launch_smallc_product(plan->host, g, V16, static_cast<const int8_t*>(U), Mw, s);
+    e = rnsw::launch_smallc_product(plan->host, g, V16, static_cast<const int8_t*>(U), Mw, s, planar);
     return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "smallc_product");
   }
   e = rnsw::launch_input_transform(plan->host, g, x, V, s);
   if (e != cudaSuccess) return cuda_fail(e, "input_transform");
   e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, g.K, g.Kp, g.bc, Mw, s,
-                                 rnsw::tc_output_ok(plan->host.dev) && !rnsw::force_generic());
+                                 rnsw::tc_output_ok(plan->host.dev) && !rnsw::force_generic(), planar);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "winograd_gemm");
 }
 }  // namespace
@@ -431,6 +434,11 @@ int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int 
   int8_t* V = static_cast<int8_t*>(workspace);
   int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
   cudaStream_t s = (cudaStream_t)stream;
+  if (rnsw::umma_output_ok(d)) {
+    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true)) return rc;
+    cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), y, s);
+    return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_umma");
+  }
   if (int rc = transform_and_product(plan, g, x, U, V, Mw, s)) return rc;
   cudaError_t e = rnsw::launch_output_transform(plan->host, g, Mw, y, nullptr, s);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform");
@@ -457,6 +465,12 @@ int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int
   int8_t* V = static_cast<int8_t*>(workspace);
   int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
   cudaStream_t s = (cudaStream_t)stream;
+  if (rnsw::umma_output_ok(d)) {
+    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true)) return rc;
+    cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), nullptr, s,
+                                                       out, shift, pool);
+    return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant_umma");
+  }
   if (int rc = transform_and_product(plan, g, x, U, V, Mw, s)) return rc;
   cudaError_t e = rnsw::launch_output_transform_tc(plan->host, g, Mw, nullptr, nullptr, s, out, shift, pool);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant");
@@ -473,6 +487,75 @@ int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, 
   cudaError_t e = rnsw::launch_output_transform_tc(plan->host, g, static_cast<const int16_t*>(Mw), nullptr, nullptr,
                                                    (cudaStream_t)stream, out, shift, pool);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant");
+}
+
+int rnsw_mw8_supported(const rnsw_plan* plan) {
+  if (check_plan(plan)) return 0;
+  return rnsw::umma_output_ok(plan->host.dev) ? 1 : 0;
+}
+
+int rnsw_small_channel_product_mw8(const rnsw_plan* plan, const void* V16, const void* U, int64_t P, int C, int K,
+                                   void* Mw8, size_t Mw8_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (!rnsw::umma_output_ok(plan->host.dev)) return fail(RNSW_ERR_UNSUPPORTED, "plan does not use the Mw8 layout");
+  if (V16 == nullptr || U == nullptr || Mw8 == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (P < 1 || P > 2147483647LL || C < 1 || K < 1) return fail(RNSW_ERR_SHAPE, "bad product shape P=%lld C=%d K=%d",
+                                                          (long long)P, C, K);
+  rnsw::Geometry g{};
+  g.P = P;
+  g.C = C;
+  g.K = K;
+  g.Cp = padded_channels(C);
+  g.Kp = (int)round_up(K, 16);
+  if (!rnsw::smallc_ok(plan->host.dev, g))
+    return fail(RNSW_ERR_UNSUPPORTED, "small-channel product needs C <= 4 (C=%d)", C);
+  if (Mw8_bytes < m_bytes(plan->host.dev, P, g.Kp)) return fail(RNSW_ERR_WORKSPACE, "Mw8 buffer too small");
+  cudaError_t e = rnsw::launch_smallc_product(plan->host, g, static_cast<const int16_t*>(V16),
+                                              static_cast<const int8_t*>(U), static_cast<int16_t*>(Mw8),
+                                              (cudaStream_t)stream, true);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "small_channel_product_mw8");
+}
+
+int rnsw_winograd_gemm_mw8(const rnsw_plan* plan, const void* V, const void* U, int64_t P, int C, int K, void* Mw8,
+                           size_t Mw8_bytes, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (!rnsw::umma_output_ok(plan->host.dev)) return fail(RNSW_ERR_UNSUPPORTED, "plan does not use the Mw8 layout");
+  if (V == nullptr || U == nullptr || Mw8 == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (P < 1 || C < 1 || K < 1) return fail(RNSW_ERR_SHAPE, "bad GEMM shape P=%lld C=%d K=%d", (long long)P, C, K);
+  if ((int64_t)C * 128 * 128 > 2147483647LL) return fail(RNSW_ERR_OVERFLOW, "C=%d can overflow int32", C);
+  const int Cp = padded_channels(C), Kp = (int)round_up(K, 16);
+  if (Mw8_bytes < m_bytes(plan->host.dev, P, Kp)) return fail(RNSW_ERR_WORKSPACE, "Mw8 buffer too small");
+  cudaError_t e = rnsw::launch_winograd_gemm(plan->host, static_cast<const int8_t*>(V), static_cast<const int8_t*>(U),
+                                             P, Cp, K, Kp, Cp < 128 ? Cp : 128, static_cast<int16_t*>(Mw8),
+                                             (cudaStream_t)stream, true, true);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "winograd_gemm_mw8");
+}
+
+int rnsw_output_transform_mw8(const rnsw_plan* plan, const void* Mw8, int B, int H, int W, int K, int pad, int layout,
+                              int32_t* y, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (!rnsw::umma_output_ok(plan->host.dev)) return fail(RNSW_ERR_UNSUPPORTED, "plan does not use the Mw8 layout");
+  if (Mw8 == nullptr || y == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, 1, K, pad, layout, &g)) return rc;
+  cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, static_cast<const uint8_t*>(Mw8), y,
+                                                     (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_mw8");
+}
+
+int rnsw_output_transform_requant_mw8(const rnsw_plan* plan, const void* Mw8, int B, int H, int W, int K, int pad,
+                                      int shift, int pool, int8_t* out, void* stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (!rnsw::umma_output_ok(plan->host.dev)) return fail(RNSW_ERR_UNSUPPORTED, "plan does not use the Mw8 layout");
+  if (Mw8 == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (shift < 0 || shift > 31) return fail(RNSW_ERR_INVALID, "shift must be in [0, 31]");
+  if ((K & 3) != 0) return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs K %% 4 == 0");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, 1, K, pad, RNSW_LAYOUT_NHWC, &g)) return rc;
+  if (pool && (g.Ho < 2 || g.Wo < 2)) return fail(RNSW_ERR_SHAPE, "pooling needs Ho, Wo >= 2");
+  cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, static_cast<const uint8_t*>(Mw8), nullptr,
+                                                     (cudaStream_t)stream, out, shift, pool);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant_mw8");
 }
 
 size_t rnsw_direct_weight_bytes(int R, int C, int K) {

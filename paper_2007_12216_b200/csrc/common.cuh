@@ -171,6 +171,14 @@ RNSW_DEV void tma_load_3d(void* dst, const void* desc, uint64_t* bar, int c0, in
       : "memory");
 }
 
+RNSW_DEV void tma_load_5d(void* dst, const void* desc, uint64_t* bar, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
 // Bulk tensor store smem -> global (bulk-group completion).
 RNSW_DEV void tma_store_2d(const void* desc, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -285,6 +293,47 @@ RNSW_DEV uint64_t umma_desc_kmajor(uint32_t smem_addr, uint32_t row_bytes) {
   d |= (uint64_t)1 << 46;                                  // descriptor version (sm_100)
   d |= layout << 61;
   return d;
+}
+
+// UMMA descriptor for an MN-major operand in the 128B-swizzled canonical
+// layout: each K index is one 128-byte row of 128 consecutive M (or N)
+// int8 elements, 8-row groups 1024 bytes apart (SBO); M = 128 is a single
+// atom wide, so LBO is unused.
+RNSW_DEV uint64_t umma_desc_mn_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                   // LBO (unused: one MN atom)
+  d |= (uint64_t)(1024 >> 4) << 32;         // SBO: next 8 K rows
+  d |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+  d |= 2ull << 61;                          // SWIZZLE_128B
+  return d;
+}
+
+// ... in the 32B-swizzled canonical layout: each K index is one 32-byte row
+// of 32 consecutive M elements, 8-row K groups 256 bytes apart (SBO), the
+// next 32 M elements (MN atom) `atom_stride` bytes further (LBO).
+RNSW_DEV uint64_t umma_desc_mn_sw32(uint32_t smem_addr, uint32_t atom_stride) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((atom_stride >> 4) & 0x3FFF) << 16;  // LBO: next MN atom
+  d |= (uint64_t)(256 >> 4) << 32;                      // SBO: next 8 K rows
+  d |= (uint64_t)1 << 46;
+  d |= 6ull << 61;                                      // SWIZZLE_32B
+  return d;
+}
+
+// Byte offset of element (row, col) of a dense array of 32-byte rows under
+// the 32B swizzle (16-byte chunk bit 4 ^= address bit 7).
+__host__ __device__ constexpr uint32_t swz32(uint32_t off) { return off ^ (((off >> 7) & 1u) << 4); }
+// ... of 128-byte rows under the 128B swizzle (chunk ^= row & 7).
+__host__ __device__ constexpr uint32_t swz128(uint32_t off) { return off ^ (((off >> 7) & 7u) << 4); }
+
+// Instruction descriptor for kind::i8 with explicit operand signedness and
+// majorness (a_mn / b_mn: MN-major operand).
+__host__ __device__ constexpr uint32_t idesc_i8x(uint32_t m, uint32_t n, bool a_signed, bool b_signed, bool a_mn,
+                                                 bool b_mn) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
 // Instruction descriptor: s8 x s8 -> s32, both K-major, M x N tile.

@@ -70,6 +70,8 @@ struct GemmArgs {
   int pos_out;  // fast2 16-bit residues written as y mod m in [0, m) (the output
                 // transform's limb split accepts it; saves the symmetric shift)
   int16_t* Mw;
+  int64_t mw8_plane;  // bytes between the two limb planes of one (tile block, residue, position) (Mw8)
+  int planar;  // pos_out residues as two byte planes (Mw8, kernels.h) for the tcgen05 output transform
   FastDiv div_kb, div_pb, div_pos;  // work-tile index decomposition (total_tiles < 2^31)
 };
 
@@ -141,6 +143,38 @@ RNSW_DEV void sts16_swz(uint8_t* stg, int row, int col, const int32_t (&r)[16]) 
   *reinterpret_cast<uint4*>(box + (((c + 1) ^ (row & 7)) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
+// Planar variant (Mw8): the low and high bytes of 16 residues [0, m) into
+// the two plane tiles of the staging buffer (BN-byte rows; 128B swizzle for
+// BN = 128, 64B swizzle for BN = 64, matching the store tensor map).
+template <int BN>
+RNSW_DEV void sts8x2_swz(uint8_t* stg, int row, int col, const int32_t (&r)[16]) {
+  uint32_t lo[4], hi[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t a = __byte_perm((uint32_t)r[4 * e], (uint32_t)r[4 * e + 1], 0x5140);
+    const uint32_t b = __byte_perm((uint32_t)r[4 * e + 2], (uint32_t)r[4 * e + 3], 0x5140);
+    lo[e] = __byte_perm(a, b, 0x5410);
+    hi[e] = __byte_perm(a, b, 0x7632);
+  }
+  uint32_t off = row * BN + col;
+  off = BN == 128 ? swz128(off) : (off ^ (((off >> 7) & 3u) << 4));
+  *reinterpret_cast<uint4*>(stg + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  *reinterpret_cast<uint4*>(stg + kBlockM * BN + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+}
+
+RNSW_DEV void store8x2(uint8_t* lo_row, uint8_t* hi_row, const int32_t (&r)[16]) {
+  uint32_t lo[4], hi[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t a = __byte_perm((uint32_t)r[4 * e], (uint32_t)r[4 * e + 1], 0x5140);
+    const uint32_t b = __byte_perm((uint32_t)r[4 * e + 2], (uint32_t)r[4 * e + 3], 0x5140);
+    lo[e] = __byte_perm(a, b, 0x5410);
+    hi[e] = __byte_perm(a, b, 0x7632);
+  }
+  *reinterpret_cast<uint4*>(lo_row) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  *reinterpret_cast<uint4*>(hi_row) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+}
+
 // Epilogue helpers.  Each thread owns one accumulator row (tile p) and a
 // half of the BN columns.  All TMEM loads of a batch are issued before a
 // single wait; the accumulator is released (tempty arrive) as soon as the
@@ -168,8 +202,8 @@ RNSW_DEV void release_acc(uint64_t* bar, int lane) {
 
 // 16-bit residues: two accumulators (A256, A1) per column.
 template <int BN, int ACC_COLS>
-RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
-                             uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
+RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, uint8_t* out8, int col0,
+                             bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 32 ? kHalf : 32;  // 2 x 32 registers in flight
   const FastMod fm = a.fm[res];
@@ -205,10 +239,21 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
           r[e] = reduce_generic(reduce_generic(hi[j][e], a, res) * 256 + reduce_generic(lo[j][e], a, res), a, res);
       }
       const int col = col0 + c0 + 16 * j;
-      if (stg != nullptr)
+      if (a.planar && !(a.fast2 && a.pos_out)) {
+        // Mw8 holds y mod m in [0, m): lift the symmetric representatives
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] += r[e] < 0 ? fm.m : 0;
+      }
+      if (a.planar) {
+        if (stg != nullptr)
+          sts8x2_swz<BN>(stg, srow, scol0 + c0 + 16 * j, r);
+        else if (row_ok && col < a.Kp)
+          store8x2(out8 + col, out8 + a.mw8_plane + col, r);
+      } else if (stg != nullptr) {
         sts16_swz(stg, srow, scol0 + c0 + 16 * j, r);
-      else if (row_ok && col < a.Kp)
+      } else if (row_ok && col < a.Kp) {
         store16(out_row + col, r);
+      }
     }
   }
 }
@@ -430,7 +475,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // or ragged P): nothing to reduce, just free the accumulator
         release_acc(&tempty[as], lane);
       } else if (MAXPL == 2 && pl == 2) {
-        epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane, stg_t,
+        uint8_t* out8 = reinterpret_cast<uint8_t*>(args.Mw) +
+                        mw8_offset(p, res, 0, pos, args.n_res, args.npos, args.Kp);
+        epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, out8, col0, row_ok, &tempty[as], lane, stg_t,
                                          q * 32 + lane, half * kHalf);
       } else {
         epilogue_single<BN>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane, stg_t, q * 32 + lane,
@@ -440,9 +487,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
         named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
-          const int row0 = (int)(((int64_t)pb * args.n_res * args.npos + res * args.npos + pos) * kBlockM);
+          if (args.planar) {
+            // the two limb planes: rows ((pb * n_res + res) * 2 + limb) * npos + pos) * 128
 #pragma unroll
-          for (int bx = 0; bx < (BN + 63) / 64; ++bx) tma_store_2d(&tmM, stg_b + bx * (kBlockM * 128), kb * BN + 64 * bx, row0);
+            for (int limb = 0; limb < 2; ++limb) {
+              const int row0 = (int)(((((int64_t)pb * args.n_res + res) * 2 + limb) * args.npos + pos) * kBlockM);
+              tma_store_2d(&tmM, stg_b + limb * (kBlockM * BN), kb * BN, row0);
+            }
+          } else {
+            const int row0 = (int)(((int64_t)pb * args.n_res * args.npos + res * args.npos + pos) * kBlockM);
+#pragma unroll
+            for (int bx = 0; bx < (BN + 63) / 64; ++bx)
+              tma_store_2d(&tmM, stg_b + bx * (kBlockM * 128), kb * BN + 64 * bx, row0);
+          }
           bulk_commit();
         }
       }
@@ -477,6 +534,20 @@ bool make_tmap_mw(CUtensorMap* tm, const void* base, int Kp, int64_t rows) {
   return r == CUDA_SUCCESS;
 }
 
+// Mw8 as a 2-D uint8 array [rows][Kp] (rows = limb-plane rows), box BN x 128.
+bool make_tmap_mw8_store(CUtensorMap* tm, const void* base, int Kp, int64_t rows, int bn) {
+  auto encode = encode_fn();
+  if (encode == nullptr) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)Kp};
+  cuuint32_t box[2] = {(cuuint32_t)bn, (cuuint32_t)kBlockM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, bn == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // 3-D view [slabs][rows][Cp] of int8 limb planes; box = (bc bytes, box_rows, 1).
 bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t slabs, int bc, int box_rows) {
   auto encode = encode_fn();
@@ -505,7 +576,11 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_uplanes * a.npos, BC, BN)) return cudaErrorInvalidValue;
   CUtensorMap tmM;
   const int64_t mw_rows = (a.P + kBlockM - 1) / kBlockM * (int64_t)a.n_res * a.npos * kBlockM;
-  if (!make_tmap_mw(&tmM, a.Mw, a.Kp, mw_rows)) return cudaErrorInvalidValue;
+  if (a.planar) {
+    if (!make_tmap_mw8_store(&tmM, a.Mw, a.Kp, mw_rows * 2, BN)) return cudaErrorInvalidValue;
+  } else if (!make_tmap_mw(&tmM, a.Mw, a.Kp, mw_rows)) {
+    return cudaErrorInvalidValue;
+  }
   auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC, TS, SB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
@@ -567,7 +642,7 @@ cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t
 }  // namespace
 
 cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp, int K,
-                                 int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out) {
+                                 int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out, bool planar) {
   const PlanDevice& d = plan.dev;
   GemmArgs a{};
   a.P = P;
@@ -579,6 +654,8 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   a.nkc = Cp / bc;
   a.Mw = Mw;
   a.pos_out = pos_out ? 1 : 0;
+  a.planar = planar ? 1 : 0;
+  a.mw8_plane = (int64_t)a.npos * kBlockM * Kp;
   int maxpl = 1;
   for (int r = 0; r < d.n_res; ++r) {
     a.planes[r] = d.res[r].planes;

@@ -29,6 +29,14 @@ __host__ __device__ inline int64_t mw_offset(int64_t p, int rp, int nrp, int Kp)
   return (((p >> 7) * nrp + rp) * 128 + (p & 127)) * (int64_t)Kp;
 }
 
+// Mw8: the planar variant of Mw that the tcgen05 output transform reads
+// (output_umma.cu): 16-bit residues y mod m in [0, m) split into two byte
+// planes (limb 0 = low byte, limb 1 = high byte),
+// [ceil(P/128)][res][limb][pos][128][Kp] uint8 -- the same size as Mw.
+__host__ __device__ inline int64_t mw8_offset(int64_t p, int res, int limb, int pos, int nres, int npos, int Kp) {
+  return (((((p >> 7) * nres + res) * 2 + limb) * npos + pos) * 128 + (p & 127)) * (int64_t)Kp;
+}
+
 // Host-side mirror of the plan (kept next to the device copy).
 struct PlanHost {
   PlanDevice dev;         // host copy of the tables
@@ -45,7 +53,8 @@ cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, cons
 // pos_out: 16-bit residues as y mod m in [0, m) instead of symmetric (whole-layer
 // path only; the stage API keeps the reference's symmetric residues)
 cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp,
-                                 int K, int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out = false);
+                                 int K, int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out = false,
+                                 bool planar = false);
 cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
                                     int16_t* y_res, cudaStream_t s);
 cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
@@ -54,6 +63,12 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s);
 bool tc_output_ok(const PlanDevice& d);
+// tcgen05 output transform (output_umma.cu): F(14x14,3x3) over two 16-bit
+// residues; reads Mw8.  mode 0: int32 y (layout g.layout), 1: requant int8,
+// 3: requant + 2x2 max-pool int8.
+bool umma_output_ok(const PlanDevice& d);
+cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g, const uint8_t* Mw8, int32_t* y,
+                                         cudaStream_t s, int8_t* out8 = nullptr, int shift = 0, int pool = 0);
 bool force_generic();
 // Small-channel path (C <= 4): compact input transform + CUDA-core product (smallc.cu)
 bool smallc_ok(const PlanDevice& d, const Geometry& g);
@@ -61,7 +76,7 @@ size_t smallc_v16_bytes(const PlanDevice& d, const Geometry& g);
 cudaError_t launch_input_transform_compact(const PlanHost& plan, const Geometry& g, const int8_t* x, int16_t* V16,
                                            cudaStream_t s);
 cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const int16_t* V16, const int8_t* U,
-                                  int16_t* Mw, cudaStream_t s);
+                                  int16_t* Mw, cudaStream_t s, bool planar = false);
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
 size_t direct_weight_bytes(int R, int C, int K);
 cudaError_t launch_pack_weights(const int8_t* w, int R, int C, int K, int layout, int8_t* w2, cudaStream_t s);

@@ -1,0 +1,386 @@
+// K4-K6 on the 5th-generation tensor cores for F(14x14, 3x3) over two 16-bit
+// residues (BASELINE configs 2 and 4): inverse Winograd transform
+// Y = AT M A mod m for both residues, mixed-radix reconstruction and
+// crop/scatter -- or the fused relu / shift / clip / 2x2 max-pool glue -- in
+// one kernel (rw/kernel.py:50-53, rw/residue.py:180-206, rw/layer.py:374-388).
+//
+// CTA = 32 output channels x a run of tiles, 8 warps, 256 TMEM columns.
+// The GEMM (or the small-channel product) leaves y mod m in [0, m) as two
+// byte planes (Mw8, kernels.h), so both transform passes are tcgen05
+// kind::i8 MMAs with M = 128, N = 32, K = 32 and the CUDA cores only
+// recombine limbs, reduce and reconstruct:
+//
+//   pass 1  rows (j, k) = 4 columns j x 32 channels k, K = (limb, i):
+//           A1 = Mat[i][j] limbs, TMA-loaded MN-major (32B swizzle) straight
+//           from Mw8; B1 = [256 AT mod m | AT] limbs; D1 = [A256 | A1] per a.
+//           z[a] = 256 A256 + A1 = sum_i AT[a][i] Mat[i][j] (mod m) is kept
+//           exact (|z| < 2^23, plan z3) and written back as three bytes
+//           z0, z1 (u8) and z2 (s8) into
+//   pass 2  rows (k, a) = 8 channels x 16 rows a, K = (limb, j):
+//           A2 = z limbs (MN-major, one 16-byte chunk per (thread, limb)),
+//           B2 = limbs of AT W, 256 AT W and 65536 AT W mod m (W = the
+//           mixed-radix factor of the residue), plus constant K rows that
+//           add a multiple of m as the reduction bias; D2 = [A256 | A1] per
+//           b.  y = 256 A256 + A1 reduces once to the mixed-radix digit.
+//
+// Per tile and 32 channels: 8 TMA boxes, 8 + 16 MMAs, two TMEM round trips.
+// The next tile's Mw8 boxes load while the current tile's epilogues run.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rnsw {
+namespace {
+
+constexpr int kKB = 32;     // output channels per CTA
+constexpr int kThr = 256;   // 8 warps: TMEM lane quadrant q = warp & 3, half h = warp >> 2
+constexpr int kOpBytes = 4096;  // one MMA A operand: 32 K rows x 128 bytes
+constexpr int kOffA1 = 0;                         // [res][g]          8 x 4 KB
+constexpr int kOffA2 = kOffA1 + 8 * kOpBytes;     // [res][mb][step]  16 x 4 KB
+constexpr int kOffB1 = kOffA2 + 16 * kOpBytes;    // [res]             2 x 1 KB
+constexpr int kOffB2 = kOffB1 + 2 * 1024;         // [res][step]       4 x 1 KB
+constexpr int kOffOut = kOffB2 + 4 * 1024;        // output staging
+constexpr int kPixB = 36;   // staged bytes per pixel (int8 modes; 9 words: conflict-free)
+constexpr int kPixW = 33;   // staged words per pixel (int32 mode)
+constexpr int out_bytes(int mode) { return mode == 0 ? 196 * kPixW * 4 : (mode == 1 ? 196 * kPixB : 49 * kPixB); }
+constexpr int smem_bytes(int mode) { return 1024 + kOffOut + ((out_bytes(mode) + 15) & ~15) + 64; }
+
+struct UArgs {
+  Geometry g;
+  int8_t* out8;
+  int32_t* y;
+  int shift;
+  int tiles_per_cta;
+  FastDiv div_img, div_tw;
+};
+
+// Balanced limb of a symmetric residue c: hi = (c + 128) >> 8, lo = c - 256 hi.
+RNSW_DEV int32_t limb_of(int32_t c, int acc) {
+  const int32_t hi = limb_hi(c);
+  return acc == 0 ? hi : c - 256 * hi;
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kThr, 2)
+    output_umma_kernel(const PlanDevice* __restrict__ plan, const __grid_constant__ CUtensorMap tm, UArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned, derived from the shared array so stores stay STS
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffOut + ((out_bytes(kMode) + 15) & ~15));
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, h = warp >> 2;
+  const Geometry& g = args.g;
+  const int k0 = blockIdx.x * kKB;
+  const int p_begin = blockIdx.y * args.tiles_per_cta;
+  const int p_end = min((int)g.P, p_begin + args.tiles_per_cta);
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tm);
+    mbar_init(&bar[0], 1);  // Mw8 boxes landed
+    mbar_init(&bar[1], 1);  // MMA batch complete
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<256>(tslot);
+
+  // Constant B operands (K-major, 32-byte rows, 32B swizzle), built once.
+  const FastMod fm0 = fast_mod_of(plan->res[0]), fm1 = fast_mod_of(plan->res[1]);
+  const int32_t w10 = plan->mrc_w[1][0];
+  for (int idx = tid; idx < 2 * 32 * 32; idx += kThr) {
+    // B1[res]: row n = (acc, a), K slot = (limb, i); limb 0 (low byte)
+    // multiplies AT, limb 1 (high byte, weight 256) multiplies 256 AT mod m
+    const int res = idx >> 10, n = (idx >> 5) & 31, kap = idx & 31;
+    const int acc = n >> 4, a = n & 15, limb = kap >> 4, i = kap & 15;
+    const FastMod f = res ? fm1 : fm0;
+    const int32_t at = a < 14 ? plan->res[res].at[a * RNSW_MAX_N + i] : 0;
+    const int32_t c = limb == 0 ? at : red_fast(at * 256, f);
+    smem[kOffB1 + res * 1024 + swz32(n * 32 + kap)] = (uint8_t)(int8_t)limb_of(c, acc);
+  }
+  for (int idx = tid; idx < 2 * 2 * 32 * 32; idx += kThr) {
+    // B2[res][step]: row n = (acc, b); step 0 K slot = (z0 | z1, j) against
+    // ATW and 256 ATW, step 1 = (z2, j) against 65536 ATW, then zero padding
+    const int res = idx >> 11, step = (idx >> 10) & 1, n = (idx >> 5) & 31, kap = idx & 31;
+    const int acc = n >> 4, b = n & 15, j = kap & 15;
+    const FastMod f = res ? fm1 : fm0;
+    int32_t c = 0;
+    if (step == 1 && kap >= 16) {
+      // bias slots: A2 holds 127 in these K rows, so pass 2 adds
+      // 127 (256 S256 + S1) = 127 X with X = m ceil(320000 / m) == 0 (mod m),
+      // X spread over the 16 slots; 127 X > 3.95e7 exceeds every negative
+      // pass-2 sum (> -2.22e7, minus the digit term > -1.74e7), keeping the
+      // reduction's input in [0, 2^30)
+      const int32_t m = res ? fm1.m : fm0.m;
+      const int32_t X = m * ((320000 + m - 1) / m);
+      const int32_t S = acc == 0 ? (X >> 8) : (X & 255), sl = kap - 16;
+      c = S / 16 + (sl < S % 16 ? 1 : 0);
+      smem[kOffB2 + (res * 2 + step) * 1024 + swz32(n * 32 + kap)] = (uint8_t)(int8_t)c;
+      continue;
+    }
+    if (b < 14 && (step == 0 || kap < 16)) {
+      const int32_t at = plan->res[res].at[b * RNSW_MAX_N + j];
+      c = res ? red_fast(at * w10, f) : at;  // AT W[1][0]: pass 2 yields y_1 W[1][0]
+      const int shifts = step == 1 ? 2 : (kap >> 4);
+      for (int s = 0; s < shifts; ++s) c = red_fast(c * 256, f);
+    }
+    smem[kOffB2 + (res * 2 + step) * 1024 + swz32(n * 32 + kap)] = (uint8_t)(int8_t)limb_of(c, acc);
+  }
+  // the constant 127 in K rows 16..31 of every step-1 A2 operand (see B2)
+  for (int idx = tid; idx < 8 * 512; idx += kThr) {
+    const int u = idx >> 9, w = idx & 511;  // 512 words = rows 16..31 of buffer u
+    *reinterpret_cast<uint32_t*>(smem + kOffA2 + (u * 2 + 1) * kOpBytes + 2048 + 4 * w) = 0x7F7F7F7Fu;
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  const int32_t negw10 = -w10;
+  const uint32_t m0 = (uint32_t)fm0.m;
+  const uint32_t signed_bound = (uint32_t)plan->signed_bound, dyn_range = (uint32_t)plan->dynamic_range;
+  constexpr uint32_t kIdP1 = idesc_i8x(128, 32, false, true, true, false);   // u8 MN-major x s8
+  constexpr uint32_t kIdP2s = idesc_i8x(128, 32, true, true, true, false);   // s8 MN-major x s8
+  uint8_t* A1 = smem + kOffA1;
+  uint8_t* A2 = smem + kOffA2;
+
+  auto issue_load = [&](int p) {
+    mbar_arrive_expect_tx(&bar[0], 8 * kOpBytes);
+    const int L0 = (p >> 7) * 4;  // (pb * n_res + res) * 2 + limb, n_res = 2
+#pragma unroll
+    for (int res = 0; res < 2; ++res)
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg)
+        tma_load_5d(A1 + (res * 4 + gg) * kOpBytes, &tm, &bar[0], k0, 0, L0 + 2 * res, 4 * gg, p & 127);
+  };
+  if (tid == 0 && p_begin < p_end) issue_load(p_begin);
+
+  uint32_t ph_tma = 0, ph_mma = 0;
+  for (int p = p_begin; p < p_end; ++p) {
+    // ---- pass 1 ----
+    if (tid == 0) {
+      mbar_wait(&bar[0], ph_tma);
+      tc_fence_after();
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        mma_i8(tbase + u * 32, umma_desc_mn_sw32(smem_u32(A1 + u * kOpBytes), 1024),
+               umma_desc_kmajor(smem_u32(smem + kOffB1 + (u >> 2) * 1024), 32), kIdP1, 0u);
+      mma_commit(&bar[1]);
+    }
+    ph_tma ^= 1;
+    mbar_wait(&bar[1], ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+    if (tid == 0 && p + 1 < p_end) issue_load(p + 1);  // A1 is free: overlaps the epilogues
+
+    // ---- epilogue 1: warp (q, h) = columns j = 4 gg + q of residue h, lane = channel ----
+    {
+      uint8_t* a2 = A2 + (h * 4 + (lane >> 3)) * 2 * kOpBytes;
+      const uint32_t chunk = (uint32_t)(lane & 7) << 4;
+#pragma unroll 1
+      for (int gg = 0; gg < 4; ++gg) {
+        const int j = 4 * gg + q;
+        int32_t hi[16], lo[16];
+        const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + (h * 4 + gg) * 32;
+        tmem_ld16(ta, hi);
+        tmem_ld16(ta + 16, lo);
+        tmem_ld_wait();
+        int32_t z[16];
+#pragma unroll
+        for (int a = 0; a < 14; ++a) z[a] = hi[a] * 256 + lo[a];
+        z[14] = z[15] = 0;  // rows a >= 14 of AT are zero; their pass-2 rows are discarded
+        uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t t01 = __byte_perm(z[4 * c], z[4 * c + 1], 0x5140);
+          const uint32_t t23 = __byte_perm(z[4 * c + 2], z[4 * c + 3], 0x5140);
+          w0[c] = __byte_perm(t01, t23, 0x5410);
+          w1[c] = __byte_perm(t01, t23, 0x7632);
+          w2[c] = __byte_perm(__byte_perm(z[4 * c], z[4 * c + 1], 0x0062),
+                              __byte_perm(z[4 * c + 2], z[4 * c + 3], 0x0062), 0x5410);
+        }
+        *reinterpret_cast<uint4*>(a2 + swz128(j * 128 + chunk)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+        *reinterpret_cast<uint4*>(a2 + swz128((16 + j) * 128 + chunk)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+        *reinterpret_cast<uint4*>(a2 + kOpBytes + swz128(j * 128 + chunk)) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- pass 2 ----
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {  // u = res * 4 + mb
+        const uint8_t* a2 = A2 + u * 2 * kOpBytes;
+        const uint8_t* b2 = smem + kOffB2 + (u >> 2) * 2 * 1024;
+        mma_i8(tbase + u * 32, umma_desc_mn_sw128(smem_u32(a2)), umma_desc_kmajor(smem_u32(b2), 32), kIdP1, 0u);
+        mma_i8(tbase + u * 32, umma_desc_mn_sw128(smem_u32(a2 + kOpBytes)), umma_desc_kmajor(smem_u32(b2 + 1024), 32),
+               kIdP2s, 1u);
+      }
+      mma_commit(&bar[1]);
+    }
+    mbar_wait(&bar[1], ph_mma);
+    ph_mma ^= 1;
+    tc_fence_after();
+
+    // ---- epilogue 2: lane row (k, a) = (2q + lane/16, lane % 16) of channel blocks mb = 2h, 2h+1 ----
+    const int b_img = (int)fdiv((uint32_t)p, args.div_img);
+    const int rem = p - b_img * (int)args.div_img.d;
+    const int ti = (int)fdiv((uint32_t)rem, args.div_tw);
+    const int tj = rem - ti * g.tw;
+    {
+      const int a = lane & 15, kk8 = 2 * q + (lane >> 4);
+#pragma unroll 1
+      for (int mbi = 0; mbi < 2; ++mbi) {
+        const int mb = 2 * h + mbi, kl = mb * 8 + kk8;
+        int32_t h0[16], l0[16], h1[16], l1[16];
+        const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + mb * 32;
+        tmem_ld16(ta, h0);
+        tmem_ld16(ta + 16, l0);
+        tmem_ld16(ta + 128, h1);
+        tmem_ld16(ta + 144, l1);
+        tmem_ld_wait();
+        int32_t qv[14];
+#pragma unroll
+        for (int b = 0; b < 14; ++b) {
+          // mixed-radix digits (rw/residue.py:195-206): d0 = y0 mod m0,
+          // d1 = (y1 - d0) m0^-1 mod m1 (the factor rides in B2 of residue 1)
+          // (the MMA added the bias: both sums are already non-negative)
+          const int32_t d0 = red_pos_biased(h0[b] * 256 + l0[b], fm0);
+          const int32_t d1 = red_pos_biased(d0 * negw10 + (h1[b] * 256 + l1[b]), fm1);
+          const uint32_t x = (uint32_t)d0 + m0 * (uint32_t)d1;
+          const bool neg = x > signed_bound;
+          if constexpr (kMode == 0)
+            qv[b] = (int32_t)(neg ? x - dyn_range : x);
+          else if constexpr (kMode == 1)
+            qv[b] = neg ? 0 : min((int32_t)(x >> args.shift), 127);
+          else
+            qv[b] = neg ? 0 : (int32_t)x;  // shift and clip after the max (monotone)
+        }
+        if constexpr (kMode == 3) {
+#pragma unroll
+          for (int c = 0; c < 7; ++c) {
+            int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
+            m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
+            m2 = min(m2 >> args.shift, 127);
+            if ((a & 1) == 0 && a < 14) smem[kOffOut + ((a >> 1) * 7 + c) * kPixB + kl] = (uint8_t)m2;
+          }
+        } else if constexpr (kMode == 1) {
+          if (a < 14) {
+#pragma unroll
+            for (int b = 0; b < 14; ++b) smem[kOffOut + (a * 14 + b) * kPixB + kl] = (uint8_t)qv[b];
+          }
+        } else {
+          int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
+          if (a < 14) {
+#pragma unroll
+            for (int b = 0; b < 14; ++b) ys[(a * 14 + b) * kPixW + kl] = qv[b];
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // staging complete; D2 read (the next pass 1 may overwrite it)
+
+    // ---- stores ----
+    if constexpr (kMode == 0) {
+      const int32_t* ys = reinterpret_cast<const int32_t*>(smem + kOffOut);
+      if (g.layout == 0) {
+        for (int idx = tid; idx < 196 * kKB; idx += kThr) {
+          const int px = idx >> 5, c = idx & 31, a = px / 14, b = px - a * 14;
+          const int ho = ti * 14 + a, wo = tj * 14 + b;
+          if (ho < g.Ho && wo < g.Wo && k0 + c < g.K)
+            args.y[(((int64_t)b_img * g.Ho + ho) * g.Wo + wo) * g.K + k0 + c] = ys[px * kPixW + c];
+        }
+      } else {
+        for (int idx = tid; idx < 196 * kKB; idx += kThr) {
+          const int c = idx / 196, px = idx - c * 196, a = px / 14, b = px - a * 14;
+          const int ho = ti * 14 + a, wo = tj * 14 + b;
+          if (ho < g.Ho && wo < g.Wo && k0 + c < g.K)
+            args.y[(((int64_t)b_img * g.K + k0 + c) * g.Ho + ho) * g.Wo + wo] = ys[px * kPixW + c];
+        }
+      }
+    } else {
+      constexpr int side = kMode == 3 ? 7 : 14;
+      const int Ho = kMode == 3 ? g.Ho / 2 : g.Ho, Wo = kMode == 3 ? g.Wo / 2 : g.Wo;
+      for (int idx = tid; idx < side * side * (kKB / 4); idx += kThr) {
+        const int wq = idx & 7, px = idx >> 3, a = px / side, b = px - a * side;
+        const int ho = ti * side + a, wo = tj * side + b;
+        if (ho >= Ho || wo >= Wo || k0 + 4 * wq >= g.K) continue;
+        const uint32_t word = *reinterpret_cast<const uint32_t*>(smem + kOffOut + px * kPixB + 4 * wq);
+        *reinterpret_cast<uint32_t*>(args.out8 + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 4 * wq) = word;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tbase);
+  }
+}
+
+// Mw8 as a 5-D tensor (k, i, L = (pb * n_res + res) * 2 + limb, j, t); one
+// box = 32 channels x 16 rows i x 2 limbs x 4 columns j x 1 tile lands in
+// shared memory as [j][limb][i][32 channels]: per column j a 32 B-swizzled
+// MN atom of K = 32 rows (limb, i), the 4 atoms 1 KB apart -- an MN-major
+// M = 128 (j, k), K = 32 operand.  (With the 128B swizzle TMA would pad
+// each 32-byte box row to 128 bytes.)
+bool make_tmap_mw8(CUtensorMap* tm, const void* base, int Kp, int64_t num_pb, int nres) {
+  auto encode = encode_fn();
+  if (encode == nullptr) return false;
+  cuuint64_t dims[5] = {(cuuint64_t)Kp, 16, (cuuint64_t)(num_pb * nres * 2), 16, 128};
+  cuuint64_t strides[4] = {(cuuint64_t)Kp * 128 * 16, (cuuint64_t)Kp * 128 * 256, (cuuint64_t)Kp * 128,
+                           (cuuint64_t)Kp};
+  cuuint32_t box[5] = {32, 16, 2, 4, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool umma_output_ok(const PlanDevice& d) {
+  static const bool off = getenv("RNSW_K4_MMA_SYNC") != nullptr;  // A/B switch: the mma.sync kernel
+  return !off && !force_generic() && d.fast && d.n == 16 && d.m_out == 14 && d.n_res == 2 &&
+         d.res[0].planes == 2 && d.res[1].planes == 2 && d.z3;
+}
+
+cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g, const uint8_t* Mw8, int32_t* y,
+                                         cudaStream_t s, int8_t* out8, int shift, int pool) {
+  if (g.P >= (1ll << 31)) return cudaErrorInvalidValue;
+  const int64_t num_pb = (g.P + 127) / 128;
+  CUtensorMap tm;
+  if (!make_tmap_mw8(&tm, Mw8, g.Kp, num_pb, 2)) return cudaErrorInvalidValue;
+  UArgs a{};
+  a.g = g;
+  a.out8 = out8;
+  a.y = y;
+  a.shift = shift;
+  const int kblocks = (g.K + kKB - 1) / kKB;
+  const int64_t units = g.P * kblocks;
+  a.tiles_per_cta = (int)std::max<int64_t>(1, std::min<int64_t>(16, units / (148 * 2 * 4)));
+  a.div_img = make_fastdiv((uint32_t)(g.th * g.tw));
+  a.div_tw = make_fastdiv((uint32_t)g.tw);
+  dim3 grid(kblocks, (unsigned)((g.P + a.tiles_per_cta - 1) / a.tiles_per_cta));
+  const int mode = out8 == nullptr ? 0 : (pool ? 3 : 1);
+  auto launch = [&](auto kern, int smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThr, smem, s>>>(plan.d_plan, tm, a);
+    return cudaGetLastError();
+  };
+  if (mode == 0) return launch(output_umma_kernel<0>, smem_bytes(0));
+  if (mode == 1) return launch(output_umma_kernel<1>, smem_bytes(1));
+  return launch(output_umma_kernel<3>, smem_bytes(3));
+}
+
+}  // namespace rnsw

@@ -20,7 +20,9 @@ namespace {
 // kPL == 2 (16-bit moduli): Mw holds y mod m in [0, m), which the output
 // transform's limb split accepts (its bound analysis covers [0, m)).
 // kPL == 1: symmetric residues (the s8 fragments of the output transform).
-template <int kPL>
+// kPlanar (16-bit only): write Mw8, the two byte planes the tcgen05 output
+// transform reads (kernels.h mw8_offset).
+template <int kPL, bool kPlanar = false>
 __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* __restrict__ plan, int P, int K,
                                                              int Kp, int Cp, const int16_t* __restrict__ V16,
                                                              const int8_t* __restrict__ U, int16_t* __restrict__ Mw,
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
       const int32_t v0 = (int32_t)(w.x << 16) >> 16, v1 = (int32_t)w.x >> 16;
       const int32_t v2 = (int32_t)(w.y << 16) >> 16, v3 = (int32_t)w.y >> 16;
       uint32_t o[4];
+      int32_t yv[8];
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         int32_t y[2];
@@ -81,10 +84,22 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
           // |sum| <= 4 h^2 < 2^28 for m < 4500
           const int32_t n = bias + v0 * u[kk][0] + v1 * u[kk][1] + v2 * u[kk][2] + v3 * u[kk][3];
           y[e] = kPL == 2 ? red_pos_biased(n, fm) : red_pos_biased(n, fm) - fm.h;
+          yv[kk] = y[e];
         }
         o[h] = __byte_perm((uint32_t)y[0], (uint32_t)y[1], 0x5410);
       }
-      *(reinterpret_cast<uint4*>(Mw + mw_offset(p, rp, nrp, Kp)) + kg) = make_uint4(o[0], o[1], o[2], o[3]);
+      if constexpr (kPlanar) {
+        uint8_t* base = reinterpret_cast<uint8_t*>(Mw) + mw8_offset(p, r, 0, pos, nres, npos, Kp) + 8 * kg;
+        const uint32_t a0 = __byte_perm((uint32_t)yv[0], (uint32_t)yv[1], 0x5140);
+        const uint32_t a1 = __byte_perm((uint32_t)yv[2], (uint32_t)yv[3], 0x5140);
+        const uint32_t a2 = __byte_perm((uint32_t)yv[4], (uint32_t)yv[5], 0x5140);
+        const uint32_t a3 = __byte_perm((uint32_t)yv[6], (uint32_t)yv[7], 0x5140);
+        *reinterpret_cast<uint2*>(base) = make_uint2(__byte_perm(a0, a1, 0x5410), __byte_perm(a2, a3, 0x5410));
+        *reinterpret_cast<uint2*>(base + (int64_t)npos * 128 * Kp) =
+            make_uint2(__byte_perm(a0, a1, 0x7632), __byte_perm(a2, a3, 0x7632));
+      } else {
+        *(reinterpret_cast<uint4*>(Mw + mw_offset(p, rp, nrp, Kp)) + kg) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
     }
   }
 }
@@ -98,7 +113,7 @@ size_t smallc_v16_bytes(const PlanDevice& d, const Geometry& g) {
 }
 
 cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const int16_t* V16, const int8_t* U,
-                                  int16_t* Mw, cudaStream_t s) {
+                                  int16_t* Mw, cudaStream_t s, bool planar) {
   const PlanDevice& d = plan.dev;
   const int npos = d.n * d.n, slots = npos * (g.Kp / 8);
   const int bx = (slots + 255) / 256;
@@ -107,7 +122,9 @@ cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const
   const int64_t per_tile = (int64_t)bx * d.n_res;
   const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, g.P * per_tile / (148 * 4)));
   dim3 grid(bx, d.n_res, (unsigned)((g.P + tpc - 1) / tpc));
-  if (d.res[0].planes == 2)
+  if (d.res[0].planes == 2 && planar)
+    smallc_product_kernel<2, true><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+  else if (d.res[0].planes == 2)
     smallc_product_kernel<2><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
   else
     smallc_product_kernel<1><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);

@@ -175,7 +175,8 @@ def test_fused_requant_single_layers():
 
 @pytest.mark.skipif(__import__("os").environ.get("RNSW_K4_NO_Z3") is not None, reason="already the alternate path")
 def test_alternate_kernel_paths_in_subprocess():
-    """The A/B switches read once per process (RNSW_K4_NO_Z3: K4 with a
+    """The A/B switches read once per process (RNSW_K4_MMA_SYNC: the mma.sync
+    output transform instead of the tcgen05 one; RNSW_K4_NO_Z3: it with a
     reduced pass 1 instead of the three-limb pass 2; RNSW_GEMM_NO_MC: GEMM
     without CTA pairs) select kernels the default dispatch does not use for
     the VGG16 shapes: rerun the VGG16 and fused-epilogue checks on them."""
@@ -183,7 +184,7 @@ def test_alternate_kernel_paths_in_subprocess():
     import subprocess
     import sys
 
-    env = dict(os.environ, RNSW_K4_NO_Z3="1", RNSW_GEMM_NO_MC="1")
+    env = dict(os.environ, RNSW_K4_NO_Z3="1", RNSW_GEMM_NO_MC="1", RNSW_K4_MMA_SYNC="1")
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(here, "test_gpu_configs.py"),
