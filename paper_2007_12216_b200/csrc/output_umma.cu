@@ -4,7 +4,8 @@
 // crop/scatter -- or the fused relu / shift / clip / 2x2 max-pool glue -- in
 // one kernel (rw/kernel.py:50-53, rw/residue.py:180-206, rw/layer.py:374-388).
 //
-// CTA = 32 output channels x a run of tiles, 8 warps, 256 TMEM columns.
+// Persistent CTAs (two per SM, 8 warps, 256 TMEM columns each) over work
+// units of one tile x 32 output channels.
 // The GEMM (or the small-channel product) leaves y mod m in [0, m) as two
 // byte planes (Mw8, kernels.h), so both transform passes are tcgen05
 // kind::i8 MMAs with M = 128, N = 32, K = 32 and the CUDA cores only
@@ -23,8 +24,8 @@
 //           add a multiple of m as the reduction bias; D2 = [A256 | A1] per
 //           b.  y = 256 A256 + A1 reduces once to the mixed-radix digit.
 //
-// Per tile and 32 channels: 8 TMA boxes, 8 + 16 MMAs, two TMEM round trips.
-// The next tile's Mw8 boxes load while the current tile's epilogues run.
+// Per unit: 8 TMA boxes, 8 + 16 MMAs, two TMEM round trips; the next unit's
+// boxes load during this unit's epilogues.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -36,7 +37,7 @@
 namespace rnsw {
 namespace {
 
-constexpr int kKB = 32;     // output channels per CTA
+constexpr int kKB = 32;     // output channels per work unit
 constexpr int kThr = 256;   // 8 warps: TMEM lane quadrant q = warp & 3, half h = warp >> 2
 constexpr int kOpBytes = 4096;  // one MMA A operand: 32 K rows x 128 bytes
 constexpr int kOffA1 = 0;                         // [res][g]          8 x 4 KB
@@ -54,8 +55,10 @@ struct UArgs {
   int8_t* out8;
   int32_t* y;
   int shift;
-  int tiles_per_cta;
-  FastDiv div_img, div_tw;
+  int kblocks;
+  int64_t units;       // P * kblocks work units (tile, 32-channel block)
+  int32_t negw10;      // -W[1][0] (kept opaque to the compiler: one IMAD per digit)
+  FastDiv div_img, div_tw, div_kb;
 };
 
 // Balanced limb of a symmetric residue c: hi = (c + 128) >> 8, lo = c - 256 hi.
@@ -64,6 +67,13 @@ RNSW_DEV int32_t limb_of(int32_t c, int acc) {
   return acc == 0 ? hi : c - 256 * hi;
 }
 
+// Persistent: two CTAs per SM (each 256 TMEM columns, shared by the pass-1
+// and pass-2 accumulators) walk the work units u = (tile p, channel block
+// kb); while one CTA waits for its MMAs the other runs its epilogues.  The
+// Mw8 boxes of the next unit load during the current unit's epilogues.
+// (A single 16-warp CTA per SM that overlaps pass 1 of the next unit with
+// epilogue 2 in separate TMEM halves measured 25% slower: every warp then
+// waits on the same pass-2 completion and barriers.)
 template <int kMode>
 __global__ void __launch_bounds__(kThr, 2)
     output_umma_kernel(const PlanDevice* __restrict__ plan, const __grid_constant__ CUtensorMap tm, UArgs args) {
@@ -75,9 +85,6 @@ __global__ void __launch_bounds__(kThr, 2)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
-  const int k0 = blockIdx.x * kKB;
-  const int p_begin = blockIdx.y * args.tiles_per_cta;
-  const int p_end = min((int)g.P, p_begin + args.tiles_per_cta);
 
   if (tid == 0) {
     tma_prefetch_desc(&tm);
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(kThr, 2)
   }
   for (int idx = tid; idx < 2 * 2 * 32 * 32; idx += kThr) {
     // B2[res][step]: row n = (acc, b); step 0 K slot = (z0 | z1, j) against
-    // ATW and 256 ATW, step 1 = (z2, j) against 65536 ATW, then zero padding
+    // ATW and 256 ATW, step 1 = (z2, j) against 65536 ATW, then the bias slots
     const int res = idx >> 11, step = (idx >> 10) & 1, n = (idx >> 5) & 31, kap = idx & 31;
     const int acc = n >> 4, b = n & 15, j = kap & 15;
     const FastMod f = res ? fm1 : fm0;
@@ -139,7 +146,7 @@ __global__ void __launch_bounds__(kThr, 2)
   tc_fence_after();
   const uint32_t tbase = *tslot;
 
-  const int32_t negw10 = -w10;
+  const int32_t negw10 = args.negw10;
   const uint32_t m0 = (uint32_t)fm0.m;
   const uint32_t signed_bound = (uint32_t)plan->signed_bound, dyn_range = (uint32_t)plan->dynamic_range;
   constexpr uint32_t kIdP1 = idesc_i8x(128, 32, false, true, true, false);   // u8 MN-major x s8
@@ -147,7 +154,10 @@ __global__ void __launch_bounds__(kThr, 2)
   uint8_t* A1 = smem + kOffA1;
   uint8_t* A2 = smem + kOffA2;
 
-  auto issue_load = [&](int p) {
+  // unit -> (tile p, channel offset k0); kb fastest
+  auto unit_p = [&](int64_t u) { return (int)fdiv((uint32_t)u, args.div_kb); };
+  auto issue_load = [&](int64_t u) {
+    const int p = unit_p(u), k0 = (int)(u - (int64_t)p * args.kblocks) * kKB;
     mbar_arrive_expect_tx(&bar[0], 8 * kOpBytes);
     const int L0 = (p >> 7) * 4;  // (pb * n_res + res) * 2 + limb, n_res = 2
 #pragma unroll
@@ -156,27 +166,29 @@ __global__ void __launch_bounds__(kThr, 2)
       for (int gg = 0; gg < 4; ++gg)
         tma_load_5d(A1 + (res * 4 + gg) * kOpBytes, &tm, &bar[0], k0, 0, L0 + 2 * res, 4 * gg, p & 127);
   };
-  if (tid == 0 && p_begin < p_end) issue_load(p_begin);
+  const int64_t u_step = gridDim.x;
+  if (tid == 0 && (int64_t)blockIdx.x < args.units) issue_load(blockIdx.x);
 
   uint32_t ph_tma = 0, ph_mma = 0;
-  for (int p = p_begin; p < p_end; ++p) {
-    // ---- pass 1 ----
+  for (int64_t u = blockIdx.x; u < args.units; u += u_step) {
+    const int p = unit_p(u), k0 = (int)(u - (int64_t)p * args.kblocks) * kKB;
+    // ---- pass 1 into TMEM [0, 256) ----
     if (tid == 0) {
       mbar_wait(&bar[0], ph_tma);
       tc_fence_after();
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        mma_i8(tbase + u * 32, umma_desc_mn_sw32(smem_u32(A1 + u * kOpBytes), 1024),
-               umma_desc_kmajor(smem_u32(smem + kOffB1 + (u >> 2) * 1024), 32), kIdP1, 0u);
+      for (int v = 0; v < 8; ++v)
+        mma_i8(tbase + v * 32, umma_desc_mn_sw32(smem_u32(A1 + v * kOpBytes), 1024),
+               umma_desc_kmajor(smem_u32(smem + kOffB1 + (v >> 2) * 1024), 32), kIdP1, 0u);
       mma_commit(&bar[1]);
     }
     ph_tma ^= 1;
     mbar_wait(&bar[1], ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
-    if (tid == 0 && p + 1 < p_end) issue_load(p + 1);  // A1 is free: overlaps the epilogues
+    if (tid == 0 && u + u_step < args.units) issue_load(u + u_step);  // A1 is free: overlaps the epilogues
 
-    // ---- epilogue 1: warp (q, h) = columns j = 4 gg + q of residue h, lane = channel ----
+    // ---- epilogue 1: warp (q, h): columns j = 4 gg + q of residue h, lane = channel ----
     {
       uint8_t* a2 = A2 + (h * 4 + (lane >> 3)) * 2 * kOpBytes;
       const uint32_t chunk = (uint32_t)(lane & 7) << 4;
@@ -211,15 +223,15 @@ __global__ void __launch_bounds__(kThr, 2)
     tc_fence_before();
     __syncthreads();
 
-    // ---- pass 2 ----
+    // ---- pass 2 into the same columns (pass 1 has been read) ----
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {  // u = res * 4 + mb
-        const uint8_t* a2 = A2 + u * 2 * kOpBytes;
-        const uint8_t* b2 = smem + kOffB2 + (u >> 2) * 2 * 1024;
-        mma_i8(tbase + u * 32, umma_desc_mn_sw128(smem_u32(a2)), umma_desc_kmajor(smem_u32(b2), 32), kIdP1, 0u);
-        mma_i8(tbase + u * 32, umma_desc_mn_sw128(smem_u32(a2 + kOpBytes)), umma_desc_kmajor(smem_u32(b2 + 1024), 32),
+      for (int v = 0; v < 8; ++v) {  // v = res * 4 + mb
+        const uint8_t* a2 = A2 + v * 2 * kOpBytes;
+        const uint8_t* b2 = smem + kOffB2 + (v >> 2) * 2 * 1024;
+        mma_i8(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2)), umma_desc_kmajor(smem_u32(b2), 32), kIdP1, 0u);
+        mma_i8(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2 + kOpBytes)), umma_desc_kmajor(smem_u32(b2 + 1024), 32),
                kIdP2s, 1u);
       }
       mma_commit(&bar[1]);
@@ -237,55 +249,55 @@ __global__ void __launch_bounds__(kThr, 2)
       const int a = lane & 15, kk8 = 2 * q + (lane >> 4);
 #pragma unroll 1
       for (int mbi = 0; mbi < 2; ++mbi) {
-        const int mb = 2 * h + mbi, kl = mb * 8 + kk8;
-        int32_t h0[16], l0[16], h1[16], l1[16];
-        const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + mb * 32;
-        tmem_ld16(ta, h0);
-        tmem_ld16(ta + 16, l0);
-        tmem_ld16(ta + 128, h1);
-        tmem_ld16(ta + 144, l1);
-        tmem_ld_wait();
-        int32_t qv[14];
+      const int mb = 2 * h + mbi, kl = mb * 8 + kk8;
+      int32_t h0[16], l0[16], h1[16], l1[16];
+      const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + mb * 32;
+      tmem_ld16(ta, h0);
+      tmem_ld16(ta + 16, l0);
+      tmem_ld16(ta + 128, h1);
+      tmem_ld16(ta + 144, l1);
+      tmem_ld_wait();
+      int32_t qv[14];
 #pragma unroll
-        for (int b = 0; b < 14; ++b) {
-          // mixed-radix digits (rw/residue.py:195-206): d0 = y0 mod m0,
-          // d1 = (y1 - d0) m0^-1 mod m1 (the factor rides in B2 of residue 1)
-          // (the MMA added the bias: both sums are already non-negative)
-          const int32_t d0 = red_pos_biased(h0[b] * 256 + l0[b], fm0);
-          const int32_t d1 = red_pos_biased(d0 * negw10 + (h1[b] * 256 + l1[b]), fm1);
-          const uint32_t x = (uint32_t)d0 + m0 * (uint32_t)d1;
-          const bool neg = x > signed_bound;
-          if constexpr (kMode == 0)
-            qv[b] = (int32_t)(neg ? x - dyn_range : x);
-          else if constexpr (kMode == 1)
-            qv[b] = neg ? 0 : min((int32_t)(x >> args.shift), 127);
-          else
-            qv[b] = neg ? 0 : (int32_t)x;  // shift and clip after the max (monotone)
+      for (int b = 0; b < 14; ++b) {
+        // mixed-radix digits (rw/residue.py:195-206): d0 = y0 mod m0,
+        // d1 = (y1 - d0) m0^-1 mod m1 (the factor rides in B2 of residue 1);
+        // the MMA added the bias, both sums are already non-negative
+        const int32_t d0 = red_pos_biased(h0[b] * 256 + l0[b], fm0);
+        const int32_t d1 = red_pos_biased(d0 * negw10 + (h1[b] * 256 + l1[b]), fm1);
+        const uint32_t x = (uint32_t)d0 + m0 * (uint32_t)d1;
+        const bool neg = x > signed_bound;
+        if constexpr (kMode == 0)
+          qv[b] = (int32_t)(neg ? x - dyn_range : x);
+        else if constexpr (kMode == 1)
+          qv[b] = neg ? 0 : min((int32_t)(x >> args.shift), 127);
+        else
+          qv[b] = neg ? 0 : (int32_t)x;  // shift and clip after the max (monotone)
+      }
+      if constexpr (kMode == 3) {
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+          int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
+          m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
+          m2 = min(m2 >> args.shift, 127);
+          if ((a & 1) == 0 && a < 14) smem[kOffOut + ((a >> 1) * 7 + c) * kPixB + kl] = (uint8_t)m2;
         }
-        if constexpr (kMode == 3) {
+      } else if constexpr (kMode == 1) {
+        if (a < 14) {
 #pragma unroll
-          for (int c = 0; c < 7; ++c) {
-            int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
-            m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
-            m2 = min(m2 >> args.shift, 127);
-            if ((a & 1) == 0 && a < 14) smem[kOffOut + ((a >> 1) * 7 + c) * kPixB + kl] = (uint8_t)m2;
-          }
-        } else if constexpr (kMode == 1) {
-          if (a < 14) {
-#pragma unroll
-            for (int b = 0; b < 14; ++b) smem[kOffOut + (a * 14 + b) * kPixB + kl] = (uint8_t)qv[b];
-          }
-        } else {
-          int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
-          if (a < 14) {
-#pragma unroll
-            for (int b = 0; b < 14; ++b) ys[(a * 14 + b) * kPixW + kl] = qv[b];
-          }
+          for (int b = 0; b < 14; ++b) smem[kOffOut + (a * 14 + b) * kPixB + kl] = (uint8_t)qv[b];
         }
+      } else {
+        int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
+        if (a < 14) {
+#pragma unroll
+          for (int b = 0; b < 14; ++b) ys[(a * 14 + b) * kPixW + kl] = qv[b];
+        }
+      }
       }
     }
     tc_fence_before();
-    __syncthreads();  // staging complete; D2 read (the next pass 1 may overwrite it)
+    __syncthreads();  // staging complete; pass-2 accumulators read
 
     // ---- stores ----
     if constexpr (kMode == 0) {
@@ -365,12 +377,20 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
   a.out8 = out8;
   a.y = y;
   a.shift = shift;
-  const int kblocks = (g.K + kKB - 1) / kKB;
-  const int64_t units = g.P * kblocks;
-  a.tiles_per_cta = (int)std::max<int64_t>(1, std::min<int64_t>(16, units / (148 * 2 * 4)));
+  a.kblocks = (g.K + kKB - 1) / kKB;
+  a.units = g.P * a.kblocks;
+  if (a.units >= (1ll << 31)) return cudaErrorInvalidValue;  // FastDiv range
+  a.negw10 = -plan.dev.mrc_w[1][0];
   a.div_img = make_fastdiv((uint32_t)(g.th * g.tw));
   a.div_tw = make_fastdiv((uint32_t)g.tw);
-  dim3 grid(kblocks, (unsigned)((g.P + a.tiles_per_cta - 1) / a.tiles_per_cta));
+  a.div_kb = make_fastdiv((uint32_t)a.kblocks);
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(a.units, 2 * num_sms);
   const int mode = out8 == nullptr ? 0 : (pool ? 3 : 1);
   auto launch = [&](auto kern, int smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
