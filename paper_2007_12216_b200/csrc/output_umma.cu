@@ -167,22 +167,25 @@ __global__ void __launch_bounds__(kThr, 2)
         tma_load_5d(A1 + (res * 4 + gg) * kOpBytes, &tm, &bar[0], k0, 0, L0 + 2 * res, 4 * gg, p & 127);
   };
   const int64_t u_step = gridDim.x;
-  if (tid == 0 && (int64_t)blockIdx.x < args.units) issue_load(blockIdx.x);
-
   uint32_t ph_tma = 0, ph_mma = 0;
+  auto issue_p1 = [&]() {  // thread 0: pass 1 into the 256 TMEM columns once the boxes landed
+    mbar_wait(&bar[0], ph_tma);
+    ph_tma ^= 1;
+    tc_fence_after();
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      mma_i8(tbase + v * 32, umma_desc_mn_sw32(smem_u32(A1 + v * kOpBytes), 1024),
+             umma_desc_kmajor(smem_u32(smem + kOffB1 + (v >> 2) * 1024), 32), kIdP1, 0u);
+    mma_commit(&bar[1]);
+  };
+  if (tid == 0 && (int64_t)blockIdx.x < args.units) {
+    issue_load(blockIdx.x);
+    issue_p1();
+  }
+
   for (int64_t u = blockIdx.x; u < args.units; u += u_step) {
     const int p = unit_p(u), k0 = (int)(u - (int64_t)p * args.kblocks) * kKB;
-    // ---- pass 1 into TMEM [0, 256) ----
-    if (tid == 0) {
-      mbar_wait(&bar[0], ph_tma);
-      tc_fence_after();
-#pragma unroll
-      for (int v = 0; v < 8; ++v)
-        mma_i8(tbase + v * 32, umma_desc_mn_sw32(smem_u32(A1 + v * kOpBytes), 1024),
-               umma_desc_kmajor(smem_u32(smem + kOffB1 + (v >> 2) * 1024), 32), kIdP1, 0u);
-      mma_commit(&bar[1]);
-    }
-    ph_tma ^= 1;
+    // ---- pass 1 (issued before the previous unit's stores) ----
     mbar_wait(&bar[1], ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
@@ -298,6 +301,10 @@ __global__ void __launch_bounds__(kThr, 2)
     }
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
+    if (tid == 0 && u + u_step < args.units) {
+      tc_fence_after();
+      issue_p1();  // the next unit's pass 1 overlaps these stores
+    }
 
     // ---- stores ----
     if constexpr (kMode == 0) {
