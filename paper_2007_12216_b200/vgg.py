@@ -93,21 +93,29 @@ class VGG16Rns:
             })
         return out
 
+    def _mw8(self) -> bool:
+        """Whether the whole-layer path hands the product to the tcgen05
+        output transform in the planar Mw8 layout (include/rnsw.h)."""
+        return _native.lib().rnsw_mw8_supported(self.plan.handle) == 1
+
     def _staged_product(self, timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, mb, s):
         """Stages 1-2 of one layer as rnsw_conv_forward runs them: the
         tensor-core GEMM split, or for C <= 4 the compact transform + CUDA-core
-        product (kind "product")."""
+        product (kind "product"), into Mw8 when the plan uses it."""
         l = _native.lib()
         vp = _native.c_void_p
+        mw8 = self._mw8()
         if c <= 4:
             timed("input_transform", i, lambda: l.rnsw_input_transform_compact(
                 self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
-            timed("product", i, lambda: l.rnsw_small_channel_product(
+            product = l.rnsw_small_channel_product_mw8 if mw8 else l.rnsw_small_channel_product
+            timed("product", i, lambda: product(
                 self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), mb, s))
             return
         timed("input_transform", i, lambda: l.rnsw_input_transform(
             self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
-        timed("gemm", i, lambda: l.rnsw_winograd_gemm(
+        gemm = l.rnsw_winograd_gemm_mw8 if mw8 else l.rnsw_winograd_gemm
+        timed("gemm", i, lambda: gemm(
             self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), mb, s))
 
     def forward_staged(self, x, record):
@@ -136,7 +144,8 @@ class VGG16Rns:
             vb = (l.rnsw_v_bytes(self.plan.handle, tiles, c) + 255) // 256 * 256
             v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
             self._staged_product(timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, ws.numel() - vb, s)
-            timed("output_transform", i, lambda: l.rnsw_output_transform(
+            out_t = l.rnsw_output_transform_mw8 if self._mw8() else l.rnsw_output_transform
+            timed("output_transform", i, lambda: out_t(
                 self.plan.handle, vp(m_ptr), batch, side, side, k, 1, _native.LAYOUT_NHWC, vp(y.data_ptr()), s))
             oside = side // 2 if pool else side
             nxt = bufs["out"] if i == nl - 1 else \
@@ -287,7 +296,8 @@ class VGG16Rns:
             nxt = bufs["out"] if i == nl - 1 else \
                 bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
             self._staged_product(timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, ws.numel() - vb, s)
-            timed("output_transform", i, lambda: l.rnsw_output_transform_requant(
+            out_t = l.rnsw_output_transform_requant_mw8 if self._mw8() else l.rnsw_output_transform_requant
+            timed("output_transform", i, lambda: out_t(
                 self.plan.handle, vp(m_ptr), batch, side, side, k, 1, self.cfg.shifts[i], 1 if pool else 0,
                 vp(nxt.data_ptr()), s))
             cur = nxt
