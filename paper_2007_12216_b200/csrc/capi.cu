@@ -101,6 +101,55 @@ size_t m_bytes(const PlanDevice& d, int64_t P, int Kp) {  // blocked layout (ker
 
 }  // namespace
 
+namespace {
+// Host copy of the output_umma.cu constant operands (see PlanDevice::umma_b):
+// B1[res] rows n = (acc, a) x K slots (limb, i) hold the balanced limbs of
+// AT (limb 0) and 256 AT mod m (limb 1); B2[res][0] rows (acc, b) x (z0 | z1, j)
+// the limbs of ATW and 256 ATW, B2[res][1] (z2, j) those of 65536 ATW, then
+// 16 bias slots whose 127-weighted sum is 127 X, X = m ceil(320000 / m).
+// ATW = AT W[1][0] for residue 1 (the mixed-radix factor), AT for residue 0.
+void build_umma_b(PlanDevice& d) {
+  auto sym = [](int64_t v, int64_t m) {
+    v %= m;
+    if (v < 0) v += m;
+    return v > (m - 1) / 2 ? v - m : v;
+  };
+  auto limb = [](int64_t c, int acc) {
+    const int64_t hi = (c + 128 + 256 * 64) / 256 - 64;  // floor((c + 128) / 256)
+    return (int8_t)(acc == 0 ? hi : c - 256 * hi);
+  };
+  auto swz = [](uint32_t off) { return off ^ (((off >> 7) & 1u) << 4); };
+  memset(d.umma_b, 0, sizeof(d.umma_b));
+  for (int res = 0; res < 2; ++res) {
+    const int64_t m = d.res[res].modulus;
+    for (int n = 0; n < 32; ++n)
+      for (int kap = 0; kap < 32; ++kap) {
+        const int acc = n >> 4, a = n & 15, lb = kap >> 4, i = kap & 15;
+        const int64_t at = a < 14 ? d.res[res].at[a * RNSW_MAX_N + i] : 0;
+        d.umma_b[res * 1024 + swz(n * 32 + kap)] = (uint8_t)limb(lb == 0 ? at : sym(at * 256, m), acc);
+      }
+    for (int step = 0; step < 2; ++step)
+      for (int n = 0; n < 32; ++n)
+        for (int kap = 0; kap < 32; ++kap) {
+          const int acc = n >> 4, b = n & 15, j = kap & 15;
+          int8_t v = 0;
+          if (step == 1 && kap >= 16) {
+            const int64_t X = m * ((320000 + m - 1) / m);
+            const int64_t S = acc == 0 ? (X >> 8) : (X & 255), sl = kap - 16;
+            v = (int8_t)(S / 16 + (sl < S % 16 ? 1 : 0));
+          } else if (b < 14 && (step == 0 || kap < 16)) {
+            int64_t c = d.res[res].at[b * RNSW_MAX_N + j];
+            if (res) c = sym(c * d.mrc_w[1][0], m);
+            const int shifts = step == 1 ? 2 : (kap >> 4);
+            for (int t = 0; t < shifts; ++t) c = sym(c * 256, m);
+            v = limb(c, acc);
+          }
+          d.umma_b[2048 + (res * 2 + step) * 1024 + swz(n * 32 + kap)] = (uint8_t)v;
+        }
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char* rnsw_error_string(int code) {
@@ -237,6 +286,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
       const int64_t mj = moduli[j], next = i == j - 1 ? 1 : d.mrc_w[j][i + 1];
       d.mrc_w[j][i] = (int32_t)(((next * (d.mrc_inv[j][i] % mj)) % mj + mj) % mj);
     }
+  if (n == 16 && tile_m == 14 && n_res == 2 && d.res[0].planes == 2 && d.res[1].planes == 2) build_umma_b(d);
   cudaError_t e = cudaGetDevice(&plan->host.device);
   if (e == cudaSuccess) e = cudaMalloc(&plan->host.d_plan, sizeof(PlanDevice));
   if (e == cudaSuccess) e = cudaMemcpy(plan->host.d_plan, &d, sizeof(d), cudaMemcpyHostToDevice);

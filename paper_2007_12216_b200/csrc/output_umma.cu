@@ -94,47 +94,11 @@ __global__ void __launch_bounds__(kThr, 2)
   }
   if (warp == 0) tmem_alloc<256>(tslot);
 
-  // Constant B operands (K-major, 32-byte rows, 32B swizzle), built once.
+  // Constant B operands (K-major, 32-byte rows, 32B swizzle): built on the
+  // host into the plan (capi.cu build_umma_b), 6 KB copied once per CTA
+  for (int idx = tid; idx < 6144 / 16; idx += kThr)
+    reinterpret_cast<uint4*>(smem + kOffB1)[idx] = __ldg(reinterpret_cast<const uint4*>(plan->umma_b) + idx);
   const FastMod fm0 = fast_mod_of(plan->res[0]), fm1 = fast_mod_of(plan->res[1]);
-  const int32_t w10 = plan->mrc_w[1][0];
-  for (int idx = tid; idx < 2 * 32 * 32; idx += kThr) {
-    // B1[res]: row n = (acc, a), K slot = (limb, i); limb 0 (low byte)
-    // multiplies AT, limb 1 (high byte, weight 256) multiplies 256 AT mod m
-    const int res = idx >> 10, n = (idx >> 5) & 31, kap = idx & 31;
-    const int acc = n >> 4, a = n & 15, limb = kap >> 4, i = kap & 15;
-    const FastMod f = res ? fm1 : fm0;
-    const int32_t at = a < 14 ? plan->res[res].at[a * RNSW_MAX_N + i] : 0;
-    const int32_t c = limb == 0 ? at : red_fast(at * 256, f);
-    smem[kOffB1 + res * 1024 + swz32(n * 32 + kap)] = (uint8_t)(int8_t)limb_of(c, acc);
-  }
-  for (int idx = tid; idx < 2 * 2 * 32 * 32; idx += kThr) {
-    // B2[res][step]: row n = (acc, b); step 0 K slot = (z0 | z1, j) against
-    // ATW and 256 ATW, step 1 = (z2, j) against 65536 ATW, then the bias slots
-    const int res = idx >> 11, step = (idx >> 10) & 1, n = (idx >> 5) & 31, kap = idx & 31;
-    const int acc = n >> 4, b = n & 15, j = kap & 15;
-    const FastMod f = res ? fm1 : fm0;
-    int32_t c = 0;
-    if (step == 1 && kap >= 16) {
-      // bias slots: A2 holds 127 in these K rows, so pass 2 adds
-      // 127 (256 S256 + S1) = 127 X with X = m ceil(320000 / m) == 0 (mod m),
-      // X spread over the 16 slots; 127 X > 3.95e7 exceeds every negative
-      // pass-2 sum (> -2.22e7, minus the digit term > -1.74e7), keeping the
-      // reduction's input in [0, 2^30)
-      const int32_t m = res ? fm1.m : fm0.m;
-      const int32_t X = m * ((320000 + m - 1) / m);
-      const int32_t S = acc == 0 ? (X >> 8) : (X & 255), sl = kap - 16;
-      c = S / 16 + (sl < S % 16 ? 1 : 0);
-      smem[kOffB2 + (res * 2 + step) * 1024 + swz32(n * 32 + kap)] = (uint8_t)(int8_t)c;
-      continue;
-    }
-    if (b < 14 && (step == 0 || kap < 16)) {
-      const int32_t at = plan->res[res].at[b * RNSW_MAX_N + j];
-      c = res ? red_fast(at * w10, f) : at;  // AT W[1][0]: pass 2 yields y_1 W[1][0]
-      const int shifts = step == 1 ? 2 : (kap >> 4);
-      for (int s = 0; s < shifts; ++s) c = red_fast(c * 256, f);
-    }
-    smem[kOffB2 + (res * 2 + step) * 1024 + swz32(n * 32 + kap)] = (uint8_t)(int8_t)limb_of(c, acc);
-  }
   // the constant 127 in K rows 16..31 of every step-1 A2 operand (see B2)
   for (int idx = tid; idx < 8 * 512; idx += kThr) {
     const int u = idx >> 9, w = idx & 511;  // 512 words = rows 16..31 of buffer u

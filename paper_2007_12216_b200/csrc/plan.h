@@ -47,4 +47,9 @@ struct PlanDevice {
   // (mod m_j), W[j][i] = prod_{k=i}^{j-1} m_k^-1 mod m_j, in [0, m_j).
   int32_t mrc_w[RNSW_MAX_RES][RNSW_MAX_RES];
   ResidueTables res[RNSW_MAX_RES];
+  // Constant B operands of the tcgen05 output transform (output_umma.cu),
+  // built on the host for F(14x14,3x3) plans over two 16-bit residues:
+  // B1[res] (1 KB each) then B2[res][step] (1 KB each), 32-byte rows,
+  // 32B-swizzled s8.
+  alignas(16) uint8_t umma_b[6144];
 };
