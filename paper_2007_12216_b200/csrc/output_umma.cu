@@ -58,6 +58,7 @@ struct UArgs {
   int kblocks;
   int64_t units;       // P * kblocks work units (tile, 32-channel block)
   int32_t negw10;      // -W[1][0] (kept opaque to the compiler: one IMAD per digit)
+  uint32_t mul0;       // ceil(2^32 / m0): quotient estimate of the first digit
   FastDiv div_img, div_tw, div_kb;
 };
 
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(kThr, 2)
   const uint32_t tbase = *tslot;
 
   const int32_t negw10 = args.negw10;
+  const uint32_t mul0 = args.mul0;
   const uint32_t m0 = (uint32_t)fm0.m;
   const uint32_t signed_bound = (uint32_t)plan->signed_bound, dyn_range = (uint32_t)plan->dynamic_range;
   constexpr uint32_t kIdP1 = idesc_i8x(128, 32, false, true, true, false);   // u8 MN-major x s8
@@ -229,13 +231,18 @@ __global__ void __launch_bounds__(kThr, 2)
       for (int b = 0; b < 14; ++b) {
         // mixed-radix digits (rw/residue.py:195-206): d0 = y0 mod m0,
         // d1 = (y1 - d0) m0^-1 mod m1 (the factor rides in B2 of residue 1);
-        // the MMA added the bias, both sums are already non-negative
-        const int32_t d0 = red_pos_biased(h0[b] * 256 + l0[b], fm0);
+        // the MMA added the bias, both sums are already non-negative.
+        // d0 may be any representative in [-m0, m0): its quotient
+        // umulhi(n, ceil(2^32 / m0)) is floor(n / m0) or one more (no shift).
+        // Then x = d0 + m0 d1 in [-m0, D) is still the right value mod D,
+        // and x < 0 is a (small) negative output, folded by the signed test.
+        const int32_t n0 = h0[b] * 256 + l0[b];
+        const int32_t d0 = (int32_t)(__umulhi((uint32_t)n0, mul0) * fm0.negm + (uint32_t)n0);
         const int32_t d1 = red_pos_biased(d0 * negw10 + (h1[b] * 256 + l1[b]), fm1);
         const uint32_t x = (uint32_t)d0 + m0 * (uint32_t)d1;
-        const bool neg = x > signed_bound;
+        const bool neg = x > signed_bound;  // unsigned: also every x < 0
         if constexpr (kMode == 0)
-          qv[b] = (int32_t)(neg ? x - dyn_range : x);
+          qv[b] = (int32_t)((int32_t)x > (int32_t)signed_bound ? x - dyn_range : x);
         else if constexpr (kMode == 1)
           qv[b] = neg ? 0 : min((int32_t)(x >> args.shift), 127);
         else
@@ -352,6 +359,7 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
   a.units = g.P * a.kblocks;
   if (a.units >= (1ll << 31)) return cudaErrorInvalidValue;  // FastDiv range
   a.negw10 = -plan.dev.mrc_w[1][0];
+  a.mul0 = (uint32_t)(((1ull << 32) + plan.dev.res[0].modulus - 1) / plan.dev.res[0].modulus);
   a.div_img = make_fastdiv((uint32_t)(g.th * g.tw));
   a.div_tw = make_fastdiv((uint32_t)g.tw);
   a.div_kb = make_fastdiv((uint32_t)a.kblocks);
