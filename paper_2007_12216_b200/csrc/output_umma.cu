@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThr, 2)
   // 1024-byte aligned, derived from the shared array so stores stay STS
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffOut + ((out_bytes(kMode) + 15) & ~15));
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(kThr, 2)
   if (tid == 0) {
     tma_prefetch_desc(&tm);
     mbar_init(&bar[0], 1);  // Mw8 boxes landed
-    mbar_init(&bar[1], 1);  // MMA batch complete
+    mbar_init(&bar[1], 1);  // MMA batch for warps 0-3 complete
+    mbar_init(&bar[2], 1);  // MMA batch for warps 4-7 complete (implies bar[1]: commits track all prior MMAs)
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<256>(tslot);
@@ -133,16 +134,21 @@ __global__ void __launch_bounds__(kThr, 2)
         tma_load_5d(A1 + (res * 4 + gg) * kOpBytes, &tm, &bar[0], k0, 0, L0 + 2 * res, 4 * gg, p & 127);
   };
   const int64_t u_step = gridDim.x;
+  // each MMA batch is committed in two halves, one per warp group (h), so the
+  // first group starts its epilogue while the second half still runs
   uint32_t ph_tma = 0, ph_mma = 0;
+  uint64_t* my_bar = &bar[1 + h];
   auto issue_p1 = [&]() {  // thread 0: pass 1 into the 256 TMEM columns once the boxes landed
     mbar_wait(&bar[0], ph_tma);
     ph_tma ^= 1;
     tc_fence_after();
 #pragma unroll
-    for (int v = 0; v < 8; ++v)
+    for (int v = 0; v < 8; ++v) {  // v = res * 4 + gg; residue h feeds warp group h
       mma_i8(tbase + v * 32, umma_desc_mn_sw32(smem_u32(A1 + v * kOpBytes), 1024),
              umma_desc_kmajor(smem_u32(smem + kOffB1 + (v >> 2) * 1024), 32), kIdP1, 0u);
-    mma_commit(&bar[1]);
+      if (v == 3) mma_commit(&bar[1]);
+    }
+    mma_commit(&bar[2]);
   };
   if (tid == 0 && (int64_t)blockIdx.x < args.units) {
     issue_load(blockIdx.x);
@@ -152,10 +158,11 @@ __global__ void __launch_bounds__(kThr, 2)
   for (int64_t u = blockIdx.x; u < args.units; u += u_step) {
     const int p = unit_p(u), k0 = (int)(u - (int64_t)p * args.kblocks) * kKB;
     // ---- pass 1 (issued before the previous unit's stores) ----
-    mbar_wait(&bar[1], ph_mma);
+    mbar_wait(my_bar, ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
-    if (tid == 0 && u + u_step < args.units) issue_load(u + u_step);  // A1 is free: overlaps the epilogues
+    // the second group's barrier means all of pass 1 is done: A1 is free
+    if (tid == kThr / 2 && u + u_step < args.units) issue_load(u + u_step);  // lands during the epilogues
 
     // ---- epilogue 1: warp (q, h): columns j = 4 gg + q of residue h, lane = channel ----
     {
@@ -196,16 +203,18 @@ __global__ void __launch_bounds__(kThr, 2)
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {  // v = res * 4 + mb
+      for (int o = 0; o < 8; ++o) {  // channel blocks mb 0, 1 (warps 0-3) first, then mb 2, 3
+        const int v = (o & 2) * 2 + (o >> 2) * 2 + (o & 1);  // v = res * 4 + mb
         const uint8_t* a2 = A2 + v * 2 * kOpBytes;
         const uint8_t* b2 = smem + kOffB2 + (v >> 2) * 2 * 1024;
         mma_i8(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2)), umma_desc_kmajor(smem_u32(b2), 32), kIdP1, 0u);
         mma_i8(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2 + kOpBytes)), umma_desc_kmajor(smem_u32(b2 + 1024), 32),
                kIdP2s, 1u);
+        if (o == 3) mma_commit(&bar[1]);
       }
-      mma_commit(&bar[1]);
+      mma_commit(&bar[2]);
     }
-    mbar_wait(&bar[1], ph_mma);
+    mbar_wait(my_bar, ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
 
