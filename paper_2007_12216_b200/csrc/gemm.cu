@@ -488,12 +488,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
           if (args.planar) {
-            // the two limb planes: rows ((pb * n_res + res) * 2 + limb) * npos + pos) * 128
-#pragma unroll
-            for (int limb = 0; limb < 2; ++limb) {
-              const int row0 = (int)(((((int64_t)pb * args.n_res + res) * 2 + limb) * args.npos + pos) * kBlockM);
-              tma_store_2d(&tmM, stg_b + limb * (kBlockM * BN), kb * BN, row0);
-            }
+            // both limb planes of the tile: slabs (pb * n_res + res) * 2 + {0, 1}
+            tma_store_3d(&tmM, stg_b, kb * BN, pos * kBlockM, (pb * args.n_res + res) * 2);
           } else {
             const int row0 = (int)(((int64_t)pb * args.n_res * args.npos + res * args.npos + pos) * kBlockM);
 #pragma unroll
@@ -535,14 +531,17 @@ bool make_tmap_mw(CUtensorMap* tm, const void* base, int Kp, int64_t rows) {
 }
 
 // Mw8 as a 2-D uint8 array [rows][Kp] (rows = limb-plane rows), box BN x 128.
-bool make_tmap_mw8_store(CUtensorMap* tm, const void* base, int Kp, int64_t rows, int bn) {
+// Mw8 as [slab = (pb * n_res + res) * 2 + limb][pos * 128 + t][Kp]; one box =
+// both limb planes of an output tile (BN x 128 rows x 2), one store per tile.
+bool make_tmap_mw8_store(CUtensorMap* tm, const void* base, int Kp, int64_t rows, int bn, int npos) {
   auto encode = encode_fn();
   if (encode == nullptr) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)Kp};
-  cuuint32_t box[2] = {(cuuint32_t)bn, (cuuint32_t)kBlockM};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+  const int64_t slab_rows = (int64_t)npos * kBlockM;
+  cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)slab_rows, (cuuint64_t)(rows / slab_rows)};
+  cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(slab_rows * Kp)};
+  cuuint32_t box[3] = {(cuuint32_t)bn, (cuuint32_t)kBlockM, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, bn == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                       CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -577,7 +576,7 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   CUtensorMap tmM;
   const int64_t mw_rows = (a.P + kBlockM - 1) / kBlockM * (int64_t)a.n_res * a.npos * kBlockM;
   if (a.planar) {
-    if (!make_tmap_mw8_store(&tmM, a.Mw, a.Kp, mw_rows * 2, BN)) return cudaErrorInvalidValue;
+    if (!make_tmap_mw8_store(&tmM, a.Mw, a.Kp, mw_rows * 2, BN, a.npos)) return cudaErrorInvalidValue;
   } else if (!make_tmap_mw(&tmM, a.Mw, a.Kp, mw_rows)) {
     return cudaErrorInvalidValue;
   }
