@@ -1,5 +1,7 @@
 """Check the tcgen05 output transform (rnsw_output_transform_mw8) on synthetic
-Mw8 input against numpy: Y = AT M AT^T mod m per residue, MRC, crop.
+Mw8 input against numpy: Y = AT M AT^T mod m per residue, MRC, crop; prints
+the mismatch pattern per tile row/column/channel (a debugging aid; the
+pytest version is tests/test_gpu_mw8.py).
 
 usage: python tools/debug_mw8.py [mode]   mode: rand | delta I J | const
 """
@@ -84,46 +86,3 @@ if bad.any():
     print("bad per k", t0.sum(axis=(0, 1)).tolist())
     print("got tile0 k0\n", got[0, :14, :14, 0])
     print("want tile0 k0\n", want[0, :14, :14, 0])
-
-import os
-dump = os.environ.get("RNSW_UMMA_DUMP")
-if dump:
-    raw = np.fromfile(dump, np.uint8)
-    OP = 4096
-    def unswz(buf):
-        out = np.empty_like(buf)
-        for off in range(buf.size):
-            out[off] = buf[off ^ (((off >> 7) & 1) << 4)]
-        return out
-    A1 = raw[:8 * OP]
-    for name, f in (("swz32", unswz), ("plain", lambda b: b)):
-        bad = 0
-        for res in range(2):
-            for gg in range(4):
-                blk = f(A1[(res * 4 + gg) * OP:(res * 4 + gg + 1) * OP]).reshape(4, 2, 16, 32)
-                for jl in range(4):
-                    j = 4 * gg + jl
-                    for L in range(2):
-                        v = (mat[res, 0, np.arange(16) * 16 + j, :] >> (8 * L)) & 255  # (i, k)
-                        want_b = np.zeros((16, 32), np.int64)
-                        want_b[:, :K] = v[:, :K]
-                        bad += int((blk[jl, L] != want_b).sum())
-        print("A1", name, "bad bytes", bad)
-    # D1 z values
-    d1 = raw[24 * OP:].view(np.int32).reshape(2, 16, 32, 16)
-    def sym(v, m):
-        v = v % m
-        return np.where(v > (m - 1) // 2, v - m, v)
-    zbad = 0
-    for res, m in enumerate(mods):
-        AT = mts[res].at.astype(np.int64)
-        ATp = sym(AT * 256, m)
-        M = mat[res, 0].reshape(16, 16, K)
-        hi, lo = M >> 8, M & 255
-        z = np.einsum("ai,ijk->jka", ATp, hi) + np.einsum("ai,ijk->jka", AT, lo)  # (j, k, a)
-        got_z = d1[res][:, :K, :14]
-        zbad += int((got_z != z).sum())
-        if res == 0 and (got_z != z).any():
-            w = np.argwhere(got_z != z)
-            print("z first bad (j,k,a)", w[:8].tolist(), got_z[tuple(w[0])], z[tuple(w[0])])
-    print("D1 z bad", zbad)
