@@ -691,8 +691,10 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   bool all16 = true;
   for (int r = 0; r < d.n_res; ++r) all16 = all16 && d.res[r].planes == 2;
   static const bool no_mc = getenv("RNSW_GEMM_NO_MC") != nullptr;  // A/B switch
-  if (maxpl == 2 && all16 && a.num_pb >= 2 && !no_mc) {
-    // CTA pairs over (pb, pb+1) with the filter planes multicast (see the kernel)
+  if (maxpl == 2 && all16 && a.num_pb >= 4 && !no_mc) {
+    // CTA pairs over (pb, pb+1) with the filter planes multicast (see the kernel);
+    // with only 2-3 tile blocks the pair's lockstep costs more than the shared
+    // filter bytes save (VGG16 conv5 at batch 256: -10% without pairs)
     const int num_pbu = (a.num_pb + 1) / 2;
     a.total_tiles = (int64_t)d.n_res * a.npos * num_pbu * a.num_kb;
     a.div_pb = make_fastdiv((uint32_t)num_pbu);
