@@ -22,7 +22,8 @@ namespace {
 // kPL == 1: symmetric residues (the s8 fragments of the output transform).
 // kPlanar (16-bit only): write Mw8, the two byte planes the tcgen05 output
 // transform reads (kernels.h mw8_offset).
-template <int kPL, bool kPlanar = false>
+// kC3: C == 3 (VGG16 conv1_1), the zero fourth channel is skipped.
+template <int kPL, bool kPlanar = false, bool kC3 = false>
 __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* __restrict__ plan, int P, int K,
                                                              int Kp, int Cp, const int16_t* __restrict__ V16,
                                                              const int8_t* __restrict__ U, int16_t* __restrict__ Mw,
@@ -60,14 +61,16 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
   const int p_begin = blockIdx.z * tiles_per_cta, p_end = min(P, p_begin + tiles_per_cta);
   const uint2* src = reinterpret_cast<const uint2*>(V16) + ((int64_t)r * P + p_begin) * npos + pos;
   const int rp = r * npos + pos, nrp = nres * npos;
-  // V16 rows of 4 tiles are loaded together ahead of their products
-  for (int p0 = p_begin; p0 < p_end; p0 += 4) {
-    uint2 wv[4];
+  // V16 rows of 8 tiles are loaded together ahead of their products
+  constexpr int kAhead = 8;
+  uint8_t* out8 = nullptr;  // Mw8 row of the current tile (advances by Kp within a block of 128 tiles)
+  for (int p0 = p_begin; p0 < p_end; p0 += kAhead) {
+    uint2 wv[kAhead];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < kAhead; ++i)
       wv[i] = p0 + i < p_end ? __ldg(src + (int64_t)(p0 - p_begin + i) * npos) : make_uint2(0, 0);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kAhead; ++i) {
       const int p = p0 + i;
       if (p >= p_end) break;
       const uint2 w = wv[i];
@@ -82,14 +85,20 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
         for (int e = 0; e < 2; ++e) {
           const int kk = 2 * h + e;
           // |sum| <= 4 h^2 < 2^28 for m < 4500
-          const int32_t n = bias + v0 * u[kk][0] + v1 * u[kk][1] + v2 * u[kk][2] + v3 * u[kk][3];
+          const int32_t n =
+              kC3 ? bias + v0 * u[kk][0] + v1 * u[kk][1] + v2 * u[kk][2]
+                  : bias + v0 * u[kk][0] + v1 * u[kk][1] + v2 * u[kk][2] + v3 * u[kk][3];
           y[e] = kPL == 2 ? red_pos_biased(n, fm) : red_pos_biased(n, fm) - fm.h;
           yv[kk] = y[e];
         }
         o[h] = __byte_perm((uint32_t)y[0], (uint32_t)y[1], 0x5410);
       }
       if constexpr (kPlanar) {
-        uint8_t* base = reinterpret_cast<uint8_t*>(Mw) + mw8_offset(p, r, 0, pos, nres, npos, Kp) + 8 * kg;
+        if (p == p_begin || (p & 127) == 0)
+          out8 = reinterpret_cast<uint8_t*>(Mw) + mw8_offset(p, r, 0, pos, nres, npos, Kp) + 8 * kg;
+        else
+          out8 += Kp;
+        uint8_t* base = out8;
         const uint32_t a0 = __byte_perm((uint32_t)yv[0], (uint32_t)yv[1], 0x5140);
         const uint32_t a1 = __byte_perm((uint32_t)yv[2], (uint32_t)yv[3], 0x5140);
         const uint32_t a2 = __byte_perm((uint32_t)yv[4], (uint32_t)yv[5], 0x5140);
@@ -122,7 +131,9 @@ cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const
   const int64_t per_tile = (int64_t)bx * d.n_res;
   const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, g.P * per_tile / (148 * 4)));
   dim3 grid(bx, d.n_res, (unsigned)((g.P + tpc - 1) / tpc));
-  if (d.res[0].planes == 2 && planar)
+  if (d.res[0].planes == 2 && planar && g.C == 3)
+    smallc_product_kernel<2, true, true><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+  else if (d.res[0].planes == 2 && planar)
     smallc_product_kernel<2, true><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
   else if (d.res[0].planes == 2)
     smallc_product_kernel<2><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
