@@ -106,7 +106,10 @@ namespace {
 // B1[res] rows n = (acc, a) x K slots (limb, i) hold the balanced limbs of
 // AT (limb 0) and 256 AT mod m (limb 1); B2[res][0] rows (acc, b) x (z0 | z1, j)
 // the limbs of ATW and 256 ATW, B2[res][1] (z2, j) those of 65536 ATW, then
-// 16 bias slots whose 127-weighted sum is 127 X, X = m ceil(320000 / m).
+// 16 bias slots whose 127-weighted sum is 127 X, X = m ceil(360000 / m): for
+// every m < 4500 it exceeds the most negative pass-2 input (pass-2 sum
+// >= -16 h (255 + 255 + 128) > -2.3e7, digit term d0 W[1][0] > -m0 m1 > -2.03e7)
+// and keeps the largest below 2^30.
 // ATW = AT W[1][0] for residue 1 (the mixed-radix factor), AT for residue 0.
 void build_umma_b(PlanDevice& d) {
   auto sym = [](int64_t v, int64_t m) {
@@ -134,7 +137,7 @@ void build_umma_b(PlanDevice& d) {
           const int acc = n >> 4, b = n & 15, j = kap & 15;
           int8_t v = 0;
           if (step == 1 && kap >= 16) {
-            const int64_t X = m * ((320000 + m - 1) / m);
+            const int64_t X = m * ((360000 + m - 1) / m);
             const int64_t S = acc == 0 ? (X >> 8) : (X & 255), sl = kap - 16;
             v = (int8_t)(S / 16 + (sl < S % 16 ? 1 : 0));
           } else if (b < 14 && (step == 0 || kap < 16)) {

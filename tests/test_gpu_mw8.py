@@ -136,3 +136,27 @@ def test_mw8_unsupported_plans_refuse():
     rc = l.rnsw_output_transform_mw8(plan8.handle, _native.c_void_p(16), 1, 8, 8, 16, 1, 0, _native.c_void_p(16),
                                      None)
     assert rc != 0 and b"Mw8" in l.rnsw_last_error()
+
+
+def test_mw8_moduli_near_the_fast_limit():
+    """RNS(4493, 4489) at F(14,3): the largest 16-bit moduli the tcgen05 output
+    transform takes (m < 4500), where its bias and limb bounds are tightest;
+    extreme and random int8 operands against direct conv and the oracle."""
+    import paper_2007_12216_b200 as rnsw
+    from oracle import ref_port
+    from paper_2007_12216_b200 import _native
+    from paper_2007_12216_b200.layer import plan_for
+
+    system = rnsw.RnsSystem((4493, 4489))
+    plan = plan_for(rnsw.cached_transforms(14, 3), system)
+    assert _native.lib().rnsw_mw8_supported(plan.handle) == 1
+    spec = rnsw.LayerSpec(h=30, w=30, c=64, k=32, r=3, padding=1, tile_m=14)
+    rng = np.random.default_rng(4493)
+    cases = [(rng.integers(-128, 128, spec.input_shape()), rng.integers(-127, 128, spec.weight_shape())),
+             (np.full(spec.input_shape(), -128), np.full(spec.weight_shape(), 127)),
+             (np.full(spec.input_shape(), 127), np.where(rng.random(spec.weight_shape()) < 0.5, -127, 127))]
+    for x, w in cases:
+        x, w = x.astype(np.int8), w.astype(np.int8)
+        got = rnsw.winograd_layer_conv(spec, w, x, system)
+        assert np.array_equal(got, oracle.direct_conv_c(x, w, 1))
+    assert np.array_equal(got, ref_port.winograd_layer(x, w, 1, 14, system.moduli))
