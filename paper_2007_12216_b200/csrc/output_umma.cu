@@ -62,12 +62,6 @@ struct UArgs {
   FastDiv div_img, div_tw, div_kb;
 };
 
-// Balanced limb of a symmetric residue c: hi = (c + 128) >> 8, lo = c - 256 hi.
-RNSW_DEV int32_t limb_of(int32_t c, int acc) {
-  const int32_t hi = limb_hi(c);
-  return acc == 0 ? hi : c - 256 * hi;
-}
-
 // Persistent: two CTAs per SM (each 256 TMEM columns, shared by the pass-1
 // and pass-2 accumulators) walk the work units u = (tile p, channel block
 // kb); while one CTA waits for its MMAs the other runs its epilogues.  The
