@@ -122,10 +122,8 @@ __global__ void __launch_bounds__(kThr, 2)
     mbar_arrive_expect_tx(&bar[0], 8 * kOpBytes);
     const int L0 = (p >> 7) * 4;  // (pb * n_res + res) * 2 + limb, n_res = 2
 #pragma unroll
-    for (int res = 0; res < 2; ++res)
-#pragma unroll
-      for (int gg = 0; gg < 4; ++gg)
-        tma_load_5d(A1 + (res * 4 + gg) * kOpBytes, &tm, &bar[0], k0, 0, L0 + 2 * res, 4 * gg, p & 127);
+    for (int res = 0; res < 2; ++res)  // one box per residue: all 16 columns j (4 KB per column group)
+      tma_load_5d(A1 + res * 4 * kOpBytes, &tm, &bar[0], k0, 0, L0 + 2 * res, 0, p & 127);
   };
   const int64_t u_step = gridDim.x;
   // each MMA batch is committed in two halves, one per warp group (h), so the
@@ -331,7 +329,7 @@ bool make_tmap_mw8(CUtensorMap* tm, const void* base, int Kp, int64_t num_pb, in
   cuuint64_t dims[5] = {(cuuint64_t)Kp, 16, (cuuint64_t)(num_pb * nres * 2), 16, 128};
   cuuint64_t strides[4] = {(cuuint64_t)Kp * 128 * 16, (cuuint64_t)Kp * 128 * 256, (cuuint64_t)Kp * 128,
                            (cuuint64_t)Kp};
-  cuuint32_t box[5] = {32, 16, 2, 4, 1};
+  cuuint32_t box[5] = {32, 16, 2, 16, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(base), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
