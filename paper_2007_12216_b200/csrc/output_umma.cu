@@ -130,20 +130,21 @@ __global__ void __launch_bounds__(kThr, 2)
   // first group starts its epilogue while the second half still runs
   uint32_t ph_tma = 0, ph_mma = 0;
   uint64_t* my_bar = &bar[1 + h];
-  auto issue_p1 = [&]() {  // thread 0: pass 1 into the 256 TMEM columns once the boxes landed
+  auto issue_p1 = [&]() {  // warp 0: pass 1 into the 256 TMEM columns once the boxes landed
     mbar_wait(&bar[0], ph_tma);
     ph_tma ^= 1;
     tc_fence_after();
 #pragma unroll
     for (int v = 0; v < 8; ++v) {  // v = res * 4 + gg; residue h feeds warp group h
-      mma_i8(tbase + v * 32, umma_desc_mn_sw32(smem_u32(A1 + v * kOpBytes), 1024),
-             umma_desc_kmajor(smem_u32(smem + kOffB1 + (v >> 2) * 1024), 32), kIdP1, 0u);
-      if (v == 3) mma_commit(&bar[1]);
+      mma_i8_warp(tbase + v * 32, umma_desc_mn_sw32(smem_u32(A1 + v * kOpBytes), 1024),
+                  umma_desc_kmajor(smem_u32(smem + kOffB1 + (v >> 2) * 1024), 32), kIdP1, 0u);
+      if (v == 3) mma_commit_warp(&bar[1]);
     }
-    mma_commit(&bar[2]);
+    mma_commit_warp(&bar[2]);
   };
-  if (tid == 0 && (int64_t)blockIdx.x < args.units) {
-    issue_load(blockIdx.x);
+  if (warp == 0 && (int64_t)blockIdx.x < args.units) {
+    if (lane == 0) issue_load(blockIdx.x);
+    __syncwarp();
     issue_p1();
   }
 
@@ -192,19 +193,20 @@ __global__ void __launch_bounds__(kThr, 2)
     __syncthreads();
 
     // ---- pass 2 into the same columns (pass 1 has been read) ----
-    if (tid == 0) {
+    if (warp == 0) {
       tc_fence_after();
 #pragma unroll
       for (int o = 0; o < 8; ++o) {  // channel blocks mb 0, 1 (warps 0-3) first, then mb 2, 3
         const int v = (o & 2) * 2 + (o >> 2) * 2 + (o & 1);  // v = res * 4 + mb
         const uint8_t* a2 = A2 + v * 2 * kOpBytes;
         const uint8_t* b2 = smem + kOffB2 + (v >> 2) * 2 * 1024;
-        mma_i8(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2)), umma_desc_kmajor(smem_u32(b2), 32), kIdP1, 0u);
-        mma_i8(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2 + kOpBytes)), umma_desc_kmajor(smem_u32(b2 + 1024), 32),
-               kIdP2s, 1u);
-        if (o == 3) mma_commit(&bar[1]);
+        mma_i8_warp(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2)), umma_desc_kmajor(smem_u32(b2), 32), kIdP1,
+                    0u);
+        mma_i8_warp(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2 + kOpBytes)),
+                    umma_desc_kmajor(smem_u32(b2 + 1024), 32), kIdP2s, 1u);
+        if (o == 3) mma_commit_warp(&bar[1]);
       }
-      mma_commit(&bar[2]);
+      mma_commit_warp(&bar[2]);
     }
     mbar_wait(my_bar, ph_mma);
     ph_mma ^= 1;
@@ -273,7 +275,7 @@ __global__ void __launch_bounds__(kThr, 2)
     }
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
-    if (tid == 0 && u + u_step < args.units) {
+    if (warp == 0 && u + u_step < args.units) {
       tc_fence_after();
       issue_p1();  // the next unit's pass 1 overlaps these stores
     }
