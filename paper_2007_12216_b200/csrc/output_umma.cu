@@ -161,14 +161,10 @@ __global__ void __launch_bounds__(kThr, 2)
     {
       uint8_t* a2 = A2 + (h * 4 + (lane >> 3)) * 2 * kOpBytes;
       const uint32_t chunk = (uint32_t)(lane & 7) << 4;
-#pragma unroll 1
-      for (int gg = 0; gg < 4; ++gg) {
+      // column group gg: z -> three byte limbs -> A2 (the TMEM loads of the
+      // next group are in flight meanwhile: two register sets, one wait each)
+      auto body = [&](int gg, const int32_t (&hi)[16], const int32_t (&lo)[16]) {
         const int j = 4 * gg + q;
-        int32_t hi[16], lo[16];
-        const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + (h * 4 + gg) * 32;
-        tmem_ld16(ta, hi);
-        tmem_ld16(ta + 16, lo);
-        tmem_ld_wait();
         int32_t z[16];
 #pragma unroll
         for (int a = 0; a < 14; ++a) z[a] = hi[a] * 256 + lo[a];
@@ -186,7 +182,25 @@ __global__ void __launch_bounds__(kThr, 2)
         *reinterpret_cast<uint4*>(a2 + swz128(j * 128 + chunk)) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
         *reinterpret_cast<uint4*>(a2 + swz128((16 + j) * 128 + chunk)) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
         *reinterpret_cast<uint4*>(a2 + kOpBytes + swz128(j * 128 + chunk)) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
-      }
+      };
+      const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + h * 4 * 32;
+      int32_t hA[16], lA[16], hB[16], lB[16];
+      tmem_ld16(ta, hA);
+      tmem_ld16(ta + 16, lA);
+      tmem_ld_wait();
+      tmem_ld16(ta + 32, hB);
+      tmem_ld16(ta + 48, lB);
+      body(0, hA, lA);
+      tmem_ld_wait();
+      tmem_ld16(ta + 64, hA);
+      tmem_ld16(ta + 80, lA);
+      body(1, hB, lB);
+      tmem_ld_wait();
+      tmem_ld16(ta + 96, hB);
+      tmem_ld16(ta + 112, lB);
+      body(2, hA, lA);
+      tmem_ld_wait();
+      body(3, hB, lB);
     }
     fence_proxy_async();
     tc_fence_before();
