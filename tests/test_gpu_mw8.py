@@ -81,7 +81,8 @@ def test_output_transform_mw8_against_numpy(B, H, W, K, layout):
     assert np.array_equal(got, _expected(rnsw, ts, system, mat, B, H, W, K))
 
 
-@pytest.mark.parametrize("c,k,h,pool,shift", [(3, 64, 30, 1, 9), (32, 48, 28, 0, 8), (64, 96, 20, 1, 10)])
+@pytest.mark.parametrize("c,k,h,pool,shift", [(3, 64, 30, 1, 9), (32, 48, 28, 0, 8), (64, 96, 20, 1, 10),
+                                             (16, 20, 30, 0, 7), (16, 36, 18, 1, 8)])
 def test_mw8_stage_chain_equals_layer_and_oracle(c, k, h, pool, shift):
     import torch
     from paper_2007_12216_b200 import _native
