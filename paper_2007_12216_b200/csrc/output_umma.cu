@@ -45,10 +45,9 @@ constexpr int kOffA2 = kOffA1 + 8 * kOpBytes;     // [res][mb][step]  16 x 4 KB
 constexpr int kOffB1 = kOffA2 + 16 * kOpBytes;    // [res]             2 x 1 KB
 constexpr int kOffB2 = kOffB1 + 2 * 1024;         // [res][step]       4 x 1 KB
 constexpr int kOffOut = kOffB2 + 4 * 1024;        // output staging
-constexpr int kPixB = 36;   // staged bytes per pixel, pooled mode (9 words: conflict-free)
-constexpr int kPixB1 = 40;  // ... unpooled mode (8-byte aligned rows for 8-byte stores; 2-way conflicts)
+constexpr int kPixB = 40;   // staged bytes per pixel, int8 modes (8-byte aligned rows for 8-byte stores)
 constexpr int kPixW = 33;   // staged words per pixel (int32 mode)
-constexpr int out_bytes(int mode) { return mode == 0 ? 196 * kPixW * 4 : (mode == 1 ? 196 * kPixB1 : 49 * kPixB); }
+constexpr int out_bytes(int mode) { return mode == 0 ? 196 * kPixW * 4 : (mode == 1 ? 196 * kPixB : 49 * kPixB); }
 constexpr int smem_bytes(int mode) { return 1024 + kOffOut + ((out_bytes(mode) + 15) & ~15) + 64; }
 
 struct UArgs {
@@ -277,7 +276,7 @@ __global__ void __launch_bounds__(kThr, 2)
       } else if constexpr (kMode == 1) {
         if (a < 14) {
 #pragma unroll
-          for (int b = 0; b < 14; ++b) smem[kOffOut + (a * 14 + b) * kPixB1 + kl] = (uint8_t)qv[b];
+          for (int b = 0; b < 14; ++b) smem[kOffOut + (a * 14 + b) * kPixB + kl] = (uint8_t)qv[b];
         }
       } else {
         int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
@@ -313,24 +312,25 @@ __global__ void __launch_bounds__(kThr, 2)
             args.y[(((int64_t)b_img * g.K + k0 + c) * g.Ho + ho) * g.Wo + wo] = ys[px * kPixW + c];
         }
       }
-    } else if (kMode == 1 && (g.K & 7) == 0) {
-      // unpooled: 8-byte words (K % 8 == 0)
-      for (int idx = tid; idx < 196 * (kKB / 8); idx += kThr) {
-        const int wq = idx & 3, px = idx >> 2, a = px / 14, b = px - a * 14;
-        const int ho = ti * 14 + a, wo = tj * 14 + b;
-        if (ho >= g.Ho || wo >= g.Wo || k0 + 8 * wq >= g.K) continue;
-        const uint2 word = *reinterpret_cast<const uint2*>(smem + kOffOut + px * kPixB1 + 8 * wq);
-        *reinterpret_cast<uint2*>(args.out8 + (((int64_t)b_img * g.Ho + ho) * g.Wo + wo) * g.K + k0 + 8 * wq) = word;
+    } else if ((g.K & 7) == 0) {
+      // 8-byte words (K % 8 == 0)
+      constexpr int side = kMode == 3 ? 7 : 14;
+      const int Ho = kMode == 3 ? g.Ho / 2 : g.Ho, Wo = kMode == 3 ? g.Wo / 2 : g.Wo;
+      for (int idx = tid; idx < side * side * (kKB / 8); idx += kThr) {
+        const int wq = idx & 3, px = idx >> 2, a = px / side, b = px - a * side;
+        const int ho = ti * side + a, wo = tj * side + b;
+        if (ho >= Ho || wo >= Wo || k0 + 8 * wq >= g.K) continue;
+        const uint2 word = *reinterpret_cast<const uint2*>(smem + kOffOut + px * kPixB + 8 * wq);
+        *reinterpret_cast<uint2*>(args.out8 + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 8 * wq) = word;
       }
     } else {
       constexpr int side = kMode == 3 ? 7 : 14;
-      constexpr int pixb = kMode == 3 ? kPixB : kPixB1;
       const int Ho = kMode == 3 ? g.Ho / 2 : g.Ho, Wo = kMode == 3 ? g.Wo / 2 : g.Wo;
       for (int idx = tid; idx < side * side * (kKB / 4); idx += kThr) {
         const int wq = idx & 7, px = idx >> 3, a = px / side, b = px - a * side;
         const int ho = ti * side + a, wo = tj * side + b;
         if (ho >= Ho || wo >= Wo || k0 + 4 * wq >= g.K) continue;
-        const uint32_t word = *reinterpret_cast<const uint32_t*>(smem + kOffOut + px * pixb + 4 * wq);
+        const uint32_t word = *reinterpret_cast<const uint32_t*>(smem + kOffOut + px * kPixB + 4 * wq);
         *reinterpret_cast<uint32_t*>(args.out8 + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 4 * wq) = word;
       }
     }
