@@ -45,7 +45,7 @@ constexpr int kOffA2 = kOffA1 + 8 * kOpBytes;     // [res][mb][step]  16 x 4 KB
 constexpr int kOffB1 = kOffA2 + 16 * kOpBytes;    // [res]             2 x 1 KB
 constexpr int kOffB2 = kOffB1 + 2 * 1024;         // [res][step]       4 x 1 KB
 constexpr int kOffOut = kOffB2 + 4 * 1024;        // output staging
-constexpr int kPixB = 40;   // staged bytes per pixel, int8 modes (8-byte aligned rows for 8-byte stores)
+constexpr int kPixB = 48;   // staged bytes per pixel, int8 modes (16-byte aligned rows for 16-byte stores)
 constexpr int kPixW = 33;   // staged words per pixel (int32 mode)
 constexpr int out_bytes(int mode) { return mode == 0 ? 196 * kPixW * 4 : (mode == 1 ? 196 * kPixB : 49 * kPixB); }
 constexpr int smem_bytes(int mode) { return 1024 + kOffOut + ((out_bytes(mode) + 15) & ~15) + 64; }
@@ -312,16 +312,16 @@ __global__ void __launch_bounds__(kThr, 2)
             args.y[(((int64_t)b_img * g.K + k0 + c) * g.Ho + ho) * g.Wo + wo] = ys[px * kPixW + c];
         }
       }
-    } else if ((g.K & 7) == 0) {
-      // 8-byte words (K % 8 == 0)
+    } else if ((g.K & 15) == 0) {
+      // 16-byte words (K % 16 == 0)
       constexpr int side = kMode == 3 ? 7 : 14;
       const int Ho = kMode == 3 ? g.Ho / 2 : g.Ho, Wo = kMode == 3 ? g.Wo / 2 : g.Wo;
-      for (int idx = tid; idx < side * side * (kKB / 8); idx += kThr) {
-        const int wq = idx & 3, px = idx >> 2, a = px / side, b = px - a * side;
+      for (int idx = tid; idx < side * side * (kKB / 16); idx += kThr) {
+        const int wq = idx & 1, px = idx >> 1, a = px / side, b = px - a * side;
         const int ho = ti * side + a, wo = tj * side + b;
-        if (ho >= Ho || wo >= Wo || k0 + 8 * wq >= g.K) continue;
-        const uint2 word = *reinterpret_cast<const uint2*>(smem + kOffOut + px * kPixB + 8 * wq);
-        *reinterpret_cast<uint2*>(args.out8 + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 8 * wq) = word;
+        if (ho >= Ho || wo >= Wo || k0 + 16 * wq >= g.K) continue;
+        const uint4 word = *reinterpret_cast<const uint4*>(smem + kOffOut + px * kPixB + 16 * wq);
+        *reinterpret_cast<uint4*>(args.out8 + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 16 * wq) = word;
       }
     } else {
       constexpr int side = kMode == 3 ? 7 : 14;
