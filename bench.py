@@ -4,19 +4,21 @@
 Workload (BASELINE.json config 4; config 2 at --batch 1): the 13 3x3 conv
 layers of VGG16 on 224x224x3 int8 images, every layer an exact int32
 RNS-Winograd convolution F(14x14,3x3) over RNS(4001,4331) plus the device
-glue (relu, >> shift, clip, 2x2 max-pool).  Weak scaling: each rank (one
-process per GPU) serves its own shard of --batch images (default 256), so the
-global batch is 256 x N; the only collective is one all-gather of the final
-(B,7,7,512) int8 maps.
+glue (relu, >> shift, clip, 2x2 max-pool).  Strong scaling by default: the
+256-image batch of config 4 is split over the N ranks (one process per GPU,
+256/N images each); ``--weak`` gives every rank --batch images instead.  The
+only collective is one all-gather of the final (B,7,7,512) int8 maps.
 
 Metric: direct-conv-equivalent INT8 TOPS = sum over layers of
 2*B*Ho*Wo*C*K*9 divided by the stack latency (whole job, all ranks).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--weak] [--impl reference]
 
-One JSON line on rank 0.  ``--impl reference`` times the CPU reference arm:
-the numpy restatement of the reference's winograd_layer_conv
-(oracle/ref_port.py), on the host cores, one image per worker process.
+With --gpus N > 1 and no torchrun environment, bench.py launches itself
+under torch.distributed.run with N ranks (NCCL, 127.0.0.1).  One JSON line on
+rank 0.  ``--impl reference`` times the CPU reference arm: the numpy
+restatement of the reference's winograd_layer_conv (oracle/ref_port.py), on
+the host cores, one image per worker process.
 """
 
 from __future__ import annotations
@@ -44,7 +46,10 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=256,
-                    help="images per GPU (weak scaling: the global batch is batch x N, one shard per rank)")
+                    help="global batch (strong scaling, split over the ranks); with --weak, images per GPU")
+    ap.add_argument("--weak", action="store_true", help="weak scaling: every rank serves --batch images")
+    ap.add_argument("--no-layer-configs", action="store_true",
+                    help="skip the per-layer latency lines of BASELINE configs 1, 3 and 5")
     ap.add_argument("--impl", default="rnsw", choices=["rnsw", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-images", type=int, default=1)
@@ -147,7 +152,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (seeded PCG64, rw/cli.py:82-94 convention)",
         "config": {"workload": "VGG16 13x conv3x3 stack, 224x224x3, F(14x14,3x3), RNS(4001,4331), CPU sample",
                    "images_per_step": procs},
@@ -236,13 +241,95 @@ def measure_int8_peak(torch):
 
 def load_traffic():
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture (profiles/*traffic*.json), if one matches this build."""
+    capture (profiles/*traffic*.json): an EARLIER capture of this build's
+    kernels (ncu cannot run inside the timed bench), labelled as such."""
     for p in sorted((ROOT / "profiles").glob("*traffic*.json"), reverse=True):
         try:
-            return json.loads(p.read_text())
+            return json.loads(p.read_text()), str(p.relative_to(ROOT))
         except (OSError, ValueError):
             continue
-    return {}
+    return {}, None
+
+
+def layer_config_latencies(torch, reps: int = 10):
+    """BASELINE configs 1, 3 and 5 as single layers through the reference
+    entry point winograd_layer_conv (filters precomputed, as rw/cli.py:458-472
+    does): device latency with resident torch tensors (CUDA events, best of
+    `reps`), end-to-end latency with numpy host buffers in and out (the H2D
+    copy, the kernels and the D2H copy, wall clock, best of `reps`), and the
+    device tcgen05 direct conv beside it.  Returns {name: {...}}."""
+    import numpy as np
+
+    import paper_2007_12216_b200 as rnsw
+    from paper_2007_12216_b200 import workloads as W
+
+    cases = []
+    c1, w1, x1 = W.config1()
+    cases.append((c1, w1, x1))
+    c3, w3, x3 = W.config3()
+    cases.append((c3, w3, x3))
+    w5, x5 = W.config5_operands()
+    for c5 in W.config5_cases():
+        cases.append((c5, w5, x5))
+    out = {}
+    direct_done = {}
+    for case, w, x in cases:
+        spec = rnsw.LayerSpec(h=case.h, w=case.w, c=case.c, k=case.k, r=case.r, padding=case.pad,
+                              batch=case.batch, tile_m=case.tile_m)
+        system = rnsw.RnsSystem(case.moduli)
+        mts = rnsw.reduce_for_system(rnsw.cached_transforms(case.tile_m, case.r), system)
+        bank = rnsw.precompute_filter_transforms(w, mts)
+        xd = torch.from_numpy(x).cuda()
+        wd = torch.from_numpy(w).cuda()
+
+        def dev_call():
+            return rnsw.winograd_layer_conv(spec, wd, xd, system, declared_bound=case.declared_bound, filters=bank)
+
+        for _ in range(3):
+            dev_call()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dev_call()
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        host_best = float("inf")
+        for _ in range(max(3, reps // 2)):
+            t0 = time.perf_counter()
+            y = rnsw.winograd_layer_conv(spec, w, x, system, declared_bound=case.declared_bound, filters=bank)
+            host_best = min(host_best, time.perf_counter() - t0)
+        assert isinstance(y, np.ndarray) and y.dtype == np.int32
+        rec = {"ms": round(best, 4), "TOPS": round(case.direct_ops() / (best * 1e-3) / 1e12, 2),
+               "e2e_host_ms": round(host_best * 1e3, 4),
+               "tile": f"F({case.tile_m}x{case.tile_m},{case.r}x{case.r})", "moduli": list(case.moduli)}
+        dkey = (case.batch, case.h, case.c, case.k, case.r)
+        if dkey not in direct_done:
+            packed = rnsw.DirectWeights(wd)
+            for _ in range(3):
+                rnsw.direct_conv(spec, wd, xd, packed)
+            torch.cuda.synchronize()
+            dbest = float("inf")
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                rnsw.direct_conv(spec, wd, xd, packed)
+                e1.record()
+                e1.synchronize()
+                dbest = min(dbest, e0.elapsed_time(e1))
+            direct_done[dkey] = round(dbest, 4)
+        rec["direct_tcgen05_ms"] = direct_done[dkey]
+        out[case.name] = rec
+    return out
+
+
+def _roofline_bound(ops: float, nbytes: float, tensor_peak_tops: float, hbm_gbs: float) -> str:
+    """Which roof binds a kernel: its arithmetic intensity (int8 ops per
+    algorithmic DRAM byte) against the ridge point of the two peaks."""
+    ridge = tensor_peak_tops * 1e12 / (hbm_gbs * 1e9)
+    return "tensor" if nbytes > 0 and ops / nbytes > ridge else "hbm"
 
 
 def run_gpu_arm(args):
@@ -250,7 +337,7 @@ def run_gpu_arm(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2007_12216_b200 import parallel
+    from paper_2007_12216_b200 import _native, parallel
     from paper_2007_12216_b200 import workloads as W
     from paper_2007_12216_b200.vgg import VGG16Rns
 
@@ -258,9 +345,10 @@ def run_gpu_arm(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # weak scaling: every rank serves its own shard of `batch` images (global
-    # batch = batch x N); the ranks meet once, in the final all-gather
-    global_batch = args.batch * world
+    # strong scaling (default): config 4's batch is split over the ranks;
+    # weak: every rank serves its own --batch images.  The ranks meet once,
+    # in the final all-gather.
+    global_batch = args.batch * world if args.weak else args.batch
     start, shard = parallel.shard_range(global_batch, world, rank)
     net = VGG16Rns()
     x_host = W.vgg16_images(shard, start=start)
@@ -272,7 +360,7 @@ def run_gpu_arm(args):
     fwd = net.forward if args.unfused else net.forward_fused
     if not args.unfused and not args.no_graph:
         # one CUDA graph per step (the same kernels, launched by the driver
-        # instead of 39 ctypes calls); the e2e pass copies host input into it
+        # instead of 39 ctypes calls); capture does two eager passes first
         fwd = net.graph(x_dev)
     fwd_staged = net.forward_staged if args.unfused else net.forward_fused_staged
 
@@ -286,25 +374,15 @@ def run_gpu_arm(args):
             dist.barrier()
 
     # clocks are sampled from before the warm-up (nvidia-smi needs ~0.5 s to
-    # produce its first sample) until the timed region ends; every sample is
-    # taken with the GPU under this workload's load
+    # produce its first sample) until the timed region ends
     gpu_index = local
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
         gpu_index = vis.split(",")[local]
     with ClockSampler(gpu_index) as clocks:
-        t_warm = time.time()
-        n_warm = 0
-        while True:
-            for _ in range(args.warmup):
-                step(x_dev)
-            n_warm += args.warmup
-            torch.cuda.synchronize()
-            flag = torch.tensor([1.0 if time.time() - t_warm > 1.0 else 0.0], device="cuda")
-            if world > 1:
-                dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if flag.item() > 0:
-                break
+        for _ in range(args.warmup):  # exactly W untimed warm-up steps
+            step(x_dev)
+        torch.cuda.synchronize()
         barrier()
         # -------- timed region: K steps, inputs resident in HBM --------
         torch.cuda.synchronize()
@@ -374,46 +452,58 @@ def run_gpu_arm(args):
             dist.destroy_process_group()
         return
 
-    import json as _json
-
-    peaks = _json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    work_key = {"gemm": "gemm_ops", "input_transform": "input_transform_bytes", "product": "product_bytes",
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)"
+    work_key = {"gemm": "gemm_bytes", "input_transform": "input_transform_bytes", "product": "product_bytes",
                 "output_transform": "output_transform_bytes", "glue": "glue_bytes"}
 
-    def kind_work(kind):
+    def kind_work(kind, key=None):
         # algorithmic work of the layers that ran this kind of kernel
-        return sum(work[i][work_key[kind]] for i, v in per_layer.items() if kind in v)
+        key = key or work_key[kind]
+        return sum(work[i][key] for i, v in per_layer.items() if kind in v)
 
-    if dominant == "gemm":
-        int8_peak = measure_int8_peak(torch)
-        achieved = kind_work("gemm") / per_kind["gemm"] / 1e12
-        roof = {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(int8_peak, 1), "unit": "TFLOP/s",
-                "peak_source": "measured this run: torch._int_mm int8 8192^3 burst"}
+    int8_peak = measure_int8_peak(torch)
+    dom_bytes = kind_work(dominant)
+    dom_ops = kind_work(dominant, "gemm_ops") if dominant == "gemm" else 0
+    bound = _roofline_bound(dom_ops, dom_bytes, int8_peak, hbm_peak)
+    if bound == "tensor":
+        roof = {"bound": "tensor", "achieved": round(dom_ops / per_kind[dominant] / 1e12, 3),
+                "peak": round(int8_peak, 1), "unit": "TFLOP/s",
+                "peak_source": "measured this run: torch._int_mm int8 8192^3 burst (MEASURED_PEAKS.json has no int8)"}
     else:
-        achieved = kind_work(dominant) / per_kind[dominant] / 1e9
-        peak = peaks.get("hbm_gbs", 6650.0)
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
+        roof = {"bound": "hbm", "achieved": round(dom_bytes / per_kind[dominant] / 1e9, 1), "peak": hbm_peak,
+                "unit": "GB/s", "peak_source": hbm_src}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["kernel"] = dominant
-    traffic = load_traffic().get(f"{dominant}:b{shard}")
-    roof["traffic"] = traffic
+    roof["algorithmic_bytes_per_step"] = dom_bytes
+    if dom_ops:
+        roof["intensity_ops_per_byte"] = round(dom_ops / dom_bytes, 1)
+    roof["ridge_ops_per_byte"] = round(int8_peak * 1e12 / (hbm_peak * 1e9), 1)
+    traffic_tab, traffic_src = load_traffic()
+    roof["traffic"] = traffic_tab.get(f"{dominant}:b{shard}")
+    roof["traffic_source"] = (f"{traffic_src}: ncu dram__bytes_read.sum + dram__bytes_write.sum of this kernel's "
+                              f"launches in one step, from an earlier capture (not measured in this run)"
+                              if roof["traffic"] is not None else None)
 
     stages = {}
     for kind, sec in per_kind.items():
-        s = {"ms": round(sec * 1e3, 3), "share": round(sec / stage_sum, 4)}
+        st = {"ms": round(sec * 1e3, 3), "share": round(sec / stage_sum, 4),
+              "GB_s": round(kind_work(kind) / sec / 1e9, 1)}
+        st["frac_hbm"] = round(st["GB_s"] / hbm_peak, 4)
         if kind == "gemm":
-            s["TOPS"] = round(kind_work(kind) / sec / 1e12, 2)
-        else:
-            s["GB_s"] = round(kind_work(kind) / sec / 1e9, 1)
-        stages[kind] = s
+            st["TOPS"] = round(kind_work(kind, "gemm_ops") / sec / 1e12, 2)
+            st["frac_int8_peak"] = round(st["TOPS"] / int8_peak, 4)
+        stages[kind] = st
     layer_ms = {work[i]["name"]: round(sum(v.values()) * 1e3, 3) for i, v in sorted(per_layer.items())}
     layer_stage_ms = {work[i]["name"]: {k: round(t * 1e3, 3) for k, t in v.items()} for i, v in sorted(per_layer.items())}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": n_warm, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
+        "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "int8",
+        "dtype_note": "int8 operands on tcgen05 kind::i8 with int32 accumulation; every layer exact in int32 "
+                      "(RNS residues), int8 maps between layers (BASELINE glue)",
         "data": "synthetic (seeded PCG64 images U{0..127}, weights round(N(0,20^2)) clipped; no dataset)",
         "config": {"workload": f"BASELINE config 4: VGG16 13x conv3x3 stack, 224x224x3, batch {global_batch} "
                                f"({shard} images per GPU), F(14x14,3x3), RNS(4001,4331), relu/shift/maxpool glue "
@@ -421,16 +511,27 @@ def run_gpu_arm(args):
                                   "fused into each layer's output stage"),
                    "global_batch": global_batch, "per_rank_batch": shard, "tile": "F(14x14,3x3)",
                    "moduli": [4001, 4331], "parallelism": f"image-sharded x{world}, one all-gather at the end",
-                   "l2": "inputs and intermediates larger than L2 (126 MB)",
+                   "l2": "inputs and intermediates larger than L2 (126 MB); no flush needed",
                    "layer_ms": layer_ms, "layer_stage_ms": layer_stage_ms,
                    "launch": "CUDA graph per step" if graph_used else "eager"},
         "stages": stages,
-        "gpu_launches": (net.launches_per_forward() if args.unfused else 3 * len(W.VGG16_LAYERS)) * args.steps,
+        "gpu_launches": (net.launches_per_forward() if args.unfused else net.launches_fused()) * args.steps,
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": round(e2e_elapsed / args.steps * 1e3, 3)},
+                "ms_per_step": round(e2e_elapsed / args.steps * 1e3, 3),
+                "path": "VGG16Rns.run_stream: pinned host batch -> H2D -> 13 layers (CUDA graph) -> D2H, copies "
+                        "overlapped with the neighbouring steps on a copy stream"},
         "roofline": roof,
+        "int8_peak_tops_measured": round(int8_peak, 1),
         "clocks": clocks.summary(),
     }
+    if _native.library_path() != _native._PRODUCT_LIB:
+        line["diagnostic_library"] = str(_native.library_path())
+
+    if world == 1 and not args.no_layer_configs:
+        try:
+            line["layer_configs"] = layer_config_latencies(torch)
+        except Exception as exc:  # reported, never silently dropped
+            line["layer_configs"] = {"error": repr(exc)}
 
     if world == 1 and not args.no_cpu_baseline:
         n_res = 2
@@ -447,8 +548,24 @@ def run_gpu_arm(args):
         dist.destroy_process_group()
 
 
+def spawn_ranks(args) -> int:
+    """--gpus N without a torchrun environment: relaunch this script under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

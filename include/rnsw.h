@@ -22,6 +22,9 @@
  *                              rw/residue.py:180-206)
  *   rnsw_conv_forward       <- winograd_layer_conv body after its pre-flight
  *                              checks (rw/layer.py:343-389)
+ *   rnsw_conv_forward_timed <- the same body with the reference's StageTimings
+ *                              accounting (rw/layer.py:211-232, 366-376)
+ *   rnsw_tile_decompose     <- layer.tile_decompose (rw/layer.py:118-158)
  *   rnsw_mrc_reconstruct    <- residue.mrc_reconstruct_arrays (rw/residue.py:180-206)
  *
  * Conventions
@@ -70,7 +73,8 @@ typedef struct rnsw_plan rnsw_plan;
  * [n_res][n_res] with mrc_inv[j][i] = m_i^-1 mod m_j for i < j (host memory).
  * Errors: RNSW_ERR_INVALID (bad modulus / geometry), RNSW_ERR_NOT_COPRIME,
  * RNSW_ERR_SYSTEM (inverse table inconsistent), RNSW_ERR_UNSUPPORTED
- * (N > 16, R > 8, n_res > 4), RNSW_ERR_CUDA. */
+ * (N > 24, R > 8, n_res > 4; tiles with N <= 16 and moduli < 4500 run the
+ * tensor-core kernels, larger ones the generic CUDA-core kernels), RNSW_ERR_CUDA. */
 int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_t* moduli,
                      const int16_t* at, const int16_t* g, const int16_t* bt,
                      const int32_t* mrc_inv);
@@ -124,12 +128,28 @@ int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int 
                       int pad, int layout, const void* U, int32_t* y, void* workspace,
                       size_t workspace_bytes, void* stream);
 
+/* rnsw_conv_forward with CUDA events between its stages: the same kernel
+ * chain (whatever the plan dispatches to), then a host synchronisation;
+ * stage_ms[0..2] = input transform, Winograd product (GEMM or small-channel
+ * product), output transform + reconstruction + scatter, in milliseconds.
+ * The only synchronising entry point (the reference's `timings` argument). */
+int rnsw_conv_forward_timed(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K,
+                            int pad, int layout, const void* U, int32_t* y, void* workspace,
+                            size_t workspace_bytes, void* stream, float* stage_ms);
+/* Overlapping N x N patches of the zero canvas at stride tile_m
+ * (rw/layer.py:118-158): x NHWC int8 -> patches
+ * (B, ceil(Ho/M), ceil(Wo/M), N, N, C) int8 on the device. */
+int rnsw_tile_decompose(const int8_t* x, int B, int H, int W, int C, int tile_m, int r, int pad,
+                        int8_t* patches, size_t patches_bytes, void* stream);
+
 /* Whole layer with the VGG16-stack glue fused into the output stage:
  * relu, >> shift, clip to [0,127], optional 2x2 max-pool (even tile_m),
  * written as int8 NHWC (B, Ho[/2], Wo[/2], K) -- the int32 output is never
  * materialised.  Not part of the reference package (BASELINE.json configs
  * 2/4 define the glue); equals rnsw_conv_forward followed by
- * rnsw_requant_pool.  NHWC only; K % 4 == 0; moduli < 4500. */
+ * rnsw_requant_pool.  NHWC only; K % 4 == 0; moduli < 4500; `out` 4-byte
+ * aligned (RNSW_ERR_INVALID otherwise; 16-byte alignment with K % 16 == 0
+ * selects 16-byte stores). */
 int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K,
                               int pad, const void* U, int shift, int pool, int8_t* out, void* workspace,
                               size_t workspace_bytes, void* stream);

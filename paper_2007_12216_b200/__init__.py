@@ -24,6 +24,7 @@ from .layer import (
     LayerSpec,
     RangeReport,
     StageTimings,
+    TilePlacement,
     conv2d_rns,
     count_operations,
     direct_conv,
@@ -31,6 +32,7 @@ from .layer import (
     precompute_filter_transforms,
     precompute_filters_oihw,
     range_check,
+    tile_decompose,
     winograd_layer_conv,
 )
 from .residue import RnsSystem, mod_inverse, mod_reduce
@@ -59,7 +61,8 @@ __all__ = [
     "INF", "ExactTransformSet", "ModularTransformSet", "default_points", "vandermonde", "vandermonde_inverse",
     "derive_transforms", "cached_transforms", "check_modulus_compatibility", "reduce_transforms_mod",
     "reduce_for_system",
-    "LayerSpec", "RangeReport", "StageTimings", "FilterBank", "range_check", "count_operations",
+    "LayerSpec", "RangeReport", "StageTimings", "FilterBank", "TilePlacement", "range_check", "count_operations",
+    "tile_decompose",
     "precompute_filter_transforms", "precompute_filters_oihw", "winograd_layer_conv", "layer_conv", "conv2d_rns",
     "direct_conv", "DirectWeights",
     "read_tensor", "write_tensor", "QTNS_MAGIC", "QTNS_VERSION", "tile_conv_mod", "rns_tile_conv",

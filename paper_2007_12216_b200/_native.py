@@ -15,7 +15,25 @@ import numpy as np
 
 from .errors import raise_for
 
-_LIB_PATH = Path(os.environ.get("RNSW_LIB") or Path(__file__).resolve().parent / "librnsw.so")
+_PRODUCT_LIB = Path(__file__).resolve().parent / "librnsw.so"
+
+
+def _lib_path() -> Path:
+    """The in-tree librnsw.so.  Diagnostic A/B builds (tools/ab_*.sh, some of
+    which skip loads or MMAs and compute wrong answers on purpose) load only
+    when RNSW_DIAG=1 is set together with RNSW_LIB, and announce themselves on
+    stderr; bench.py records the override in its JSON line."""
+    override = os.environ.get("RNSW_LIB")
+    if override and os.environ.get("RNSW_DIAG") == "1":
+        import sys
+
+        print(f"[rnsw] DIAGNOSTIC library {override} (RNSW_DIAG=1): results may be wrong by design",
+              file=sys.stderr)
+        return Path(override)
+    return _PRODUCT_LIB
+
+
+_LIB_PATH = _lib_path()
 _lock = threading.Lock()
 _lib = None
 
@@ -48,6 +66,11 @@ _SIGNATURES = {
     "rnsw_output_residues": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "rnsw_conv_forward": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                   c_void_p, c_void_p, c_size_t, c_void_p]),
+    "rnsw_conv_forward_timed": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                        c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
+                                        ctypes.POINTER(ctypes.c_float)]),
+    "rnsw_tile_decompose": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_size_t,
+                                    c_void_p]),
     "rnsw_conv_forward_requant": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                           c_int, c_int, c_void_p, c_void_p, c_size_t, c_void_p]),
     "rnsw_output_transform_requant": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
@@ -124,6 +147,12 @@ class Plan:
         g = np.ascontiguousarray(g, dtype=np.int16)
         bt = np.ascontiguousarray(bt, dtype=np.int16)
         inv = np.ascontiguousarray(mrc_inv, dtype=np.int32)
+        # identity of the modular transform matrices: two plans with the same
+        # key compute the same filter bank (default and custom points differ)
+        import hashlib
+
+        self.key = (self.tile_m, self.r, self.moduli,
+                    hashlib.sha1(at.tobytes() + g.tobytes() + bt.tobytes()).hexdigest())
         handle = c_void_p()
         check(l.rnsw_plan_create(ctypes.byref(handle), self.tile_m, self.r, len(self.moduli),
                                  mods.ctypes.data_as(_i32p), at.ctypes.data_as(_i16p), g.ctypes.data_as(_i16p),

@@ -455,21 +455,46 @@ namespace {
 // K1 + K3 of a whole-layer call: the tensor-core GEMM path, or for C <= 4
 // the compact transform + CUDA-core product (smallc.cu), into Mw.
 // planar: leave Mw8 (the byte planes the tcgen05 output transform reads).
+// ev (optional): events recorded after K1 (ev[0]) and after K3 (ev[1]).
 int transform_and_product(const rnsw_plan* plan, const rnsw::Geometry& g, const int8_t* x, const void* U, int8_t* V,
-                          int16_t* Mw, cudaStream_t s, bool planar = false) {
+                          int16_t* Mw, cudaStream_t s, bool planar = false, cudaEvent_t* ev = nullptr) {
   cudaError_t e;
   if (rnsw::smallc_ok(plan->host.dev, g) && !rnsw::force_generic()) {
     int16_t* V16 = reinterpret_cast<int16_t*>(V);
     e = rnsw::launch_input_transform_compact(plan->host, g, x, V16, s);
     if (e != cudaSuccess) return cuda_fail(e, "input_transform_compact");
+    if (ev) cudaEventRecord(ev[0], s);
     e = rnsw::launch_smallc_product(plan->host, g, V16, static_cast<const int8_t*>(U), Mw, s, planar);
+    if (ev) cudaEventRecord(ev[1], s);
     return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "smallc_product");
   }
   e = rnsw::launch_input_transform(plan->host, g, x, V, s);
   if (e != cudaSuccess) return cuda_fail(e, "input_transform");
+  if (ev) cudaEventRecord(ev[0], s);
   e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, g.K, g.Kp, g.bc, Mw, s,
                                  rnsw::tc_output_ok(plan->host.dev) && !rnsw::force_generic(), planar);
+  if (ev) cudaEventRecord(ev[1], s);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "winograd_gemm");
+}
+
+// One whole layer: the dispatch rnsw_conv_forward runs (and, with ev, the
+// same chain with events between the stages: rnsw_conv_forward_timed).
+int conv_forward_impl(const rnsw_plan* plan, const rnsw::Geometry& g, const int8_t* x, const void* U, int32_t* y,
+                      void* workspace, size_t workspace_bytes, cudaStream_t s, cudaEvent_t* ev) {
+  const PlanDevice& d = plan->host.dev;
+  const size_t vb = round_up(v_bytes(d, g.P, g.Cp), 256);
+  const size_t mb = m_bytes(d, g.P, g.Kp);
+  if (workspace_bytes < vb + mb) return fail(RNSW_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, vb + mb);
+  int8_t* V = static_cast<int8_t*>(workspace);
+  int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
+  if (rnsw::umma_output_ok(d)) {
+    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true, ev)) return rc;
+    cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), y, s);
+    return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_umma");
+  }
+  if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, false, ev)) return rc;
+  cudaError_t e = rnsw::launch_output_transform(plan->host, g, Mw, y, nullptr, s);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform");
 }
 }  // namespace
 
@@ -480,21 +505,51 @@ int rnsw_conv_forward(const rnsw_plan* plan, const int8_t* x, int B, int H, int 
     return fail(RNSW_ERR_INVALID, "null buffer");
   rnsw::Geometry g;
   if (int rc = make_geometry(plan, B, H, W, C, K, pad, layout, &g)) return rc;
-  const PlanDevice& d = plan->host.dev;
-  const size_t vb = round_up(v_bytes(d, g.P, g.Cp), 256);
-  const size_t mb = m_bytes(d, g.P, g.Kp);
-  if (workspace_bytes < vb + mb) return fail(RNSW_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, vb + mb);
-  int8_t* V = static_cast<int8_t*>(workspace);
-  int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
+  return conv_forward_impl(plan, g, x, U, y, workspace, workspace_bytes, (cudaStream_t)stream, nullptr);
+}
+
+int rnsw_conv_forward_timed(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
+                            int layout, const void* U, int32_t* y, void* workspace, size_t workspace_bytes,
+                            void* stream, float* stage_ms) {
+  if (int rc = check_plan(plan)) return rc;
+  if (x == nullptr || U == nullptr || y == nullptr || workspace == nullptr || stage_ms == nullptr)
+    return fail(RNSW_ERR_INVALID, "null buffer");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, C, K, pad, layout, &g)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
-  if (rnsw::umma_output_ok(d)) {
-    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true)) return rc;
-    cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), y, s);
-    return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_umma");
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ev[i]);
+  int rc = RNSW_OK;
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "cudaEventCreate");
+  } else {
+    cudaEventRecord(ev[0], s);
+    rc = conv_forward_impl(plan, g, x, U, y, workspace, workspace_bytes, s, ev + 1);
+    if (rc == RNSW_OK) {
+      cudaEventRecord(ev[3], s);
+      e = cudaEventSynchronize(ev[3]);
+      for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaEventElapsedTime(&stage_ms[i], ev[i], ev[i + 1]);
+      if (e != cudaSuccess) rc = cuda_fail(e, "stage timing");
+    }
   }
-  if (int rc = transform_and_product(plan, g, x, U, V, Mw, s)) return rc;
-  cudaError_t e = rnsw::launch_output_transform(plan->host, g, Mw, y, nullptr, s);
-  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform");
+  for (int i = 0; i < 4; ++i)
+    if (ev[i]) cudaEventDestroy(ev[i]);
+  return rc;
+}
+
+int rnsw_tile_decompose(const int8_t* x, int B, int H, int W, int C, int tile_m, int r, int pad, int8_t* patches,
+                        size_t patches_bytes, void* stream) {
+  if (x == nullptr || patches == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
+  if (B < 1 || H < 1 || W < 1 || C < 1 || tile_m < 1 || r < 1 || pad < 0)
+    return fail(RNSW_ERR_SHAPE, "bad tiling geometry");
+  const int Ho = H + 2 * pad - r + 1, Wo = W + 2 * pad - r + 1;
+  if (Ho < 1 || Wo < 1) return fail(RNSW_ERR_SHAPE, "padded input smaller than the filter");
+  const int th = (Ho + tile_m - 1) / tile_m, tw = (Wo + tile_m - 1) / tile_m, n = tile_m + r - 1;
+  const size_t need = (size_t)B * th * tw * n * n * C;
+  if (patches_bytes < need) return fail(RNSW_ERR_WORKSPACE, "patch buffer %zu < %zu bytes", patches_bytes, need);
+  cudaError_t e = rnsw::launch_tile_decompose(x, B, H, W, C, tile_m, r, pad, patches, (cudaStream_t)stream);
+  return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "tile_decompose");
 }
 
 int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
@@ -507,6 +562,7 @@ int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int
   if (!rnsw::tc_output_ok(plan->host.dev))
     return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs the tensor-core transform path (moduli < 4500)");
   if ((K & 3) != 0) return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs K %% 4 == 0");
+  if ((reinterpret_cast<uintptr_t>(out) & 3) != 0) return fail(RNSW_ERR_INVALID, "out must be 4-byte aligned");
   if (pool && (plan->host.dev.m_out & 1)) return fail(RNSW_ERR_UNSUPPORTED, "fused 2x2 pooling needs an even tile_m");
   rnsw::Geometry g;
   if (int rc = make_geometry(plan, B, H, W, C, K, pad, RNSW_LAYOUT_NHWC, &g)) return rc;
@@ -535,6 +591,7 @@ int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, 
   if (Mw == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
   if (!rnsw::tc_output_ok(plan->host.dev) || (K & 3) != 0 || (pool && (plan->host.dev.m_out & 1)))
     return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation not available for this plan/geometry");
+  if ((reinterpret_cast<uintptr_t>(out) & 3) != 0) return fail(RNSW_ERR_INVALID, "out must be 4-byte aligned");
   rnsw::Geometry g;
   if (int rc = make_geometry(plan, B, H, W, 1, K, pad, RNSW_LAYOUT_NHWC, &g)) return rc;
   cudaError_t e = rnsw::launch_output_transform_tc(plan->host, g, static_cast<const int16_t*>(Mw), nullptr, nullptr,
@@ -603,6 +660,7 @@ int rnsw_output_transform_requant_mw8(const rnsw_plan* plan, const void* Mw8, in
   if (Mw8 == nullptr || out == nullptr) return fail(RNSW_ERR_INVALID, "null buffer");
   if (shift < 0 || shift > 31) return fail(RNSW_ERR_INVALID, "shift must be in [0, 31]");
   if ((K & 3) != 0) return fail(RNSW_ERR_UNSUPPORTED, "fused requantisation needs K %% 4 == 0");
+  if ((reinterpret_cast<uintptr_t>(out) & 3) != 0) return fail(RNSW_ERR_INVALID, "out must be 4-byte aligned");
   rnsw::Geometry g;
   if (int rc = make_geometry(plan, B, H, W, 1, K, pad, RNSW_LAYOUT_NHWC, &g)) return rc;
   if (pool && (g.Ho < 2 || g.Wo < 2)) return fail(RNSW_ERR_SHAPE, "pooling needs Ho, Wo >= 2");

@@ -564,7 +564,28 @@ bool make_tmap(CUtensorMap* tm, const void* base, int Cp, int64_t rows, int64_t 
   return r == CUDA_SUCCESS;
 }
 
-int g_num_sms = 0;
+}  // namespace
+
+// SM count of the current device, cached per device id (plans are per device,
+// and one process may drive several GPUs).
+int num_sms_current() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return 148;
+  if (dev >= 64) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }
+  if (cache[dev] == 0) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+namespace {
 
 template <int BN, int BC, int MAXPL, int MC, bool TS, int SB>
 cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
@@ -583,12 +604,8 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   auto kern = winograd_gemm_kernel<BN, BC, MAXPL, MC, TS, SB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int64_t grid = a.total_tiles * MC < g_num_sms ? a.total_tiles * MC : g_num_sms;
+  const int num_sms = num_sms_current();
+  int64_t grid = a.total_tiles * MC < num_sms ? a.total_tiles * MC : num_sms;
   grid = grid / MC * MC;
   if (grid < MC) grid = MC;
   if (MC == 1) {

@@ -78,10 +78,13 @@ cudaError_t launch_input_transform_compact(const PlanHost& plan, const Geometry&
 cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const int16_t* V16, const int8_t* U,
                                   int16_t* Mw, cudaStream_t s, bool planar = false);
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn();
+int num_sms_current();  // SM count of the current device (cached per device)
 size_t direct_weight_bytes(int R, int C, int K);
 cudaError_t launch_pack_weights(const int8_t* w, int R, int C, int K, int layout, int8_t* w2, cudaStream_t s);
 cudaError_t launch_direct_conv(const int8_t* x, int B, int H, int W, int C, const int8_t* w2, int K, int R, int pad,
                                int stride, int32_t* y, cudaStream_t s);
+cudaError_t launch_tile_decompose(const int8_t* x, int B, int H, int W, int C, int tile_m, int r, int pad,
+                                  int8_t* patches, cudaStream_t s);
 cudaError_t launch_mrc(const PlanHost& plan, const int16_t* residues, int64_t count, int64_t* out,
                        cudaStream_t s);
 cudaError_t launch_requant_pool(const int32_t* y, int B, int H, int W, int C, int shift, int pool, int8_t* out,

@@ -55,6 +55,7 @@ struct UArgs {
   int8_t* out8;
   int32_t* y;
   int shift;
+  int vec16;           // int8 output: K % 16 == 0 and out8 16-byte aligned -> 16-byte stores
   int kblocks;
   int64_t units;       // P * kblocks work units (tile, 32-channel block)
   int32_t negw10;      // -W[1][0] (kept opaque to the compiler: one IMAD per digit)
@@ -312,8 +313,8 @@ __global__ void __launch_bounds__(kThr, 2)
             args.y[(((int64_t)b_img * g.K + k0 + c) * g.Ho + ho) * g.Wo + wo] = ys[px * kPixW + c];
         }
       }
-    } else if ((g.K & 15) == 0) {
-      // 16-byte words (K % 16 == 0)
+    } else if (args.vec16) {
+      // 16-byte words (K % 16 == 0 and a 16-byte aligned output buffer)
       constexpr int side = kMode == 3 ? 7 : 14;
       const int Ho = kMode == 3 ? g.Ho / 2 : g.Ho, Wo = kMode == 3 ? g.Wo / 2 : g.Wo;
       for (int idx = tid; idx < side * side * (kKB / 16); idx += kThr) {
@@ -383,6 +384,7 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
   a.out8 = out8;
   a.y = y;
   a.shift = shift;
+  a.vec16 = out8 != nullptr && (g.K & 15) == 0 && (reinterpret_cast<uintptr_t>(out8) & 15) == 0;
   a.kblocks = (g.K + kKB - 1) / kKB;
   a.units = g.P * a.kblocks;
   if (a.units >= (1ll << 31)) return cudaErrorInvalidValue;  // FastDiv range
@@ -391,17 +393,18 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
   a.div_img = make_fastdiv((uint32_t)(g.th * g.tw));
   a.div_tw = make_fastdiv((uint32_t)g.tw);
   a.div_kb = make_fastdiv((uint32_t)a.kblocks);
-  static int num_sms = 0;
-  if (num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const unsigned grid = (unsigned)std::min<int64_t>(a.units, 2 * num_sms);
+  const int num_sms = num_sms_current();
   const int mode = out8 == nullptr ? 0 : (pool ? 3 : 1);
   auto launch = [&](auto kern, int smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
+    // persistent grid: as many CTAs as are co-resident (2 per SM for the int8
+    // modes; the int32 mode's 26 KB staging tile leaves room for only 1)
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThr, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    const unsigned grid = (unsigned)std::min<int64_t>(a.units, (int64_t)per_sm * num_sms);
     kern<<<grid, kThr, smem, s>>>(plan.d_plan, tm, a);
     return cudaGetLastError();
   };

@@ -328,6 +328,30 @@ __global__ void requant_pool_vec4_kernel(const int4* __restrict__ y, int B, int 
   }
 }
 
+// tile_decompose (rw/layer.py:118-158): overlapping N x N patches at stride
+// tile_m of the zero canvas (input at offset pad, zero-extended right and
+// bottom), patches[b][ti][tj][a][c2][ch].  Not on the layer path (K1 reads the
+// canvas through its own addressing); this is the public API counterpart.
+__global__ void tile_decompose_kernel(const int8_t* __restrict__ x, int B, int H, int W, int C, int M, int N,
+                                      int pad, int th, int tw, int8_t* __restrict__ out) {
+  const int64_t total = (int64_t)B * th * tw * N * N * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = i;
+    const int c = (int)(t % C);
+    t /= C;
+    const int bb = (int)(t % N);
+    t /= N;
+    const int a = (int)(t % N);
+    t /= N;
+    const int tj = (int)(t % tw);
+    t /= tw;
+    const int ti = (int)(t % th);
+    const int b = (int)(t / th);
+    const int h = ti * M + a - pad, w = tj * M + bb - pad;
+    out[i] = (h >= 0 && h < H && w >= 0 && w < W) ? x[(((int64_t)b * H + h) * W + w) * C + c] : (int8_t)0;
+  }
+}
+
 }  // namespace
 
 // RNSW_FORCE_GENERIC=1 routes every stage to the generic CUDA-core kernels
@@ -380,11 +404,9 @@ cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, cons
   if (tc_output_ok(plan.dev) && !force_generic()) return launch_input_transform_tc(plan, g, x, V, s);
   const int npos = plan.dev.n * plan.dev.n;
   const size_t smem = (size_t)(2 * npos * kChanBlock + plan.dev.n_res * npos) * sizeof(int32_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(input_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  // the >48 KB opt-in is per device: set it on every launch (cheap host call)
+  cudaError_t e = cudaFuncSetAttribute(input_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)g.P, g.Cp / kChanBlock);
   input_transform_kernel<<<grid, 256, smem, s>>>(plan.d_plan, g, x, V);
   return cudaGetLastError();
@@ -400,13 +422,20 @@ cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, con
   };
   while (kcb > 4 && smem_for(kcb) > 200 * 1024) kcb /= 2;  // large tiles / many residues
   const size_t smem = smem_for(kcb);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(output_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr_set = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(output_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       220 * 1024);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)g.P, (g.K + kcb - 1) / kcb);
   output_transform_kernel<<<grid, 256, smem, s>>>(plan.d_plan, g, Mw, y, y_res, kcb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tile_decompose(const int8_t* x, int B, int H, int W, int C, int tile_m, int r, int pad,
+                                  int8_t* patches, cudaStream_t s) {
+  const int Ho = H + 2 * pad - r + 1, Wo = W + 2 * pad - r + 1;
+  const int th = (Ho + tile_m - 1) / tile_m, tw = (Wo + tile_m - 1) / tile_m, n = tile_m + r - 1;
+  const int64_t total = (int64_t)B * th * tw * n * n * C;
+  tile_decompose_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, B, H, W, C, tile_m, n, pad, th, tw, patches);
   return cudaGetLastError();
 }
 

@@ -148,6 +148,49 @@ def count_operations(spec: LayerSpec, system: RnsSystem, tile_m: int | None = No
     return OperationCounts(direct, wino, tiles, Fraction(direct, wino))
 
 
+@dataclass(frozen=True)
+class TilePlacement:
+    """Where one patch's outputs land in the layer output plane (rw/layer.py:106-115)."""
+
+    row: int
+    col: int
+    out_h0: int
+    out_h1: int
+    out_w0: int
+    out_w1: int
+
+
+def tile_decompose(x, tile_m: int, r: int, padding: int):
+    """Overlapping n x n patches (n = tile_m + r - 1) of the zero canvas at
+    stride tile_m, and each patch's crop rectangle (rw/layer.py:118-158).
+
+    The layer path never materialises the patches (the input-transform kernel
+    addresses the canvas directly); this public counterpart gathers them on
+    the GPU (rnsw_tile_decompose).  numpy in -> numpy patches; torch in ->
+    device tensor.  Returns (patches (B, th, tw, n, n, C) int8, placements)."""
+    torch = _torch()
+    if len(x.shape) != 4:
+        raise ShapeMismatch(f"x must be (b, h, w, c), got {tuple(x.shape)}")
+    if not _is_int8(x):
+        raise ShapeMismatch(f"x must be int8, got {x.dtype}")
+    b, h, w, c = (int(v) for v in x.shape)
+    n = tile_m + r - 1
+    out_h, out_w = h + 2 * padding - r + 1, w + 2 * padding - r + 1
+    if out_h < 1 or out_w < 1:
+        raise ShapeMismatch("padded input smaller than the filter")
+    th, tw = ceil(out_h / tile_m), ceil(out_w / tile_m)
+    host_result = isinstance(x, np.ndarray)
+    xd = to_device(x)
+    patches = torch.empty((b, th, tw, n, n, c), dtype=torch.int8, device=xd.device)
+    l = _native.lib()
+    _native.check(l.rnsw_tile_decompose(_native.c_void_p(xd.data_ptr()), b, h, w, c, tile_m, r, padding,
+                                        _native.c_void_p(patches.data_ptr()), patches.numel(), _stream_ptr()))
+    placements = [TilePlacement(row=ti, col=tj, out_h0=ti * tile_m, out_h1=min(ti * tile_m + tile_m, out_h),
+                                out_w0=tj * tile_m, out_w1=min(tj * tile_m + tile_m, out_w))
+                  for ti in range(th) for tj in range(tw)]
+    return (patches.cpu().numpy() if host_result else patches), placements
+
+
 # ---------------------------------------------------------------------------
 # plans and operand handling
 
@@ -242,9 +285,12 @@ class FilterBank(Mapping):
         self.n = plan.n
 
     def __getitem__(self, m):
+        """The reference dict's value: int8 residues for m < 256, int16
+        otherwise (dtype_for_modulus, rw/gemm.py:25-27; rw/transforms.py:303-313)."""
         if m not in self.moduli:
             raise KeyError(m)
-        return self.device_view(m).cpu().numpy()
+        u = self.device_view(m).cpu().numpy()
+        return u.astype(np.int8) if m < 256 else u
 
     def __iter__(self):
         return iter(self.moduli)
@@ -310,7 +356,8 @@ def _bank_for(plan: _native.Plan, filters, spec_c: int, spec_k: int, n: int):
     """Validate ``filters`` like rw/layer.py:350-358 and return the device bank."""
     torch = _torch()
     if isinstance(filters, FilterBank) and filters.plan.moduli == plan.moduli and filters.n == n \
-            and filters.plan.tile_m == plan.tile_m and filters.plan.r == plan.r:
+            and filters.plan.tile_m == plan.tile_m and filters.plan.r == plan.r \
+            and (filters.plan is plan or filters.plan.key == plan.key):
         if filters.c != spec_c or filters.k != spec_k:
             raise ShapeMismatch(f"precomputed filters are for c={filters.c}, k={filters.k}; "
                                 f"layer needs ({n}, {n}, {spec_c}, {spec_k})")
@@ -334,8 +381,30 @@ def _bank_for(plan: _native.Plan, filters, spec_c: int, spec_k: int, n: int):
 # the layer
 
 
+_ws_local = threading.local()
+
+
+def _workspace(nbytes: int, device):
+    """Per-thread, per-(device, stream) workspace that grows on demand, so
+    repeated layer calls do not allocate (calls on one stream are ordered, so
+    reusing the buffer is safe; other threads / streams get their own)."""
+    torch = _torch()
+    cache = getattr(_ws_local, "bufs", None)
+    if cache is None:
+        cache = _ws_local.bufs = {}
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+    buf = cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        cache.pop(key, None)
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        cache[key] = buf
+    return buf
+
+
 def _run_layer(plan, x_dev, b, h, w, c, k, pad, layout, bank, timings: StageTimings | None):
-    """Launch the three device stages; returns the int32 output tensor."""
+    """Launch the device stages (rnsw_conv_forward); returns the int32 output
+    tensor.  With ``timings`` the same kernel chain runs through
+    rnsw_conv_forward_timed, which records CUDA events between the stages."""
     torch = _torch()
     l = _native.lib()
     ho, wo = h + 2 * pad - plan.r + 1, w + 2 * pad - plan.r + 1
@@ -344,42 +413,31 @@ def _run_layer(plan, x_dev, b, h, w, c, k, pad, layout, bank, timings: StageTimi
     ws_bytes = l.rnsw_workspace_bytes(plan.handle, b, h, w, c, k, pad)
     if ws_bytes == 0:
         raise ShapeMismatch("layer geometry rejected by the native plan")
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=x_dev.device)
+    ws = _workspace(ws_bytes, x_dev.device)
     s = _stream_ptr()
     vp = _native.c_void_p
     if timings is None:
         _native.check(l.rnsw_conv_forward(plan.handle, vp(x_dev.data_ptr()), b, h, w, c, k, pad, layout,
-                                          vp(bank.data_ptr()), vp(y.data_ptr()), vp(ws.data_ptr()), ws_bytes, s))
+                                          vp(bank.data_ptr()), vp(y.data_ptr()), vp(ws.data_ptr()), ws.numel(), s))
         return y
-    p = b * ceil(ho / plan.tile_m) * ceil(wo / plan.tile_m)
-    vb = l.rnsw_v_bytes(plan.handle, p, c)
-    vb = (vb + 255) // 256 * 256
-    v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    ev[0].record()
-    # the same kernels rnsw_conv_forward picks: for C <= 4 on a tensor-core
-    # plan the compact transform + CUDA-core product (csrc/smallc.cu)
-    compact = c <= 4 and l.rnsw_input_transform_compact(plan.handle, vp(x_dev.data_ptr()), b, h, w, c, pad, layout,
-                                                        vp(v_ptr), vb, s) == _native.RNSW_OK
-    if compact:
-        ev[1].record()
-        _native.check(l.rnsw_small_channel_product(plan.handle, vp(v_ptr), vp(bank.data_ptr()), p, c, k, vp(m_ptr),
-                                                   ws_bytes - vb, s))
-    else:
-        _native.check(l.rnsw_input_transform(plan.handle, vp(x_dev.data_ptr()), b, h, w, c, pad, layout,
-                                             vp(v_ptr), vb, s))
-        ev[1].record()
-        _native.check(l.rnsw_winograd_gemm(plan.handle, vp(v_ptr), vp(bank.data_ptr()), p, c, k, vp(m_ptr),
-                                           ws_bytes - vb, s))
-    ev[2].record()
-    _native.check(l.rnsw_output_transform(plan.handle, vp(m_ptr), b, h, w, k, pad, layout, vp(y.data_ptr()), s))
-    ev[3].record()
-    ev[3].synchronize()
-    timings.input_transform += ev[0].elapsed_time(ev[1]) / 1e3
-    timings.gemm += ev[1].elapsed_time(ev[2]) / 1e3
+    ms = (_native.ctypes.c_float * 3)()
+    _native.check(l.rnsw_conv_forward_timed(plan.handle, vp(x_dev.data_ptr()), b, h, w, c, k, pad, layout,
+                                            vp(bank.data_ptr()), vp(y.data_ptr()), vp(ws.data_ptr()), ws.numel(), s,
+                                            ms))
+    timings.input_transform += ms[0] / 1e3
+    timings.gemm += ms[1] / 1e3
     # backward transform, MRC and scatter are one fused kernel on the device
-    timings.backward_transform += ev[2].elapsed_time(ev[3]) / 1e3
+    timings.backward_transform += ms[2] / 1e3
     return y
+
+
+def _to_host(y):
+    """Device int32 result -> numpy through a pinned staging buffer."""
+    torch = _torch()
+    host = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+    host.copy_(y, non_blocking=True)
+    torch.cuda.current_stream(y.device).synchronize()
+    return host.numpy()
 
 
 def winograd_layer_conv(spec: LayerSpec, weights, x, system: RnsSystem, declared_bound: int | None = None,
@@ -415,43 +473,65 @@ def winograd_layer_conv(spec: LayerSpec, weights, x, system: RnsSystem, declared
         bank = _bank_for(plan, filters, spec.c, spec.k, n)
     y = _run_layer(plan, x_dev, spec.batch, spec.h, spec.w, spec.c, spec.k, spec.padding, _native.LAYOUT_NHWC,
                    bank, timings)
-    return y.cpu().numpy() if host_result else y
+    return _to_host(y) if host_result else y
+
+
+def _c16(c: int) -> int:
+    return (c + 15) // 16 * 16
 
 
 class DirectWeights:
-    """Weights packed once for the direct tcgen05 convolution ([K][R*R*Cp])."""
+    """Weights packed once for the direct tcgen05 convolution ([K][R*R*Cp]).
+    Channel counts that are not a multiple of 16 are zero-padded to one (the
+    activations get the same zero channels in ``direct_conv``), so every C
+    runs on the device."""
 
     def __init__(self, weights, layout: int = _native.LAYOUT_NHWC):
         torch = _torch()
         wd = to_device(weights)
         if layout == _native.LAYOUT_NHWC:
             r, _, c, k = (int(v) for v in wd.shape)
+            if c % 16:
+                wp = torch.zeros((r, r, _c16(c), k), dtype=torch.int8, device=wd.device)
+                wp[:, :, :c, :] = wd
+                wd = wp
         else:
             k, c, r, _ = (int(v) for v in wd.shape)
+            if c % 16:
+                wp = torch.zeros((k, _c16(c), r, r), dtype=torch.int8, device=wd.device)
+                wp[:, :c] = wd
+                wd = wp
+        cp = _c16(c)
         l = _native.lib()
-        nbytes = l.rnsw_direct_weight_bytes(r, c, k)
+        nbytes = l.rnsw_direct_weight_bytes(r, cp, k)
         self.data = torch.empty(nbytes, dtype=torch.int8, device=wd.device)
-        _native.check(l.rnsw_direct_pack_weights(_native.c_void_p(wd.data_ptr()), r, c, k, layout,
+        _native.check(l.rnsw_direct_pack_weights(_native.c_void_p(wd.data_ptr()), r, cp, k, layout,
                                                  _native.c_void_p(self.data.data_ptr()), nbytes, _stream_ptr()))
         self.r, self.c, self.k = r, c, k
 
 
 def direct_conv(spec: LayerSpec, weights, x, packed: DirectWeights | None = None):
     """Exact int32 convolution on the tensor cores: the device counterpart of
-    the reference's oracle direct_conv (rw/layer.py:93-103), any stride.
-    Implicit GEMM on tcgen05 kind::i8 with TMA im2col boxes; needs C % 16 == 0."""
+    the reference's oracle direct_conv (rw/layer.py:93-103), any stride and
+    any C (channels zero-padded to a multiple of 16 on the device for the TMA
+    row alignment).  Implicit GEMM on tcgen05 kind::i8 with TMA im2col boxes."""
     torch = _torch()
     _check_operands(spec, weights, x)
     host_result = isinstance(x, np.ndarray)
     xd = to_device(x)
     if packed is None:
         packed = DirectWeights(weights)
+    c = spec.c
+    if c % 16:
+        xp = torch.zeros((spec.batch, spec.h, spec.w, _c16(c)), dtype=torch.int8, device=xd.device)
+        xp[..., :c] = xd
+        xd, c = xp, _c16(c)
     y = torch.empty((spec.batch, spec.out_h, spec.out_w, spec.k), dtype=torch.int32, device=xd.device)
     l = _native.lib()
-    _native.check(l.rnsw_direct_conv(_native.c_void_p(xd.data_ptr()), spec.batch, spec.h, spec.w, spec.c,
+    _native.check(l.rnsw_direct_conv(_native.c_void_p(xd.data_ptr()), spec.batch, spec.h, spec.w, c,
                                      _native.c_void_p(packed.data.data_ptr()), spec.k, spec.r, spec.padding,
                                      spec.stride, _native.c_void_p(y.data_ptr()), _stream_ptr()))
-    return y.cpu().numpy() if host_result else y
+    return _to_host(y) if host_result else y
 
 
 def layer_conv(spec: LayerSpec, weights, x, system: RnsSystem, declared_bound: int | None = None, filters=None,
@@ -459,9 +539,6 @@ def layer_conv(spec: LayerSpec, weights, x, system: RnsSystem, declared_bound: i
     """rw/layer.py:392-412: stride != 1 goes to the direct convolution --
     here the tcgen05 implicit-GEMM kernel, not a CPU fallback."""
     if spec.stride != 1:
-        _check_operands(spec, weights, x)
-        if spec.c % 16:
-            raise UnsupportedStride(f"stride {spec.stride} with C={spec.c}: the device direct conv needs C % 16 == 0")
         return direct_conv(spec, weights, x)
     return winograd_layer_conv(spec, weights, x, system, declared_bound=declared_bound, filters=filters,
                                timings=timings)
@@ -497,7 +574,7 @@ def conv2d_rns(x_nchw, w_oihw, moduli, tile_m: int, padding: int = 0, declared_b
     else:
         bank = _bank_for(plan, filters, c, k, plan.n)
     y = _run_layer(plan, x_dev, b, h, w, c, k, padding, _native.LAYOUT_NCHW, bank, None)
-    return y.cpu().numpy() if host_result else y
+    return _to_host(y) if host_result else y
 
 
 def precompute_filters_oihw(w_oihw, moduli, tile_m: int) -> FilterBank:

@@ -69,6 +69,11 @@ class VGG16Rns:
     def launches_per_forward(self) -> int:
         return 4 * len(self.cfg.layers)  # input transform, GEMM, output transform, glue
 
+    def launches_fused(self) -> int:
+        """Kernels per forward_fused: input transform, product (GEMM or the
+        C <= 4 CUDA-core product), output transform with the glue."""
+        return 3 * len(self.cfg.layers)
+
     def layer_work(self, batch: int, fused: bool = False) -> list[dict]:
         """Algorithmic work per layer and kernel ("Roofline"):
         bytes for the memory-bound stages, int8 tensor ops for the GEMM."""
@@ -84,6 +89,9 @@ class VGG16Rns:
                 "name": name,
                 "input_transform_bytes": batch * side * side * c + planes * npos * tiles * c,
                 "gemm_ops": 2 * tiles * npos * c * k * mma_per_product,
+                # V in, the filter bank once, the Winograd-domain product out
+                "gemm_bytes": planes * npos * tiles * c + sum(1 if m < 256 else 4 for m in self.cfg.moduli)
+                * npos * k * c + len(self.cfg.moduli) * npos * tiles * k * 2,
                 "output_transform_bytes": len(self.cfg.moduli) * npos * tiles * k * 2 + (
                     batch * oside * oside * k if fused else batch * side * side * k * 4),
                 "glue_bytes": batch * side * side * k * 4 + batch * oside * oside * k,
@@ -303,9 +311,10 @@ class VGG16Rns:
             cur = nxt
         return cur
 
-    def forward(self, x, keep_int32: bool = False):
+    def forward(self, x, keep_int32: bool = False, keep_images=None):
         """x: (B, 224, 224, 3) int8 CUDA tensor (NHWC).  Returns the final
-        (B, 7, 7, 512) int8 map, plus every layer's int32 output if asked."""
+        (B, 7, 7, 512) int8 map, plus every layer's int32 output if asked
+        (only the images listed in ``keep_images``, when given)."""
         torch = _torch()
         l = _native.lib()
         vp = _native.c_void_p
@@ -322,7 +331,7 @@ class VGG16Rns:
                                               _native.LAYOUT_NHWC, vp(bank.data.data_ptr()), vp(y.data_ptr()),
                                               vp(ws.data_ptr()), ws.numel(), s))
             if keep_int32:
-                outs.append(y.clone())
+                outs.append(y[list(keep_images)].clone() if keep_images is not None else y.clone())
             oside = side // 2 if pool else side
             if i == nl - 1:
                 nxt = bufs["out"]

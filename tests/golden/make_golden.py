@@ -19,6 +19,8 @@ Outputs
   tiles.npz         single-tile API: kernel.tile_conv_mod / rns_tile_conv on
                     seeded (stacked) tiles, 8- and 16-bit moduli
   qtns.json         layer.write_tensor bytes (hex) of seeded int8 / int32 tensors
+  vgg_shards.json   config 4 beyond image 0: reference final-map digests for one
+                    image per 32-image shard, per-layer int32 digests for two
 
 ``--only tiles,qtns`` regenerates just the named fixtures.
 """
@@ -169,6 +171,39 @@ def gen_digests():
     return out
 
 
+VGG_SHARD_IMAGES = (32, 64, 96, 128, 160, 192, 224, 255)  # one per 32-image shard of config 4 (+ the last)
+VGG_LAYER_IMAGES = (128, 255)                              # per-layer int32 digests for these
+
+
+def gen_vgg_shards():
+    """Config 4 beyond image 0: the reference RNS path (winograd_layer_conv,
+    the declared bounds of workloads.vgg16_bounds) through all 13 layers plus
+    the BASELINE glue for one image of every 32-image shard; per-layer int32
+    digests for VGG_LAYER_IMAGES (conv4_2..conv5_3 run at the signed bound)."""
+    t0 = time.time()
+    weights = W.vgg16_weights()
+    bounds = W.vgg16_bounds(weights)
+    system = residue.RnsSystem(W.SYS16)
+    out = {}
+    for idx in VGG_SHARD_IMAGES:
+        x = W.vgg16_images(1, start=idx)
+        rec = {"x": sha(x)}
+        for i, ((name, side, c, k, pool), wt) in enumerate(zip(W.VGG16_LAYERS, weights)):
+            spec = layer.LayerSpec(h=side, w=side, c=c, k=k, r=3, padding=1, batch=1, tile_m=14)
+            y = layer.winograd_layer_conv(spec, wt, x, system, declared_bound=bounds[i])
+            if idx in VGG_LAYER_IMAGES:
+                rec[name] = sha(y)
+            v = np.clip(np.maximum(y, 0) >> W.VGG16_SHIFTS[i], 0, 127).astype(np.int8)
+            if pool:
+                b, hh, ww, cc = v.shape
+                v = v.reshape(b, hh // 2, 2, ww // 2, 2, cc).max(axis=(2, 4))
+            x = np.ascontiguousarray(v)
+        rec["final"] = sha(x)
+        out[str(idx)] = rec
+        print("vgg shard image", idx, time.time() - t0, flush=True)
+    return out
+
+
 def gen_verify():
     """The reference's own 217-case verification sweep (rw/cli.py:278-334):
     case list and a digest of every layer_conv output (== direct_conv)."""
@@ -260,6 +295,8 @@ def main():
             arrays, meta = gen_tiles()
             np.savez_compressed(HERE / "tiles.npz", **arrays)
             (HERE / "tiles.json").write_text(json.dumps(meta, indent=1))
+        if "vggshards" in only:
+            (HERE / "vgg_shards.json").write_text(json.dumps(gen_vgg_shards(), indent=1))
         if "qtns" in only:
             import tempfile
 
