@@ -293,8 +293,10 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
   cudaError_t e = cudaGetDevice(&plan->host.device);
   if (e == cudaSuccess) e = cudaMalloc(&plan->host.d_plan, sizeof(PlanDevice));
   if (e == cudaSuccess) e = cudaMemcpy(plan->host.d_plan, &d, sizeof(d), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = rnsw::build_kr_images(plan->host);
   if (e != cudaSuccess) {
     if (plan->host.d_plan) cudaFree(plan->host.d_plan);
+    rnsw::free_kr_images(plan->host);
     delete plan;
     return cuda_fail(e, "rnsw_plan_create");
   }
@@ -305,6 +307,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
 void rnsw_plan_destroy(rnsw_plan* plan) {
   if (plan == nullptr) return;
   if (plan->host.d_plan) cudaFree(plan->host.d_plan);
+  rnsw::free_kr_images(plan->host);
   delete plan;
 }
 

@@ -179,6 +179,14 @@ RNSW_DEV void tma_load_5d(void* dst, const void* desc, uint64_t* bar, int c0, in
       : "memory");
 }
 
+RNSW_DEV void tma_load_4d(void* dst, const void* desc, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // Bulk tensor store smem -> global (bulk-group completion).
 RNSW_DEV void tma_store_2d(const void* desc, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -190,6 +198,12 @@ RNSW_DEV void tma_store_3d(const void* desc, const void* src, int c0, int c1, in
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(desc)),
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+RNSW_DEV void tma_store_4d(const void* desc, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
 RNSW_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -339,6 +353,19 @@ RNSW_DEV uint64_t umma_desc_mn_sw32(uint32_t smem_addr, uint32_t atom_stride) {
   d |= (uint64_t)(256 >> 4) << 32;                      // SBO: next 8 K rows
   d |= (uint64_t)1 << 46;
   d |= 6ull << 61;                                      // SWIZZLE_32B
+  return d;
+}
+
+// ... in the 64B-swizzled canonical layout: each K index is one 64-byte row
+// of 64 consecutive M (or N) elements, 8-row K groups 512 bytes apart (SBO),
+// the next 64 M elements (MN atom) `atom_stride` bytes further (LBO).
+RNSW_DEV uint64_t umma_desc_mn_sw64(uint32_t smem_addr, uint32_t atom_stride) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((atom_stride >> 4) & 0x3FFF) << 16;  // LBO: next MN atom
+  d |= (uint64_t)(512 >> 4) << 32;                      // SBO: next 8 K rows
+  d |= (uint64_t)1 << 46;
+  d |= 4ull << 61;                                      // SWIZZLE_64B
   return d;
 }
 

@@ -42,7 +42,22 @@ struct PlanHost {
   PlanDevice dev;         // host copy of the tables
   PlanDevice* d_plan;     // device copy
   int device;             // CUDA device the tables live on
+  // tcgen05 input transform (input_umma.cu): the Kronecker operator
+  // kron(BT, BT) mod m per (residue, 128-position block) as shared-memory
+  // images of the MMA A operand (K-major, 128B swizzle), one per group.
+  uint8_t* d_kr;          // [groups][kr_group_bytes] (nullptr: not built)
+  int kr_groups;          // n_res * kr_npb
+  int kr_npb;             // 128-position blocks: ceil(N*N / 128)
+  int kr_kp;              // K = N*N padded to a multiple of 32
+  int kr_khalves;         // 128-byte K chunks per A row: ceil(kr_kp / 128)
+  int kr_limbs;           // 1 (m < 256) or 2 (balanced s8 limbs)
+  size_t kr_group_bytes;  // kr_limbs * kr_khalves * 16 KB
 };
+
+// Build / release PlanHost::d_kr (input_umma.cu); a plan without it keeps
+// the mma.sync input transform.
+cudaError_t build_kr_images(PlanHost& plan);
+void free_kr_images(PlanHost& plan);
 
 cudaError_t launch_filter_transform(const PlanHost& plan, const int8_t* w, int C, int K, int Cp, int layout,
                                     int8_t* U, cudaStream_t s);
@@ -60,6 +75,9 @@ cudaError_t launch_output_transform(const PlanHost& plan, const Geometry& g, con
 cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, const int16_t* Mw, int32_t* y,
                                        int16_t* y_res, cudaStream_t s, int8_t* out8 = nullptr, int shift = 0,
                                        int pool = 0);
+bool umma_input_ok(const PlanHost& plan, const Geometry& g);
+cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
+                                        cudaStream_t s);
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s);
 bool tc_output_ok(const PlanDevice& d);

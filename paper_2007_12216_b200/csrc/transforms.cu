@@ -401,7 +401,10 @@ cudaError_t launch_filter_import(const PlanHost& plan, int res, const int16_t* u
 
 cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                    cudaStream_t s) {
-  if (tc_output_ok(plan.dev) && !force_generic()) return launch_input_transform_tc(plan, g, x, V, s);
+  if (tc_output_ok(plan.dev) && !force_generic()) {
+    if (umma_input_ok(plan, g)) return launch_input_transform_umma(plan, g, x, V, s);
+    return launch_input_transform_tc(plan, g, x, V, s);
+  }
   const int npos = plan.dev.n * plan.dev.n;
   const size_t smem = (size_t)(2 * npos * kChanBlock + plan.dev.n_res * npos) * sizeof(int32_t);
   // the >48 KB opt-in is per device: set it on every launch (cheap host call)

@@ -20,6 +20,9 @@ DEFAULT_SEED = 2020  # rw/cli.py:30
 
 
 def make_rng(*entropy) -> np.random.Generator:
+    """rw/cli.py:82-94: string items fold to int.from_bytes(...) % 2**64, i.e.
+    only their first 8 bytes count -- labels must differ there (or carry an
+    int item) to give independent streams."""
     words = []
     for item in entropy:
         if isinstance(item, str):
@@ -140,7 +143,7 @@ VGG16_LAYERS = [
 # Calibrated once (tools/calibrate_vgg.py) on the seed-2020 weights and image
 # so the int8 activations use their range; frozen here so every run, CPU or
 # GPU, applies the same glue.
-VGG16_SHIFTS = (8, 8, 9, 9, 9, 10, 9, 10, 10, 10, 9, 10, 10)
+VGG16_SHIFTS = (8, 9, 8, 9, 10, 9, 9, 10, 10, 9, 11, 9, 10)
 
 
 @dataclass(frozen=True)
@@ -165,7 +168,10 @@ class VGGConfig:
 
 def vgg16_weights(seed: int = DEFAULT_SEED) -> list[np.ndarray]:
     """(3,3,C,K) int8 per layer, round(N(0, 20^2)) clipped."""
-    return [gaussian_int8(make_rng(seed, f"vgg16/{name}/w"), (3, 3, c, k)) for name, _, c, k, _ in VGG16_LAYERS]
+    # make_rng folds a string label to its first 8 bytes (the reference's
+    # rw/cli.py:82-94 convention), so the per-layer / per-image index goes in
+    # as its own entropy word: every layer and every image gets its own stream
+    return [gaussian_int8(make_rng(seed, "vgg16w", i), (3, 3, c, k)) for i, (_, _, c, k, _) in enumerate(VGG16_LAYERS)]
 
 
 def vgg16_images(batch: int, seed: int = DEFAULT_SEED, start: int = 0) -> np.ndarray:
@@ -173,7 +179,7 @@ def vgg16_images(batch: int, seed: int = DEFAULT_SEED, start: int = 0) -> np.nda
     from its own stream so any shard [start, start+batch) is reproducible."""
     out = np.empty((batch, 224, 224, 3), dtype=np.int8)
     for i in range(batch):
-        out[i] = uniform_int8(make_rng(seed, f"vgg16/image/{start + i}"), (224, 224, 3), 0, 127)
+        out[i] = uniform_int8(make_rng(seed, "vgg16img", start + i), (224, 224, 3), 0, 127)
     return out
 
 

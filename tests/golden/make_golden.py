@@ -150,6 +150,14 @@ def gen_digests():
         out[case.name] = dict(y=sha(y))
         print(case.name, time.time() - t0, flush=True)
 
+    out.update(gen_vgg_digests())
+    return out
+
+
+def gen_vgg_digests():
+    """Config 2: VGG16 batch 1 (image 0), every layer and the final map."""
+    t0 = time.time()
+    out = {}
     weights = W.vgg16_weights()
     bounds = W.vgg16_bounds(weights)
     x = W.vgg16_images(1)
@@ -295,6 +303,11 @@ def main():
             arrays, meta = gen_tiles()
             np.savez_compressed(HERE / "tiles.npz", **arrays)
             (HERE / "tiles.json").write_text(json.dumps(meta, indent=1))
+        if "vggdigests" in only:
+            d = json.loads((HERE / "digests.json").read_text())
+            d = {k: v for k, v in d.items() if not k.startswith("vgg16/")}
+            d.update(gen_vgg_digests())
+            (HERE / "digests.json").write_text(json.dumps(d, indent=1))
         if "vggshards" in only:
             (HERE / "vgg_shards.json").write_text(json.dumps(gen_vgg_shards(), indent=1))
         if "qtns" in only:

@@ -45,6 +45,23 @@ def test_vgg_inputs_match_golden_digests():
     assert bounds == [dg[f"vgg16/{n}"]["bound"] for n, *_ in W.VGG16_LAYERS]
 
 
+def test_vgg_streams_are_independent():
+    """make_rng keeps only the first 8 bytes of a string label (the
+    reference's rw/cli.py:82-94 fold), so per-image / per-layer indices travel
+    as separate entropy words: every image and every layer is its own draw."""
+    imgs = W.vgg16_images(4, start=30)
+    for i in range(4):
+        for j in range(i + 1, 4):
+            assert (imgs[i] != imgs[j]).mean() > 0.9
+    ws = W.vgg16_weights()
+    same_shape = [i for i, (_, _, c, k, _) in enumerate(W.VGG16_LAYERS) if (c, k) == (512, 512)]
+    assert len(same_shape) == 5
+    for i in same_shape[1:]:
+        assert (ws[i] != ws[same_shape[0]]).mean() > 0.9
+    # the fold itself, as the reference has it
+    assert W.make_rng(1, "vgg16/image/1").integers(0, 1 << 30) == W.make_rng(1, "vgg16/im").integers(0, 1 << 30)
+
+
 def test_vgg_direct_ops():
     assert W.VGGConfig(batch=1).direct_ops() == sum(
         2 * s * s * c * k * 9 for _, s, c, k, _ in W.VGG16_LAYERS)
