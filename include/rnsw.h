@@ -153,6 +153,16 @@ int rnsw_tile_decompose(const int8_t* x, int B, int H, int W, int C, int tile_m,
 int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K,
                               int pad, const void* U, int shift, int pool, int8_t* out, void* workspace,
                               size_t workspace_bytes, void* stream);
+/* The same two whole-layer calls with two caller-created CUDA events
+ * (cudaEvent_t, passed as void*) recorded on `stream` after the input
+ * transform and after the Winograd product: per-stage device times of the
+ * exact kernel chain the untimed call runs (no host synchronisation). */
+int rnsw_conv_forward_ev(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
+                         int layout, const void* U, int32_t* y, void* workspace, size_t workspace_bytes,
+                         void* stream, void* const* events);
+int rnsw_conv_forward_requant_ev(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K,
+                                 int pad, const void* U, int shift, int pool, int8_t* out, void* workspace,
+                                 size_t workspace_bytes, void* stream, void* const* events);
 /* Stage 3 with the fused glue (Mw from rnsw_winograd_gemm). */
 int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, int H, int W, int K, int pad,
                                   int shift, int pool, int8_t* out, void* stream);

@@ -69,6 +69,10 @@ _SIGNATURES = {
     "rnsw_conv_forward_timed": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                         c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
                                         ctypes.POINTER(ctypes.c_float)]),
+    "rnsw_conv_forward_ev": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                     c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    "rnsw_conv_forward_requant_ev": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                             c_int, c_int, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
     "rnsw_tile_decompose": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_size_t,
                                     c_void_p]),
     "rnsw_conv_forward_requant": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,

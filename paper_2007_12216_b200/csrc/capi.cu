@@ -84,8 +84,12 @@ int make_geometry(const rnsw_plan* plan, int B, int H, int W, int C, int K, int 
   g->th = (g->Ho + d.m_out - 1) / d.m_out;
   g->tw = (g->Wo + d.m_out - 1) / d.m_out;
   g->P = (int64_t)B * g->th * g->tw;
-  // s32 accumulators: |sum| <= C * 128 * 128 must stay below 2^31.
-  if ((int64_t)C * 128 * 128 > 2147483647LL)
+  // s32 accumulators must stay below 2^31: per channel at most 128 * 128
+  // (8-bit residues) or, for 16-bit residues, |v_hi u'_lo + v_lo u_lo| <=
+  // 9 * 128 + 128 * 128 = 17536 (limbs of symmetric residues, gemm.cu)
+  bool wide = false;
+  for (int i = 0; i < d.n_res; ++i) wide = wide || d.res[i].planes == 2;
+  if ((int64_t)C * (wide ? 17536 : 128 * 128) > 2147483647LL)
     return fail(RNSW_ERR_OVERFLOW, "C=%d channels can overflow the int32 tensor-core accumulator", C);
   if (g->P > 2147483647LL) return fail(RNSW_ERR_UNSUPPORTED, "too many tiles (%lld)", (long long)g->P);
   g->Cp = padded_channels(C);
@@ -471,7 +475,8 @@ int transform_and_product(const rnsw_plan* plan, const rnsw::Geometry& g, const 
     if (ev) cudaEventRecord(ev[1], s);
     return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "smallc_product");
   }
-  e = rnsw::launch_input_transform(plan->host, g, x, V, s);
+  // whole-layer path: the GEMM accepts any representative of V (relaxed K1)
+  e = rnsw::launch_input_transform(plan->host, g, x, V, s, true);
   if (e != cudaSuccess) return cuda_fail(e, "input_transform");
   if (ev) cudaEventRecord(ev[0], s);
   e = rnsw::launch_winograd_gemm(plan->host, V, static_cast<const int8_t*>(U), g.P, g.Cp, g.K, g.Kp, g.bc, Mw, s,
@@ -555,9 +560,10 @@ int rnsw_tile_decompose(const int8_t* x, int B, int H, int W, int C, int tile_m,
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "tile_decompose");
 }
 
-int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
-                              const void* U, int shift, int pool, int8_t* out, void* workspace,
-                              size_t workspace_bytes, void* stream) {
+namespace {
+int requant_impl(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad, const void* U,
+                 int shift, int pool, int8_t* out, void* workspace, size_t workspace_bytes, cudaStream_t s,
+                 cudaEvent_t* ev) {
   if (int rc = check_plan(plan)) return rc;
   if (x == nullptr || U == nullptr || out == nullptr || workspace == nullptr)
     return fail(RNSW_ERR_INVALID, "null buffer");
@@ -576,16 +582,45 @@ int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int
   if (workspace_bytes < vb + mb) return fail(RNSW_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, vb + mb);
   int8_t* V = static_cast<int8_t*>(workspace);
   int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
-  cudaStream_t s = (cudaStream_t)stream;
   if (rnsw::umma_output_ok(d)) {
-    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true)) return rc;
+    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true, ev)) return rc;
     cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), nullptr, s,
                                                        out, shift, pool);
     return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant_umma");
   }
-  if (int rc = transform_and_product(plan, g, x, U, V, Mw, s)) return rc;
+  if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, false, ev)) return rc;
   cudaError_t e = rnsw::launch_output_transform_tc(plan->host, g, Mw, nullptr, nullptr, s, out, shift, pool);
   return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant");
+}
+}  // namespace
+
+int rnsw_conv_forward_requant(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
+                              const void* U, int shift, int pool, int8_t* out, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  return requant_impl(plan, x, B, H, W, C, K, pad, U, shift, pool, out, workspace, workspace_bytes,
+                      (cudaStream_t)stream, nullptr);
+}
+
+int rnsw_conv_forward_requant_ev(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
+                                 const void* U, int shift, int pool, int8_t* out, void* workspace,
+                                 size_t workspace_bytes, void* stream, void* const* events) {
+  if (events == nullptr || events[0] == nullptr || events[1] == nullptr) return fail(RNSW_ERR_INVALID, "null event");
+  cudaEvent_t ev[2] = {(cudaEvent_t)events[0], (cudaEvent_t)events[1]};
+  return requant_impl(plan, x, B, H, W, C, K, pad, U, shift, pool, out, workspace, workspace_bytes,
+                      (cudaStream_t)stream, ev);
+}
+
+int rnsw_conv_forward_ev(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, int C, int K, int pad,
+                         int layout, const void* U, int32_t* y, void* workspace, size_t workspace_bytes, void* stream,
+                         void* const* events) {
+  if (int rc = check_plan(plan)) return rc;
+  if (x == nullptr || U == nullptr || y == nullptr || workspace == nullptr)
+    return fail(RNSW_ERR_INVALID, "null buffer");
+  if (events == nullptr || events[0] == nullptr || events[1] == nullptr) return fail(RNSW_ERR_INVALID, "null event");
+  rnsw::Geometry g;
+  if (int rc = make_geometry(plan, B, H, W, C, K, pad, layout, &g)) return rc;
+  cudaEvent_t ev[2] = {(cudaEvent_t)events[0], (cudaEvent_t)events[1]};
+  return conv_forward_impl(plan, g, x, U, y, workspace, workspace_bytes, (cudaStream_t)stream, ev);
 }
 
 int rnsw_output_transform_requant(const rnsw_plan* plan, const void* Mw, int B, int H, int W, int K, int pad,

@@ -6,31 +6,31 @@
 //     V[(i,j)] = sum_(a,b) Kr[(i,j),(a,b)] d[(a,b)],   Kr = kron(BT, BT) mod m,
 // so the whole transform of a tile (all channels at once) is ONE GEMM per
 // residue and 128-position block:
-//     D[pos, ch] = sum_pix Kr[pos, pix] * patch[pix, ch]      (M=128, N=128, K=N*N)
-//   A = Kr limbs: a per-CTA constant, resident in shared memory (K-major,
-//       128B swizzle; built on the host into the plan, PlanHost::d_kr);
-//   B = the patch, TMA-loaded as a 4-D box (channels x N columns x N rows x 1
-//       image) straight from NHWC x: the box IS the MN-major operand (K =
-//       pixel rows, N = channels), and TMA's zero fill supplies the conv
-//       padding and the canvas extension of tile_decompose (rw/layer.py:118-158);
+//     D[pos, ch] = sum_pix Kr[pos, pix] * patch[pix, ch]      (M=128, N=64, K=N*N)
+//   A = Kr limbs: a per-CTA constant, resident in TENSOR memory (K-major, four
+//       int8 per column; written once with tcgen05.st), so the MMA reads only
+//       B from shared memory;
+//   B = the patch, TMA-loaded as a 4-D box (64 channels x N columns x N rows
+//       x 1 image) straight from NHWC x: the box IS the MN-major operand (K =
+//       pixel rows, N = channels, 64B swizzle), and TMA's zero fill supplies
+//       the conv padding and the canvas extension of tile_decompose
+//       (rw/layer.py:118-158);
 //   D = s32 in TMEM; 16-bit moduli: two accumulators (Kr = 256 Kr_hi + Kr_lo,
 //       balanced s8 limbs), x = 256 D_hi + D_lo, |x| < 2^27.
 // The Kronecker form does N*N/(2N) = 8x the MACs of the two-pass separable
 // form at N = 16, but it is a single pass: no TMEM round trip between the
-// passes, and each output value costs the CUDA cores one reduction and one
-// byte split (the mma.sync kernel spent ~165 warp instructions per
-// (tile, channel, residue); this one ~8 per value / 32 lanes).  The tensor
-// pipe, idle in K1 otherwise, absorbs the extra MACs.
+// passes, and each output value costs the CUDA cores three instructions plus
+// a byte split (the mma.sync kernel spent ~165 warp instructions per
+// (tile, channel, residue)).  The tensor pipe, idle in K1 otherwise, absorbs
+// the extra MACs.
 //
 // Work: groups g = (residue, position block); CTA b serves group b % G for
-// every unit (tile x 128 channels, or a tile PAIR x 64 channels when C = 64:
-// the two 64-channel boxes are the two 64-byte MN atoms of one N = 128
-// operand), so its Kr image is loaded once.  The G CTAs of a unit run side by
-// side and read the same patch (the second to fourth reads hit L2).
-// Warp roles (384 threads): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator,
-// 4-11 epilogue (lane quadrant x column half): tcgen05.ld -> limb
-// recombination -> one exact reduction -> byte planes -> swizzled staging ->
-// one TMA bulk tensor store per plane.
+// every unit (one tile x 64 channels), so its Kr operand is loaded once.
+// The G CTAs of a unit run side by side and read the same patch (the second
+// to fourth reads hit L2).  Warp roles (384 threads): 0 TMA producer, 1 MMA
+// issuer, 2 TMEM allocator, 3 bulk stores, 4-11 epilogue (lane quadrant x
+// column half): tcgen05.ld -> limb recombination -> one reduction -> byte
+// planes -> swizzled staging; mbarriers (no CTA barriers) link the roles.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -41,76 +41,119 @@
 #include "common.cuh"
 #include "kernels.h"
 
+// Diagnostic builds only (tools/variant_build.sh -DRNSW_K1_DIAG=n): 1 = no
+// staging stores / bulk stores, 2 = no conversion, 3 = one MMA per unit.
+#ifndef RNSW_K1_DIAG
+#define RNSW_K1_DIAG 0
+#endif
+
 namespace rnsw {
 
 namespace {
 
 constexpr int kUThreads = 384;
 constexpr int kGroupRows = 128;  // positions per group (MMA M)
-constexpr int kUnitN = 128;      // channels per unit (MMA N): 1 tile x 128 or 2 tiles x 64
+constexpr int kUnitN = 64;       // channels per unit (MMA N)
 
 struct K1UArgs {
   Geometry g;
-  int npos, mout, kp, ksteps, khalves, limbs, groups, npb;
-  int tile_stride;      // two-tile: bytes between the two 64-channel patch boxes (one MN atom each)
-  int units;            // two-tile: ceil(P / 2); one-tile: P * (Cp / 128)
-  int cblocks;          // one-tile: Cp / 128
+  int npos, mout, kp, ksteps, limbs, groups, npb;
+  int units;            // P * (Cp / 64)
+  int cblocks;          // Cp / 64
   int res_of[16];       // group -> residue
   int pb_of[16];        // group -> position block
   int plane_base[RNSW_MAX_RES];
   FastMod fm[RNSW_MAX_RES];
+  uint32_t mul0[RNSW_MAX_RES];    // ceil(2^32 / m): quotient estimate (kRel16)
+  int32_t bias_s1[RNSW_MAX_RES];  // 16-bit: bias = 127 (256 S1 + S2), see K1UMode
+  int32_t bias_s2[RNSW_MAX_RES];
   FastDiv div_img, div_tw, div_cb;
-  size_t group_bytes;
+  size_t group_bytes;   // [limb][128 rows][kp] plain bytes per group
 };
 
-// Shared-memory budget (bytes): A image, S patch stages, the store staging.
+// Output modes.  For 16-bit moduli each unit's accumulators start from a
+// bias made by one extra K = 32 MMA per limb with constant operands (A =
+// 127 everywhere, B rows beta_k with sum beta = S1 resp. S2), so D_hi / D_lo
+// come out as x + 127 (256 S1 + S2) and the epilogue's reduction is three
+// instructions per value; S1, S2 are chosen on the host so the bias is a
+// multiple of m plus the offset the mode needs and exceeds the largest |x|:
+//   kSym8  (8-bit moduli): v = symmetric residue in [-h, h], one s8 plane;
+//          no bias MMA: n = x + off (off = h mod m): v = (n - h) - floor(n/m) m.
+//   kSym16 (16-bit, stage API): v symmetric, planes lo = byte0(v + 128) ^ 0x80,
+//          hi = (v + 128) >> 8 (the reference's residues, bit for bit).
+//   kRel16 (16-bit, whole-layer path): w = n - q m with q = umulhi(n, ceil(2^32/m))
+//          -- floor(n/m) or one more, no shift -- so v = w - 128 lies in
+//          [-m-128, m-128) instead of [-h, h]: any representative is exact
+//          for the GEMM, whose single reduction still holds (limb hi in
+//          [-17, 16]: 256 A256 + A1 <= 512 (17*9 + 128*9) 256 + 512 (17*128 +
+//          128*128) < 1.9e8 < 2^28 for C <= 512; capi uses it for C <= 8192).
+enum K1UMode { kSym8 = 0, kSym16 = 1, kRel16 = 2 };
+
+// TMEM columns: [accumulator buffers 2 x limbs x 64 | Kr limbs x kp/4 | bias A 8]
 template <int kLimbs>
 struct K1UConfig {
-  static constexpr int kStageBytes = 256 * 128;  // K <= 256 pixel rows x 128 channel bytes
-  static constexpr int kABytes = kLimbs * 2 * 16384;
-  static constexpr int kStgBytes = kLimbs * kGroupRows * kUnitN;  // one byte plane per limb
-  static constexpr int kStages = (227 * 1024 - 2048 - kABytes - kStgBytes) / kStageBytes > 4
-                                     ? 4
-                                     : (227 * 1024 - 2048 - kABytes - kStgBytes) / kStageBytes;
+  static constexpr int kStageBytes = 256 * kUnitN;  // K <= 256 pixel rows x 64 channel bytes
+  static constexpr int kStages = 8;
+  // staging per unit PAIR (two tiles x 64 channels, or one tile x 128): the
+  // bulk stores then write 128-byte rows instead of 64-byte ones
+  static constexpr int kStgBytes = kLimbs * kGroupRows * 2 * kUnitN;
+  static constexpr int kBiasBytes = kLimbs == 2 ? 2 * 32 * kUnitN : 0;
   static constexpr int kAccCols = kLimbs * kUnitN;
-  static constexpr int kTmemCols = 2 * kAccCols <= 256 ? 256 : 512;
-  static constexpr size_t kSmem = 1024 + (size_t)kABytes + (size_t)kStages * kStageBytes + kStgBytes + 256;
-  static_assert(kStages >= 2, "shared memory");
+  static constexpr int kACol = 2 * kAccCols;          // Kr limb l at kACol + l * 64 (kp <= 256)
+  static constexpr int kBiasCol = kACol + kLimbs * 64;
+  static constexpr int kTmemCols = kLimbs == 2 ? 512 : 256;
+  static_assert(kBiasCol + 8 <= kTmemCols, "TMEM");
+  static constexpr size_t kSmem =
+      1024 + (size_t)kStages * kStageBytes + 2 * (size_t)kStgBytes + kBiasBytes + 256;
 };
 
-template <int kLimbs, bool kTwoTiles>
+template <int kMode>
 __global__ void __launch_bounds__(kUThreads, 1)
     input_umma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmV,
-                      const uint8_t* __restrict__ kr, K1UArgs args) {
+                      const __grid_constant__ CUtensorMap tmV2, const uint8_t* __restrict__ kr, K1UArgs args) {
+  constexpr int kLimbs = kMode == kSym8 ? 1 : 2;
   using Cfg = K1UConfig<kLimbs>;
   constexpr int S = Cfg::kStages;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + Cfg::kABytes;
-  uint8_t* stg = sB + S * Cfg::kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(stg + Cfg::kStgBytes);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned, derived from the shared array so stores stay STS
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sB = smem;                          // [S][256 rows][64 bytes]
+  uint8_t* stg = sB + S * Cfg::kStageBytes;    // [2][plane][128 rows][64 bytes]
+  uint8_t* sBias = stg + 2 * Cfg::kStgBytes;   // [B_hi | B_lo] 32 rows x 64 bytes each
+  uint64_t* full = reinterpret_cast<uint64_t*>(sBias + Cfg::kBiasBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;   // staging buffer written by the 8 epilogue warps
+  uint64_t* sempty = sfull + 2;   // staging buffer read by its bulk store
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int group = (int)(blockIdx.x % args.groups);
-  const int u_begin = (int)(blockIdx.x / args.groups), u_step = (int)(gridDim.x / args.groups);
+  // units come in pairs (2k, 2k+1): two consecutive tiles when Cp = 64, else
+  // two consecutive 64-channel blocks of one tile (Cp is a multiple of 128)
+  const int pr_begin = (int)(blockIdx.x / args.groups), pr_step = (int)(gridDim.x / args.groups);
+  const int npairs = (args.units + 1) / 2;
+#define RNSW_FOR_UNITS(u)                                              \
+  for (int pr_ = pr_begin; pr_ < npairs; pr_ += pr_step)               \
+    for (int h_ = 0, u = 2 * pr_; h_ < 2 && u < args.units; ++h_, ++u)
   const int res = args.res_of[group], pb = args.pb_of[group];
   const Geometry& g = args.g;
+  const FastMod fm = args.fm[res];
 
-  // the group's constant A image (kr: built on the host in the final layout)
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(kr + (size_t)group * args.group_bytes);
-    uint4* dst = reinterpret_cast<uint4*>(sA);
-    const int n16 = (int)(args.group_bytes / 16);
-    for (int i = threadIdx.x; i < n16; i += kUThreads) dst[i] = __ldg(src + i);
+  if (kLimbs == 2) {
+    // bias B operands: row k of B_hi = beta_k (sum S1), of B_lo = gamma_k
+    // (sum S2); uniform rows, so the swizzle is moot
+    const int s1 = args.bias_s1[res], s2 = args.bias_s2[res];
+    for (int i = threadIdx.x; i < 2 * 32 * kUnitN / 4; i += kUThreads) {
+      const int k = (i % (32 * kUnitN / 4)) / (kUnitN / 4), sum = i < 32 * kUnitN / 4 ? s1 : s2;
+      const int beta = sum / 32 + (k < (sum % 32) ? 1 : 0);
+      reinterpret_cast<uint32_t*>(sBias)[i] = (uint32_t)(uint8_t)(int8_t)beta * 0x01010101u;
+    }
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmX);
-    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(args.cblocks == 1 ? &tmV : &tmV2);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -118,26 +161,50 @@ __global__ void __launch_bounds__(kUThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);
+      mbar_init(&sfull[i], 16);  // 8 epilogue warps x 2 units of a pair
+      mbar_init(&sempty[i], 1);
     }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
-  fence_proxy_async();  // A image (generic stores) -> visible to the MMA (async proxy)
+  fence_proxy_async();  // bias operands (generic stores) -> visible to the MMA (async proxy)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // unit -> first tile, channel offset
-  auto unit_tile = [&](int u, int& p, int& c0) {
-    if (kTwoTiles) {
-      p = 2 * u;
-      c0 = 0;
-    } else {
-      const int q = (int)fdiv((uint32_t)u, args.div_cb);
-      p = q;
-      c0 = (u - q * args.cblocks) * 128;
+  // epilogue thread geometry: lane quadrant q, column half hh
+  const int q = warp & 3, hh = (warp - 4) >> 2;
+  if (warp >= 4) {
+    // the group's Kr operand into TMEM: thread = row (position), limb hh
+    // (8-bit: one limb, written by hh = 0), kp/4 columns of four K bytes
+    const int row = q * 32 + lane;
+    const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16);
+    if (hh < kLimbs) {
+      const uint4* src = reinterpret_cast<const uint4*>(kr + (size_t)group * args.group_bytes +
+                                                        ((size_t)hh * kGroupRows + row) * args.kp);
+      for (int c8 = 0; c8 < args.kp / 32; ++c8) {  // 8 columns = 32 K bytes per store
+        const uint4 w0 = __ldg(src + 2 * c8), w1 = __ldg(src + 2 * c8 + 1);
+        const uint32_t v[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        tmem_st8(trow + Cfg::kACol + hh * 64 + c8 * 8, v);
+      }
     }
+    if (kLimbs == 2 && hh == 0) {
+      const uint32_t v[8] = {0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu,
+                             0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu, 0x7F7F7F7Fu};
+      tmem_st8(trow + Cfg::kBiasCol, v);
+    }
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  // unit -> tile, channel offset
+  auto unit_tile = [&](int u, int& p, int& c0) {
+    const int qq = (int)fdiv((uint32_t)u, args.div_cb);
+    p = qq;
+    c0 = (u - qq * args.cblocks) * kUnitN;
   };
   // tile p -> image and the patch's top-left canvas coordinate (may be
   // negative: TMA fills the padding with zeros)
@@ -153,22 +220,16 @@ __global__ void __launch_bounds__(kUThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      const uint32_t bytes = (uint32_t)(args.npos * 128);
+      const uint32_t bytes = (uint32_t)(args.npos * kUnitN);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = u_begin; u < args.units; u += u_step) {
-        int p, c0;
+      RNSW_FOR_UNITS(u) {
+        int p, c0, b, h0, w0;
         unit_tile(u, p, c0);
+        tile_origin(p, b, h0, w0);
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], bytes);
-        uint8_t* dst = sB + stage * Cfg::kStageBytes;
-#pragma unroll
-        for (int t = 0; t < (kTwoTiles ? 2 : 1); ++t) {
-          // tile p + t; a tile past P reads as zeros (image coordinate B is out of range)
-          int b = g.B, h0 = 0, w0 = 0;
-          if (p + t < (int)g.P) tile_origin(p + t, b, h0, w0);
-          tma_load_4d(dst + t * args.tile_stride, &tmX, &full[stage], c0, w0, h0, b);
-        }
+        tma_load_4d(sB + stage * Cfg::kStageBytes, &tmX, &full[stage], c0, w0, h0, b);
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -176,119 +237,159 @@ __global__ void __launch_bounds__(kUThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = idesc_i8x(128, kUnitN, true, true, false, true);  // A K-major, B MN-major
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int u = u_begin; u < args.units; u += u_step, ++it) {
-        const int as = it & 1;
-        mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        const uint32_t d0 = tmem_base + as * Cfg::kAccCols;
-        const uint32_t b_base = smem_u32(sB + stage * Cfg::kStageBytes);
-        for (int ks = 0; ks < args.ksteps; ++ks) {
-          const uint64_t db = kTwoTiles ? umma_desc_mn_sw64(b_base + ks * 32 * 64, args.tile_stride)
-                                        : umma_desc_mn_sw128(b_base + ks * 32 * 128);
+    // ---------------- MMA issuer (warp-collective: descriptors stay uniform) ----------------
+    constexpr uint32_t idesc = idesc_i8x(128, kUnitN, true, true, false, true);  // A K-major (TMEM), B MN-major
+    // descriptors advance by adding the byte offset / 16 to the start-address field
+    const uint64_t db0 = umma_desc_mn_sw64(smem_u32(sB), 16);
+    const uint64_t dbh = umma_desc_mn_sw64(smem_u32(sBias), 16);
+    const uint64_t dbl = umma_desc_mn_sw64(smem_u32(sBias + 32 * kUnitN), 16);
+    constexpr uint32_t kBStep = (32 * kUnitN) >> 4;  // one K-step of the patch
+    constexpr uint32_t kStageStep = Cfg::kStageBytes >> 4;
+    const uint32_t ta = tmem_base + Cfg::kACol;
+    const int ksteps = args.ksteps;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    RNSW_FOR_UNITS(u) {
+      const int as = it & 1;
+      mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      const uint32_t d0 = tmem_base + as * Cfg::kAccCols;
+      const uint64_t db_stage = db0 + (uint64_t)(stage * kStageStep);
+      if (kLimbs == 2) {  // the bias: D_hi = 127 S1, D_lo = 127 S2 (overwrites the buffer)
+        mma_i8_ts_warp(d0, tmem_base + Cfg::kBiasCol, dbh, idesc, 0u);
+        mma_i8_ts_warp(d0 + kUnitN, tmem_base + Cfg::kBiasCol, dbl, idesc, 0u);
+      }
 #pragma unroll
-          for (int l = 0; l < kLimbs; ++l) {
-            const uint32_t a_addr = smem_u32(sA) + (l * args.khalves + (ks >> 2)) * 16384 + (ks & 3) * 32;
-            mma_i8(d0 + l * kUnitN, umma_desc_kmajor(a_addr, 128), db, idesc, ks > 0 ? 1u : 0u);
-          }
-        }
-        mma_commit(&empty[stage]);
-        mma_commit(&tfull[as]);
-        if (++stage == S) {
-          stage = 0;
-          phase ^= 1;
+      for (int ks = 0; ks < 8; ++ks) {
+        if (ks < (RNSW_K1_DIAG == 3 ? 1 : ksteps)) {
+          const uint64_t db = db_stage + (uint64_t)(ks * kBStep);
+          mma_i8_ts_warp(d0, ta + ks * 8, db, idesc, (kLimbs == 2 || ks > 0) ? 1u : 0u);
+          if (kLimbs == 2) mma_i8_ts_warp(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, 1u);
         }
       }
+      mma_commit_warp(&empty[stage]);
+      mma_commit_warp(&tfull[as]);
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1;
+      }
+      ++it;
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ---------------- bulk stores of the staged V rows (one per unit pair) ----------------
+      const bool two = args.cblocks == 1;
+      int jt = 0;
+      for (int pr = pr_begin; pr < npairs; pr += pr_step, ++jt) {
+        int p, c0;
+        unit_tile(2 * pr, p, c0);
+        const int sb = jt & 1;
+        mbar_wait(&sfull[sb], (jt >> 1) & 1);
+        uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
+#pragma unroll
+        for (int pl = 0; pl < (RNSW_K1_DIAG == 1 ? 0 : kLimbs); ++pl)
+          tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0, p, pb * kGroupRows,
+                       args.plane_base[res] + pl);
+        bulk_commit();
+        bulk_wait_read<0>();  // the staging buffer may be rewritten
+        mbar_arrive(&sempty[sb]);
+      }
+      bulk_wait<0>();
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: 8 warps = 4 lane quadrants x 2 column halves ----------------
-    const int q = warp & 3, hh = (warp - 4) >> 2;
+    // ---------------- epilogue: 8 warps = 4 lane quadrants x 2 channel halves ----------------
     const int row = q * 32 + lane;  // position within the group's block
-    const FastMod fm = args.fm[res];
-    const int32_t wshift = 128 - fm.h;  // w = v + 128 from r' = v + h
-    const int etid = threadIdx.x - 128;
-    int it = 0;
-    for (int u = u_begin; u < args.units; u += u_step, ++it) {
-      int p, c0;
-      unit_tile(u, p, c0);
+    const uint32_t mul0 = args.mul0[res];
+    auto convert = [&](const int32_t (&a)[16], const int32_t (&b)[16], uint32_t* lo, uint32_t* hi) {
+      int32_t w[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        if (kMode == kRel16) {
+          const uint32_t n = (uint32_t)(a[e] * 256 + b[e]);  // x + bias, bias = 128 (mod m)
+          w[e] = (int32_t)(__umulhi(n, mul0) * fm.negm + n);  // = x + 128 (mod m), in [-m, m)
+        } else if (kMode == kSym16) {
+          const int32_t r = red_pos_biased(a[e] * 256 + b[e], fm);  // (x + h) mod m
+          w[e] = r + (128 - fm.h);                                  // v + 128
+        } else {
+          const uint32_t n = (uint32_t)(b[e] + fm.off);  // x + off, off = h (mod m)
+          const uint32_t qq = __umulhi(n, fm.mul) >> fm.shift;
+          w[e] = (int32_t)(qq * fm.negm + (n - (uint32_t)fm.h));  // v in [-h, h]
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t p01 = __byte_perm((uint32_t)w[4 * e], (uint32_t)w[4 * e + 1], 0x5140);
+        const uint32_t p23 = __byte_perm((uint32_t)w[4 * e + 2], (uint32_t)w[4 * e + 3], 0x5140);
+        const uint32_t b0 = __byte_perm(p01, p23, 0x5410);
+        lo[e] = kLimbs == 2 ? b0 ^ 0x80808080u : b0;  // low byte of v
+        hi[e] = __byte_perm(p01, p23, 0x7632);         // (v + 128) >> 8
+      }
+    };
+    const bool two = args.cblocks == 1;
+    int it = 0, jt = -1;
+    RNSW_FOR_UNITS(u) {
+      if (h_ == 0) ++jt;
       const int as = it & 1;
       mbar_wait(&tfull[as], (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Cfg::kAccCols + hh * 64;
-      uint32_t lo[16], hi[16];  // [chunk of 16 channels][word]
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        int32_t a[16], b[16];
-        if (kLimbs == 2) {
-          tmem_ld16(taddr + ch * 16, a);          // D_hi
-          tmem_ld16(taddr + kUnitN + ch * 16, b);  // D_lo
-        } else {
-          tmem_ld16(taddr + ch * 16, b);
-        }
-        tmem_ld_wait();
-        if (ch == 3) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[as]);
-        }
-        int32_t w[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int32_t x = kLimbs == 2 ? a[e] * 256 + b[e] : b[e];
-          const int32_t r = red_pos_biased(x + fm.off, fm);  // (x + h) mod m in [0, m)
-          w[e] = kLimbs == 2 ? r + wshift : r - fm.h;        // 16-bit: w = v + 128; 8-bit: v
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t p01 = __byte_perm((uint32_t)w[4 * e], (uint32_t)w[4 * e + 1], 0x5140);
-          const uint32_t p23 = __byte_perm((uint32_t)w[4 * e + 2], (uint32_t)w[4 * e + 3], 0x5140);
-          const uint32_t b0 = __byte_perm(p01, p23, 0x5410);
-          lo[ch * 4 + e] = kLimbs == 2 ? b0 ^ 0x80808080u : b0;  // low byte of v
-          hi[ch * 4 + e] = __byte_perm(p01, p23, 0x7632);         // (v + 128) >> 8
-        }
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Cfg::kAccCols + hh * 32;
+      uint32_t lo[8], hi[8];  // [chunk of 16 channels][word]
+      int32_t a0[16], b0[16], a1[16], b1[16];
+      if (kLimbs == 2) {
+        tmem_ld16(taddr, a0);
+        tmem_ld16(taddr + kUnitN, b0);
+        tmem_ld16(taddr + 16, a1);
+        tmem_ld16(taddr + kUnitN + 16, b1);
+      } else {
+        tmem_ld16(taddr, b0);
+        tmem_ld16(taddr + 16, b1);
       }
-      // staging must be free: the previous unit's bulk store has read it
-      if (etid == 0) bulk_wait_read<0>();
-      named_bar_sync(1, 256);
-      {
+      tmem_ld_wait();
+      // hand the buffer back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (RNSW_K1_DIAG != 2) {
+        convert(a0, b0, lo, hi);
+        convert(a1, b1, lo + 4, hi + 4);
+      } else {
 #pragma unroll
-        for (int pl = 0; pl < kLimbs; ++pl) {
-          uint8_t* base = stg + pl * (kGroupRows * kUnitN);
+        for (int e = 0; e < 8; ++e) lo[e] = hi[e] = (uint32_t)(a0[e] ^ b1[e]);
+      }
+      // the pair's staging buffer must be free: its previous bulk store has read it
+      const int sb = jt & 1;
+      if (h_ == 0) mbar_wait(&sempty[sb], ((jt >> 1) & 1) ^ 1);
+      uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            const uint32_t* src = pl == 0 ? lo : hi;
-            const uint4 v4 = make_uint4(src[ch * 4], src[ch * 4 + 1], src[ch * 4 + 2], src[ch * 4 + 3]);
-            uint32_t off;
-            if (kTwoTiles) {
-              // [pos][tile][64 channels], 64-byte rows, 64B swizzle
-              const uint32_t r64 = (uint32_t)(row * 2 + hh);
-              off = r64 * 64 + ((((uint32_t)ch) ^ ((r64 >> 1) & 3u)) << 4);
-            } else {
-              // [pos][128 channels], 128-byte rows, 128B swizzle
-              const uint32_t c16 = (uint32_t)(hh * 4 + ch);
-              off = (uint32_t)row * 128 + ((c16 ^ ((uint32_t)row & 7u)) << 4);
-            }
-            *reinterpret_cast<uint4*>(base + off) = v4;
+      for (int pl = 0; pl < (RNSW_K1_DIAG == 1 ? 0 : kLimbs); ++pl) {
+        uint8_t* base = sbuf + pl * (kGroupRows * 2 * kUnitN);
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const uint32_t* src = pl == 0 ? lo : hi;
+          const uint4 v4 = make_uint4(src[ch * 4], src[ch * 4 + 1], src[ch * 4 + 2], src[ch * 4 + 3]);
+          uint32_t off;
+          if (two) {
+            // [pos][tile h_][64 channels]: 64-byte rows, 64B swizzle (chunk ^= (row >> 1) & 3)
+            const uint32_t r64 = (uint32_t)(row * 2 + h_), c16 = (uint32_t)(hh * 2 + ch);
+            off = r64 * 64 + ((c16 ^ ((r64 >> 1) & 3u)) << 4);
+          } else {
+            // [pos][128 channels of blocks h_]: 128-byte rows, 128B swizzle (chunk ^= row & 7)
+            const uint32_t c16 = (uint32_t)(h_ * 4 + hh * 2 + ch);
+            off = (uint32_t)row * 128 + ((c16 ^ ((uint32_t)row & 7u)) << 4);
           }
+          *reinterpret_cast<uint4*>(base + off) = v4;
         }
       }
-      fence_proxy_async();
-      named_bar_sync(1, 256);
-      if (etid == 0) {
-#pragma unroll
-        for (int pl = 0; pl < kLimbs; ++pl)
-          tma_store_4d(&tmV, stg + pl * (kGroupRows * kUnitN), c0, p, pb * kGroupRows,
-                       args.plane_base[res] + (kLimbs == 2 ? (pl == 0 ? 0 : 1) : 0));
-        bulk_commit();
+      fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sfull[sb]);
+        if (h_ == 0 && u + 1 >= args.units) mbar_arrive(&sfull[sb]);  // a lone last unit
       }
+      ++it;
     }
-    if (etid == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -318,8 +419,9 @@ cudaError_t build_kr_images(PlanHost& plan) {
   plan.kr_groups = d.n_res * plan.kr_npb;
   plan.kr_kp = (npos + 31) / 32 * 32;
   plan.kr_khalves = (plan.kr_kp + 127) / 128;
-  plan.kr_group_bytes = (size_t)plan.kr_limbs * plan.kr_khalves * 16384;
+  plan.kr_group_bytes = (size_t)plan.kr_limbs * kGroupRows * plan.kr_kp;
   std::vector<uint8_t> img((size_t)plan.kr_groups * plan.kr_group_bytes, 0);
+  for (int r = 0; r < RNSW_MAX_RES; ++r) plan.kr_xmax[r] = 0;
   for (int r = 0; r < d.n_res; ++r) {
     const int64_t m = d.res[r].modulus;
     for (int pbk = 0; pbk < plan.kr_npb; ++pbk) {
@@ -328,24 +430,24 @@ cudaError_t build_kr_images(PlanHost& plan) {
         const int pos = pbk * kGroupRows + row;
         if (pos >= npos) break;
         const int i = pos / N, j = pos % N;
+        int64_t xrow = 0;
         for (int pix = 0; pix < npos; ++pix) {
           const int a = pix / N, b = pix % N;
           const int64_t v = sym_host((int64_t)d.res[r].bt[i * RNSW_MAX_N + a] * d.res[r].bt[j * RNSW_MAX_N + b], m);
           int8_t limb[2];
           if (plan.kr_limbs == 1) {
             limb[0] = (int8_t)v;
+            xrow += 128 * (v < 0 ? -v : v);
           } else {
             const int64_t h = (v + 128 + 256 * 64) / 256 - 64;  // floor((v + 128) / 256)
             limb[0] = (int8_t)h;            // limb 0: high (x 256)
             limb[1] = (int8_t)(v - 256 * h);  // limb 1: low
+            xrow += 128 * (256 * (h < 0 ? -h : h) + (limb[1] < 0 ? -limb[1] : limb[1]));
           }
-          const int kh = pix / 128, kb = pix % 128;
-          for (int l = 0; l < plan.kr_limbs; ++l) {
-            const size_t off = (size_t)(l * plan.kr_khalves + kh) * 16384 + row * 128 +
-                               ((((kb >> 4) ^ (row & 7)) << 4) | (kb & 15));
-            gimg[off] = (uint8_t)limb[l];
-          }
+          for (int l = 0; l < plan.kr_limbs; ++l)
+            gimg[((size_t)l * kGroupRows + row) * plan.kr_kp + pix] = (uint8_t)limb[l];
         }
+        if (xrow > plan.kr_xmax[r]) plan.kr_xmax[r] = xrow;
       }
     }
   }
@@ -371,27 +473,24 @@ bool umma_input_ok(const PlanHost& plan, const Geometry& g) {
   static const bool off = getenv("RNSW_K1_MMA_SYNC") != nullptr;  // A/B switch: the mma.sync kernel
   if (off || force_generic() || plan.d_kr == nullptr || g.layout != 0) return false;
   if (plan.kr_groups > 16) return false;
-  return g.C == 64 || (g.C % 128) == 0;
+  return g.C % 64 == 0;
 }
 
 cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
-                                        cudaStream_t s) {
+                                        cudaStream_t s, bool relaxed) {
   const PlanDevice& d = plan.dev;
-  const bool two = g.C == 64;
   K1UArgs a{};
   a.g = g;
   a.npos = d.n * d.n;
   a.mout = d.m_out;
-  a.tile_stride = (plan.kr_kp * 64 + 1023) / 1024 * 1024;
   a.kp = plan.kr_kp;
   a.ksteps = plan.kr_kp / 32;
-  a.khalves = plan.kr_khalves;
   a.limbs = plan.kr_limbs;
   a.groups = plan.kr_groups;
   a.npb = plan.kr_npb;
   a.group_bytes = plan.kr_group_bytes;
-  a.cblocks = two ? 1 : g.Cp / 128;
-  const int64_t units = two ? (g.P + 1) / 2 : g.P * a.cblocks;
+  a.cblocks = g.Cp / kUnitN;
+  const int64_t units = g.P * a.cblocks;
   if (units >= (1ll << 31) || g.P >= (1ll << 31)) return cudaErrorInvalidValue;
   a.units = (int)units;
   for (int gi = 0; gi < a.groups; ++gi) {
@@ -402,6 +501,20 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
     a.plane_base[r] = d.res[r].plane_base;
     const ResidueTables& t = d.res[r];
     a.fm[r] = FastMod{t.red_mul, t.red_shift, t.red_off, t.modulus, t.half, t.red_negm};
+    a.mul0[r] = (uint32_t)(((1ull << 32) + t.modulus - 1) / t.modulus);
+    if (plan.kr_limbs == 2) {
+      // bias = 127 T with T = 256 S1 + S2, T >= xmax / 127 and bias = target
+      // (mod m): target h (kSym16: n mod m = (x + h) mod m) or 128 (kRel16)
+      const int64_t m = t.modulus, target = relaxed ? 128 : t.half;
+      int64_t inv127 = 1;
+      while ((127 * inv127) % m != 1) ++inv127;
+      const int64_t want = target * inv127 % m;
+      const int64_t t0 = (plan.kr_xmax[r] + 126) / 127;
+      const int64_t T = t0 + ((want - t0) % m + m) % m;
+      if ((T >> 8) > 4064 || 127 * T + plan.kr_xmax[r] >= (1ll << 30)) return cudaErrorInvalidValue;
+      a.bias_s1[r] = (int32_t)(T >> 8);
+      a.bias_s2[r] = (int32_t)(T & 255);
+    }
   }
   a.div_img = make_fastdiv((uint32_t)(g.th * g.tw));
   a.div_tw = make_fastdiv((uint32_t)g.tw);
@@ -411,45 +524,53 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   if (encode == nullptr) return cudaErrorInvalidValue;
   CUtensorMap tmX, tmV;
   {
-    // x NHWC as (C, W, H, B); box = 64 or 128 channels x N x N x 1
+    // x NHWC as (C, W, H, B); box = 64 channels x N x N x 1
     cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.B};
     cuuint64_t strides[3] = {(cuuint64_t)g.C, (cuuint64_t)g.W * g.C, (cuuint64_t)g.H * g.W * g.C};
-    cuuint32_t box[4] = {(cuuint32_t)(two ? 64 : 128), (cuuint32_t)d.n, (cuuint32_t)d.n, 1};
+    cuuint32_t box[4] = {(cuuint32_t)kUnitN, (cuuint32_t)d.n, (cuuint32_t)d.n, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(x), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, two ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  CUtensorMap tmV2;
   {
-    // V as (Cp, P, npos, planes); box = channels x tiles x 128 positions x 1 plane
+    // V as (Cp, P, npos, planes); a unit pair's box = 64 channels x 2 tiles x
+    // 128 positions x 1 plane (Cp = 64, 64B swizzle) or 128 channels x 1 tile
+    // x 128 positions x 1 plane (128B swizzle)
     const int npos = d.n * d.n;
     cuuint64_t dims[4] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P, (cuuint64_t)npos, (cuuint64_t)d.n_planes};
     cuuint64_t strides[3] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P * g.Cp, (cuuint64_t)g.P * g.Cp * npos};
-    cuuint32_t box[4] = {(cuuint32_t)(two ? 64 : 128), (cuuint32_t)(two ? 2 : 1), (cuuint32_t)kGroupRows, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)kUnitN, 2, (cuuint32_t)kGroupRows, 1};
     if (encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               two ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
+    cuuint32_t box2[4] = {(cuuint32_t)(2 * kUnitN), 1, (cuuint32_t)kGroupRows, 1};
+    if (g.Cp >= 128 && encode(&tmV2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims, strides, box2, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    if (g.Cp < 128) tmV2 = tmV;
   }
   const int sms = num_sms_current();
   const int per_group = sms / a.groups > 0 ? sms / a.groups : 1;
   int64_t grid = (int64_t)per_group * a.groups;
-  const int64_t need = (int64_t)a.units * a.groups;
+  const int64_t need = (int64_t)((a.units + 1) / 2) * a.groups;
   if (grid > need) grid = need;
   grid = (grid + a.groups - 1) / a.groups * a.groups;
   auto run = [&](auto kern, size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)grid, kUThreads, smem, s>>>(tmX, tmV, plan.d_kr, a);
+    kern<<<(unsigned)grid, kUThreads, smem, s>>>(tmX, tmV, tmV2, plan.d_kr, a);
     return cudaGetLastError();
   };
   if (plan.kr_limbs == 2)
-    return two ? run(input_umma_kernel<2, true>, K1UConfig<2>::kSmem)
-               : run(input_umma_kernel<2, false>, K1UConfig<2>::kSmem);
-  return two ? run(input_umma_kernel<1, true>, K1UConfig<1>::kSmem)
-             : run(input_umma_kernel<1, false>, K1UConfig<1>::kSmem);
+    return relaxed ? run(input_umma_kernel<kRel16>, K1UConfig<2>::kSmem)
+                   : run(input_umma_kernel<kSym16>, K1UConfig<2>::kSmem);
+  return run(input_umma_kernel<kSym8>, K1UConfig<1>::kSmem);
 }
 
 }  // namespace rnsw

@@ -52,6 +52,7 @@ struct PlanHost {
   int kr_khalves;         // 128-byte K chunks per A row: ceil(kr_kp / 128)
   int kr_limbs;           // 1 (m < 256) or 2 (balanced s8 limbs)
   size_t kr_group_bytes;  // kr_limbs * kr_khalves * 16 KB
+  int64_t kr_xmax[RNSW_MAX_RES];  // max |Kr d| over positions (|d| <= 128): the accumulator bias floor
 };
 
 // Build / release PlanHost::d_kr (input_umma.cu); a plan without it keeps
@@ -64,7 +65,7 @@ cudaError_t launch_filter_transform(const PlanHost& plan, const int8_t* w, int C
 cudaError_t launch_filter_import(const PlanHost& plan, int res, const int16_t* u_nnck, int C, int K, int Cp,
                                  int8_t* U, cudaStream_t s);
 cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
-                                   cudaStream_t s);
+                                   cudaStream_t s, bool relaxed = false);
 // pos_out: 16-bit residues as y mod m in [0, m) instead of symmetric (whole-layer
 // path only; the stage API keeps the reference's symmetric residues)
 cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp,
@@ -76,8 +77,10 @@ cudaError_t launch_output_transform_tc(const PlanHost& plan, const Geometry& g, 
                                        int16_t* y_res, cudaStream_t s, int8_t* out8 = nullptr, int shift = 0,
                                        int pool = 0);
 bool umma_input_ok(const PlanHost& plan, const Geometry& g);
+// relaxed (whole-layer path, 16-bit moduli, C <= 8192): V residues in
+// [-m-128, m-128) instead of [-h, h] (see input_umma.cu K1UMode)
 cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
-                                        cudaStream_t s);
+                                        cudaStream_t s, bool relaxed = false);
 cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
                                       cudaStream_t s);
 bool tc_output_ok(const PlanDevice& d);

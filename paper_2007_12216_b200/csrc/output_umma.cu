@@ -398,12 +398,13 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
   auto launch = [&](auto kern, int smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    // persistent grid: as many CTAs as are co-resident (2 per SM for the int8
-    // modes; the int32 mode's 26 KB staging tile leaves room for only 1)
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThr, smem);
+    // persistent grid: as many CTAs as are co-resident -- 2 per SM for the
+    // int8 modes (launch bounds), 1 for the int32 mode, whose 26 KB staging
+    // tile does not fit twice in the 228 KB of shared memory (1 KB reserved
+    // per CTA)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
+    const int per_sm = (228 * 1024) / (smem + 1024) >= 2 ? 2 : 1;
     const unsigned grid = (unsigned)std::min<int64_t>(a.units, (int64_t)per_sm * num_sms);
     kern<<<grid, kThr, smem, s>>>(plan.d_plan, tm, a);
     return cudaGetLastError();

@@ -400,9 +400,10 @@ cudaError_t launch_filter_import(const PlanHost& plan, int res, const int16_t* u
 }
 
 cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, const int8_t* x, int8_t* V,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, bool relaxed) {
   if (tc_output_ok(plan.dev) && !force_generic()) {
-    if (umma_input_ok(plan, g)) return launch_input_transform_umma(plan, g, x, V, s);
+    if (umma_input_ok(plan, g))
+      return launch_input_transform_umma(plan, g, x, V, s, relaxed && plan.kr_limbs == 2 && g.C <= 8192);
     return launch_input_transform_tc(plan, g, x, V, s);
   }
   const int npos = plan.dev.n * plan.dev.n;

@@ -106,29 +106,9 @@ class VGG16Rns:
         output transform in the planar Mw8 layout (include/rnsw.h)."""
         return _native.lib().rnsw_mw8_supported(self.plan.handle) == 1
 
-    def _staged_product(self, timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, mb, s):
-        """Stages 1-2 of one layer as rnsw_conv_forward runs them: the
-        tensor-core GEMM split, or for C <= 4 the compact transform + CUDA-core
-        product (kind "product"), into Mw8 when the plan uses it."""
-        l = _native.lib()
-        vp = _native.c_void_p
-        mw8 = self._mw8()
-        if c <= 4:
-            timed("input_transform", i, lambda: l.rnsw_input_transform_compact(
-                self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
-            product = l.rnsw_small_channel_product_mw8 if mw8 else l.rnsw_small_channel_product
-            timed("product", i, lambda: product(
-                self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), mb, s))
-            return
-        timed("input_transform", i, lambda: l.rnsw_input_transform(
-            self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, 1, _native.LAYOUT_NHWC, vp(v_ptr), vb, s))
-        gemm = l.rnsw_winograd_gemm_mw8 if mw8 else l.rnsw_winograd_gemm
-        timed("gemm", i, lambda: gemm(
-            self.plan.handle, vp(v_ptr), vp(bank.data.data_ptr()), tiles, c, k, vp(m_ptr), mb, s))
-
     def forward_staged(self, x, record):
-        """Same launches as forward(), one C-ABI stage call per kernel with a
-        CUDA event pair around each (``record(kind, layer, start, end)``)."""
+        """forward() with CUDA events between the kernels of every layer
+        (``record(kind, layer, start, end)``), the glue kernel separately."""
         torch = _torch()
         l = _native.lib()
         vp = _native.c_void_p
@@ -138,28 +118,26 @@ class VGG16Rns:
         ws = bufs["ws"]
         cur = x.contiguous()
         nl = len(self.cfg.layers)
-
-        def timed(kind, i, fn):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            _native.check(fn())
-            b.record()
-            record(kind, i, a, b)
-
         for i, ((name, side, c, k, pool), bank) in enumerate(zip(self.cfg.layers, self.banks)):
             y = bufs["y"][: batch * side * side * k].view(batch, side, side, k)
-            tiles = batch * math.ceil(side / self.cfg.tile_m) ** 2
-            vb = (l.rnsw_v_bytes(self.plan.handle, tiles, c) + 255) // 256 * 256
-            v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
-            self._staged_product(timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, ws.numel() - vb, s)
-            out_t = l.rnsw_output_transform_mw8 if self._mw8() else l.rnsw_output_transform
-            timed("output_transform", i, lambda: out_t(
-                self.plan.handle, vp(m_ptr), batch, side, side, k, 1, _native.LAYOUT_NHWC, vp(y.data_ptr()), s))
+            ev, handles = self._layer_events()
+            ev[0].record()
+            _native.check(l.rnsw_conv_forward_ev(self.plan.handle, vp(cur.data_ptr()), batch, side, side, c, k, 1,
+                                                 _native.LAYOUT_NHWC, vp(bank.data.data_ptr()), vp(y.data_ptr()),
+                                                 vp(ws.data_ptr()), ws.numel(), s, handles))
+            ev[3].record()
+            record("input_transform", i, ev[0], ev[1])
+            record("product" if c <= 4 else "gemm", i, ev[1], ev[2])
+            record("output_transform", i, ev[2], ev[3])
             oside = side // 2 if pool else side
             nxt = bufs["out"] if i == nl - 1 else \
                 bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
-            timed("glue", i, lambda: l.rnsw_requant_pool(vp(y.data_ptr()), batch, side, side, k, self.cfg.shifts[i],
-                                                         1 if pool else 0, vp(nxt.data_ptr()), s))
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            _native.check(l.rnsw_requant_pool(vp(y.data_ptr()), batch, side, side, k, self.cfg.shifts[i],
+                                              1 if pool else 0, vp(nxt.data_ptr()), s))
+            g1.record()
+            record("glue", i, g0, g1)
             cur = nxt
         return cur
 
@@ -277,9 +255,21 @@ class VGG16Rns:
                 d2h[j].record(copy)
         comp.wait_stream(copy)
 
-    def forward_fused_staged(self, x, record):
-        """forward_fused() with a CUDA event pair around every kernel."""
+    def _layer_events(self):
+        """Four timing events (start, after K1, after K3, end); the middle two
+        are re-recorded inside the C ABI (rnsw_conv_forward*_ev), so the
+        stage times belong to exactly the kernel chain the untimed call runs."""
         torch = _torch()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        for e in ev[1:3]:
+            e.record()  # create the CUDA events (torch creates them lazily)
+        handles = (_native.c_void_p * 2)(ev[1]._as_parameter_.value, ev[2]._as_parameter_.value)
+        return ev, handles
+
+    def forward_fused_staged(self, x, record):
+        """forward_fused() with CUDA events between the kernels of every layer
+        (``record(kind, layer, start, end)``): kinds input_transform, gemm or
+        product (C <= 4), output_transform (with the fused glue)."""
         l = _native.lib()
         vp = _native.c_void_p
         batch = int(x.shape[0])
@@ -288,26 +278,20 @@ class VGG16Rns:
         ws = bufs["ws"]
         cur = x.contiguous()
         nl = len(self.cfg.layers)
-
-        def timed(kind, i, fn):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            _native.check(fn())
-            b.record()
-            record(kind, i, a, b)
-
         for i, ((name, side, c, k, pool), bank) in enumerate(zip(self.cfg.layers, self.banks)):
-            tiles = batch * math.ceil(side / self.cfg.tile_m) ** 2
-            vb = (l.rnsw_v_bytes(self.plan.handle, tiles, c) + 255) // 256 * 256
-            v_ptr, m_ptr = ws.data_ptr(), ws.data_ptr() + vb
             oside = side // 2 if pool else side
             nxt = bufs["out"] if i == nl - 1 else \
                 bufs["act"][i % 2][: batch * oside * oside * k].view(batch, oside, oside, k)
-            self._staged_product(timed, i, cur, batch, side, c, k, tiles, bank, v_ptr, vb, m_ptr, ws.numel() - vb, s)
-            out_t = l.rnsw_output_transform_requant_mw8 if self._mw8() else l.rnsw_output_transform_requant
-            timed("output_transform", i, lambda: out_t(
-                self.plan.handle, vp(m_ptr), batch, side, side, k, 1, self.cfg.shifts[i], 1 if pool else 0,
-                vp(nxt.data_ptr()), s))
+            ev, handles = self._layer_events()
+            ev[0].record()
+            _native.check(l.rnsw_conv_forward_requant_ev(self.plan.handle, vp(cur.data_ptr()), batch, side, side, c,
+                                                         k, 1, vp(bank.data.data_ptr()), self.cfg.shifts[i],
+                                                         1 if pool else 0, vp(nxt.data_ptr()), vp(ws.data_ptr()),
+                                                         ws.numel(), s, handles))
+            ev[3].record()
+            record("input_transform", i, ev[0], ev[1])
+            record("product" if c <= 4 else "gemm", i, ev[1], ev[2])
+            record("output_transform", i, ev[2], ev[3])
             cur = nxt
         return cur
 
