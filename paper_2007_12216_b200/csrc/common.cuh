@@ -159,6 +159,23 @@ RNSW_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Same wait with a suspend-time hint: the thread sleeps in try_wait (up to
+// `ns` nanoseconds per attempt, woken when the phase completes) instead of
+// re-issuing it in a tight loop -- waiting epilogue warps then leave their
+// issue slots to the warps that have work.
+RNSW_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 20000) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n\t"
+      "}" ::"r"(addr),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+
 RNSW_DEV void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
 }
