@@ -298,9 +298,11 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
   if (e == cudaSuccess) e = cudaMalloc(&plan->host.d_plan, sizeof(PlanDevice));
   if (e == cudaSuccess) e = cudaMemcpy(plan->host.d_plan, &d, sizeof(d), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = rnsw::build_kr_images(plan->host);
+  if (e == cudaSuccess) e = rnsw::build_kra_images(plan->host);
   if (e != cudaSuccess) {
     if (plan->host.d_plan) cudaFree(plan->host.d_plan);
     rnsw::free_kr_images(plan->host);
+    rnsw::free_kra_images(plan->host);
     delete plan;
     return cuda_fail(e, "rnsw_plan_create");
   }
@@ -312,6 +314,7 @@ void rnsw_plan_destroy(rnsw_plan* plan) {
   if (plan == nullptr) return;
   if (plan->host.d_plan) cudaFree(plan->host.d_plan);
   rnsw::free_kr_images(plan->host);
+  rnsw::free_kra_images(plan->host);
   delete plan;
 }
 
@@ -495,6 +498,11 @@ int conv_forward_impl(const rnsw_plan* plan, const rnsw::Geometry& g, const int8
   if (workspace_bytes < vb + mb) return fail(RNSW_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, vb + mb);
   int8_t* V = static_cast<int8_t*>(workspace);
   int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
+  if (rnsw::kron_output_ok(plan->host, g, 0)) {
+    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true, ev)) return rc;
+    cudaError_t e = rnsw::launch_output_transform_kron(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), y, s);
+    return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_kron");
+  }
   if (rnsw::umma_output_ok(d)) {
     if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true, ev)) return rc;
     cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), y, s);
@@ -582,6 +590,12 @@ int requant_impl(const rnsw_plan* plan, const int8_t* x, int B, int H, int W, in
   if (workspace_bytes < vb + mb) return fail(RNSW_ERR_WORKSPACE, "workspace %zu < %zu bytes", workspace_bytes, vb + mb);
   int8_t* V = static_cast<int8_t*>(workspace);
   int16_t* Mw = reinterpret_cast<int16_t*>(static_cast<uint8_t*>(workspace) + vb);
+  if (rnsw::kron_output_ok(plan->host, g, pool ? 3 : 1)) {
+    if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true, ev)) return rc;
+    cudaError_t e = rnsw::launch_output_transform_kron(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), nullptr, s,
+                                                       out, shift, pool);
+    return e == cudaSuccess ? RNSW_OK : cuda_fail(e, "output_transform_requant_kron");
+  }
   if (rnsw::umma_output_ok(d)) {
     if (int rc = transform_and_product(plan, g, x, U, V, Mw, s, true, ev)) return rc;
     cudaError_t e = rnsw::launch_output_transform_umma(plan->host, g, reinterpret_cast<const uint8_t*>(Mw), nullptr, s,

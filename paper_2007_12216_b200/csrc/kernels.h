@@ -53,12 +53,21 @@ struct PlanHost {
   int kr_limbs;           // 1 (m < 256) or 2 (balanced s8 limbs)
   size_t kr_group_bytes;  // kr_limbs * kr_khalves * 16 KB
   int64_t kr_xmax[RNSW_MAX_RES];  // max |Kr d| over positions (|d| <= 128): the accumulator bias floor
+  // tcgen05 Kronecker output transform (output_kron.cu), two 16-bit residues:
+  // kron(AT, AT) (residue 1 times the mixed-radix factor) per (residue, row
+  // block) as four balanced-limb matrices [4][128 rows][kra_kp] int8
+  uint8_t* d_kra;
+  int kra_npb;
+  int kra_kp;
+  size_t kra_bytes;
 };
 
 // Build / release PlanHost::d_kr (input_umma.cu); a plan without it keeps
 // the mma.sync input transform.
 cudaError_t build_kr_images(PlanHost& plan);
 void free_kr_images(PlanHost& plan);
+cudaError_t build_kra_images(PlanHost& plan);
+void free_kra_images(PlanHost& plan);
 
 cudaError_t launch_filter_transform(const PlanHost& plan, const int8_t* w, int C, int K, int Cp, int layout,
                                     int8_t* U, cudaStream_t s);
@@ -91,6 +100,10 @@ bool umma_output_ok(const PlanDevice& d);
 cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g, const uint8_t* Mw8, int32_t* y,
                                          cudaStream_t s, int8_t* out8 = nullptr, int shift = 0, int pool = 0);
 bool force_generic();
+// Kronecker output transform (output_kron.cu): mode 0 int32 y, 1 requant int8, 3 requant + pool
+bool kron_output_ok(const PlanHost& plan, const Geometry& g, int mode);
+cudaError_t launch_output_transform_kron(const PlanHost& plan, const Geometry& g, const uint8_t* Mw8, int32_t* y,
+                                         cudaStream_t s, int8_t* out8 = nullptr, int shift = 0, int pool = 0);
 // Small-channel path (C <= 4): compact input transform + CUDA-core product (smallc.cu)
 bool smallc_ok(const PlanDevice& d, const Geometry& g);
 size_t smallc_v16_bytes(const PlanDevice& d, const Geometry& g);
