@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--no-layer-configs", action="store_true",
                     help="skip the per-layer latency lines of BASELINE configs 1, 3 and 5")
     ap.add_argument("--impl", default="rnsw", choices=["rnsw", "reference"])
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU-only check of the multi-rank plumbing (launcher, gloo, shards, gather, max-over-ranks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-images", type=int, default=1)
     ap.add_argument("--no-graph", action="store_true", help="launch the 39 kernels per step eagerly")
@@ -548,6 +550,35 @@ def run_gpu_arm(args):
         dist.destroy_process_group()
 
 
+def run_dry_arm(args):
+    """The N-rank plumbing of the GPU arm without a GPU: same launcher, shard
+    split, final all-gather and max-over-ranks, over gloo on CPU tensors."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_12216_b200 import parallel
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    global_batch = args.batch * world if args.weak else args.batch
+    start, shard = parallel.shard_range(global_batch, world, rank)
+    local = torch.full((shard, 7, 7, 512), rank + 1, dtype=torch.int8)
+    local[:, 0, 0, 0] = torch.arange(start, start + shard, dtype=torch.int64).remainder(127).to(torch.int8)
+    maps = parallel.gather_maps(local, world)
+    elapsed = parallel.max_over_ranks(0.001 * (rank + 1), world)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "global_batch": global_batch, "per_rank_batch": shard,
+                          "scaling": "weak" if args.weak else "strong", "gathered_shape": list(maps.shape),
+                          "gathered_ranks": sorted({int(v) for v in maps[:, 1, 1, 1].tolist()}),
+                          "image_tags_ok": bool((maps[:, 0, 0, 0].to(torch.int64) ==
+                                                 torch.arange(global_batch).remainder(127)).all()),
+                          "max_elapsed_s": elapsed}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def spawn_ranks(args) -> int:
     """--gpus N without a torchrun environment: relaunch this script under
     torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
@@ -566,7 +597,9 @@ def main():
     args = parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args))
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry_arm(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_gpu_arm(args)

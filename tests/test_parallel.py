@@ -75,3 +75,32 @@ def test_two_rank_gather_matches_single_process():
     for rank, _, _, full, t in results:
         assert np.array_equal(full, want)
         assert t == 1.5  # max over ranks
+
+
+@pytest.mark.parametrize("gpus,weak", [(2, False), (4, False), (2, True)])
+def test_bench_self_launch_dry_run(gpus, weak):
+    """`bench.py --gpus N` without a torchrun environment relaunches itself
+    under torch.distributed.run with N ranks (here over gloo, --dry-run: no
+    GPU work): config 4's 256 images split 256/N per rank (strong scaling) or
+    N x --batch (weak), gathered back in image order on rank 0."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    cmd = [sys.executable, str(root / "bench.py"), "--gpus", str(gpus), "--dry-run"]
+    if weak:
+        cmd += ["--weak", "--batch", "16"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == gpus
+    if weak:
+        assert line["global_batch"] == 16 * gpus and line["per_rank_batch"] == 16
+    else:
+        assert line["global_batch"] == 256 and line["per_rank_batch"] == 256 // gpus
+    assert line["gathered_ranks"] == list(range(1, gpus + 1))
+    assert line["image_tags_ok"] and abs(line["max_elapsed_s"] - 0.001 * gpus) < 1e-9
