@@ -42,9 +42,15 @@
 #include "kernels.h"
 
 // Diagnostic builds only (tools/variant_build.sh -DRNSW_K1_DIAG=n): 1 = no
-// staging stores / bulk stores, 2 = no conversion, 3 = one MMA per unit.
+// staging stores / bulk stores, 2 = no conversion, 3 = one MMA per unit, 4 = tile-major V.
 #ifndef RNSW_K1_DIAG
 #define RNSW_K1_DIAG 0
+#endif
+// 1: the accumulator bias is added in the epilogue (one IADD per value)
+// -- measured 7% slower on conv1_2 than the bias MMAs, so off
+// instead of by two bias MMAs per unit (11% of the unit's tensor work)
+#ifndef RNSW_K1_EPI_BIAS
+#define RNSW_K1_EPI_BIAS 0
 #endif
 
 namespace rnsw {
@@ -257,16 +263,17 @@ __global__ void __launch_bounds__(kUThreads, 1)
       tc_fence_after();
       const uint32_t d0 = tmem_base + as * Cfg::kAccCols;
       const uint64_t db_stage = db0 + (uint64_t)(stage * kStageStep);
-      if (kLimbs == 2) {  // the bias: D_hi = 127 S1, D_lo = 127 S2 (overwrites the buffer)
+      if (kLimbs == 2 && !RNSW_K1_EPI_BIAS) {  // the bias: D_hi = 127 S1, D_lo = 127 S2 (overwrites the buffer)
         mma_i8_ts_warp(d0, tmem_base + Cfg::kBiasCol, dbh, idesc, 0u);
         mma_i8_ts_warp(d0 + kUnitN, tmem_base + Cfg::kBiasCol, dbl, idesc, 0u);
       }
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
-        if (ks < (RNSW_K1_DIAG == 3 ? 1 : ksteps)) {
+        if (ks < ((RNSW_K1_DIAG == 3 || RNSW_K1_DIAG >= 5) ? 1 : ksteps)) {
           const uint64_t db = db_stage + (uint64_t)(ks * kBStep);
-          mma_i8_ts_warp(d0, ta + ks * 8, db, idesc, (kLimbs == 2 || ks > 0) ? 1u : 0u);
-          if (kLimbs == 2) mma_i8_ts_warp(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, 1u);
+          const uint32_t acc = ((kLimbs == 2 && !RNSW_K1_EPI_BIAS) || ks > 0) ? 1u : 0u;
+          mma_i8_ts_warp(d0, ta + ks * 8, db, idesc, acc);
+          if (kLimbs == 2) mma_i8_ts_warp(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, acc);
         }
       }
       mma_commit_warp(&empty[stage]);
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
         mbar_wait(&sfull[sb], (jt >> 1) & 1);
         uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
-        for (int pl = 0; pl < (RNSW_K1_DIAG == 1 ? 0 : kLimbs); ++pl)
+        for (int pl = 0; pl < ((RNSW_K1_DIAG == 1 || RNSW_K1_DIAG >= 5) ? 0 : kLimbs); ++pl)
           tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0, p, pb * kGroupRows,
                        args.plane_base[res] + pl);
         bulk_commit();
@@ -302,15 +309,16 @@ __global__ void __launch_bounds__(kUThreads, 1)
     // ---------------- epilogue: 8 warps = 4 lane quadrants x 2 channel halves ----------------
     const int row = q * 32 + lane;  // position within the group's block
     const uint32_t mul0 = args.mul0[res];
+    const int32_t ebias = RNSW_K1_EPI_BIAS ? 127 * (256 * args.bias_s1[res] + args.bias_s2[res]) : 0;
     auto convert = [&](const int32_t (&a)[16], const int32_t (&b)[16], uint32_t* lo, uint32_t* hi) {
       int32_t w[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         if (kMode == kRel16) {
-          const uint32_t n = (uint32_t)(a[e] * 256 + b[e]);  // x + bias, bias = 128 (mod m)
+          const uint32_t n = (uint32_t)(a[e] * 256 + b[e] + ebias);  // x + bias, bias = 128 (mod m)
           w[e] = (int32_t)(__umulhi(n, mul0) * fm.negm + n);  // = x + 128 (mod m), in [-m, m)
         } else if (kMode == kSym16) {
-          const int32_t r = red_pos_biased(a[e] * 256 + b[e], fm);  // (x + h) mod m
+          const int32_t r = red_pos_biased(a[e] * 256 + b[e] + ebias, fm);  // (x + h) mod m
           w[e] = r + (128 - fm.h);                                  // v + 128
         } else {
           const uint32_t n = (uint32_t)(b[e] + fm.off);  // x + off, off = h (mod m)
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
-      if (RNSW_K1_DIAG != 2) {
+      if (RNSW_K1_DIAG != 2 && RNSW_K1_DIAG != 6) {
         convert(a0, b0, lo, hi);
         convert(a1, b1, lo + 4, hi + 4);
       } else {
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
       if (h_ == 0) mbar_wait(&sempty[sb], ((jt >> 1) & 1) ^ 1);
       uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
-      for (int pl = 0; pl < (RNSW_K1_DIAG == 1 ? 0 : kLimbs); ++pl) {
+      for (int pl = 0; pl < ((RNSW_K1_DIAG == 1 || RNSW_K1_DIAG >= 5) ? 0 : kLimbs); ++pl) {
         uint8_t* base = sbuf + pl * (kGroupRows * 2 * kUnitN);
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
@@ -541,7 +549,12 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
     // x 128 positions x 1 plane (128B swizzle)
     const int npos = d.n * d.n;
     cuuint64_t dims[4] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P, (cuuint64_t)npos, (cuuint64_t)d.n_planes};
+#if RNSW_K1_DIAG == 4
+    // diagnostic: tile-major V (positions of a tile contiguous) -- wrong for the GEMM, write-locality probe
+    cuuint64_t strides[3] = {(cuuint64_t)npos * g.Cp, (cuuint64_t)g.Cp, (cuuint64_t)g.P * g.Cp * npos};
+#else
     cuuint64_t strides[3] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P * g.Cp, (cuuint64_t)g.P * g.Cp * npos};
+#endif
     cuuint32_t es[4] = {1, 1, 1, 1};
     cuuint32_t box[4] = {(cuuint32_t)kUnitN, 2, (cuuint32_t)kGroupRows, 1};
     if (encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
