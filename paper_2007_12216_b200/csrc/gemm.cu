@@ -93,9 +93,14 @@ RNSW_DEV TileCoord tile_coord(uint32_t t, const GemmArgs& a) {
   return c;
 }
 
+// MAXPL: 1 = 8-bit residues (one plane each side); 2 = 16-bit residues with
+// the four-plane filter bank (u, u' = 256 u mod m: two accumulators); 3 =
+// 16-bit residues reading only the u planes of the bank (three accumulators
+// A65536 | A256 | A1, four N = BN MMAs per k-step): half the filter-bank
+// bytes, for the layers whose bank stream dominates (small P).
 template <int BN, int MAXPL>
 struct GemmTraits {
-  static constexpr int kAccCols = (MAXPL == 2 ? 2 : 1) * BN;  // TMEM columns per accumulator set
+  static constexpr int kAccCols = (MAXPL == 1 ? 1 : MAXPL == 2 ? 2 : 3) * BN;  // TMEM columns per accumulator set
   static constexpr int kTmemCols = (2 * kAccCols <= 32) ? 32
                                    : (2 * kAccCols <= 64) ? 64
                                    : (2 * kAccCols <= 128) ? 128
@@ -103,10 +108,13 @@ struct GemmTraits {
   static_assert(2 * kAccCols <= 512, "accumulators exceed TMEM");
 };
 
+constexpr int a_planes(int maxpl) { return maxpl == 1 ? 1 : 2; }
+constexpr int b_planes(int maxpl) { return maxpl == 1 ? 1 : (maxpl == 2 ? 4 : 2); }
+
 template <int BC>
 constexpr int stage_bytes(int bn, int maxpl) {
-  // A: V planes (maxpl); B: filter-bank planes (1 or 4)
-  return maxpl * kBlockM * BC + (maxpl == 2 ? 4 : 1) * bn * BC;
+  // A: V planes (1 or 2); B: filter-bank planes (1, 4, or 2)
+  return a_planes(maxpl) * kBlockM * BC + b_planes(maxpl) * bn * BC;
 }
 
 template <int BN, int BC, int MAXPL, bool TS = true, int SB = 1>
@@ -258,6 +266,51 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
   }
 }
 
+// 16-bit residues from the two-plane bank (MAXPL 3): three accumulators
+// [A65536 | A256 | A1] per column, y = 65536 A65536 + 256 A256 + A1 (mod m).
+// |A65536| <= C 17*9, |A256| <= C (17*128 + 128*9), |A1| <= C 128^2 (V limbs of
+// relaxed residues, input_umma.cu), so for C <= 8192 each partial and the
+// recombination red(A65536) r65536 + red(A256) 256 + A1 stay below 2^28.
+template <int BN>
+RNSW_DEV void epilogue_u2(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, uint8_t* out8, int col0,
+                          bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
+  constexpr int kHalf = BN / 2;
+  constexpr int kBatch = kHalf < 16 ? kHalf : 16;
+  const FastMod fm = a.fm[res];
+  const int32_t r65536 = a.r65536[res];
+  const int32_t pb = pos_bias(fm);
+#pragma unroll 1
+  for (int c0 = 0; c0 < kHalf; c0 += kBatch) {
+    int32_t h2[16], h1[16], lo[16];
+    tmem_ld16(taddr + c0, h2);
+    tmem_ld16(taddr + BN + c0, h1);
+    tmem_ld16(taddr + 2 * BN + c0, lo);
+    tmem_ld_wait();
+    if (c0 + kBatch >= kHalf) release_acc(tempty, lane);
+    int32_t r[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int32_t t = red_fast(h2[e], fm) * r65536 + red_fast(h1[e], fm) * 256 + lo[e];
+      r[e] = a.pos_out ? red_pos_biased(t + pb, fm) : red_fast(t, fm);
+    }
+    const int col = col0 + c0;
+    if (a.planar) {
+      if (!a.pos_out) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] += r[e] < 0 ? fm.m : 0;
+      }
+      if (stg != nullptr)
+        sts8x2_swz<BN>(stg, srow, scol0 + c0, r);
+      else if (row_ok && col < a.Kp)
+        store8x2(out8 + col, out8 + a.mw8_plane + col, r);
+    } else if (stg != nullptr) {
+      sts16_swz(stg, srow, scol0 + c0, r);
+    } else if (row_ok && col < a.Kp) {
+      store16(out_row + col, r);
+    }
+  }
+}
+
 // 8-bit residues: one accumulator per column.
 template <int BN>
 RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
@@ -345,10 +398,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   auto stage_a = [&](int s, int pl) { return smem + s * Cfg::kStageBytes + pl * Cfg::kAPlaneBytes; };
   auto stage_b = [&](int s, int pl) {
-    return smem + s * Cfg::kStageBytes + MAXPL * Cfg::kAPlaneBytes + pl * Cfg::kBPlaneBytes;
+    return smem + s * Cfg::kStageBytes + a_planes(MAXPL) * Cfg::kAPlaneBytes + pl * Cfg::kBPlaneBytes;
   };  // B smem slots, 16-bit: [0] u'_hi, [1] u'_lo, [2] u_hi, [3] u_lo (bank plane b -> slot 3 - b),
      // so slots 0-1 and 2-3 are each one 2*BN-row K-major operand; 8-bit: [0] u
-  auto bslot = [&](int b, int pl) { return (MAXPL == 2 && pl == 2) ? 3 - b : b; };
+  // MAXPL 3: [0] u_hi, [1] u_lo (bank planes 1, 0)
+  auto bslot = [&](int b, int pl) { return (MAXPL == 2 && pl == 2) ? 3 - b : (MAXPL == 3 ? 1 - b : b); };
 
   if (warp == 0) {
     // ---------------- TMA producer (whole warp) ----------------
@@ -361,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const TileCoord tc = tile_coord((uint32_t)t, args);
       const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
       const int pl = args.planes[res];
-      const int upl = pl == 2 ? 4 : 1;
+      const int upl = MAXPL == 3 ? 2 : (pl == 2 ? 4 : 1);
       const int nb = MC == 2 ? 2 : upl;        // filter planes this CTA loads
       const int b0 = MC == 2 ? 2 * rank : 0;   // first of them
       const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
@@ -415,6 +469,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t db_lo = umma_desc_kmajor(b0 + 32 * k, BC);
             if (MAXPL == 1 || pl == 1) {
               mma_i8(d0, da_lo, db_lo, idesc, acc);
+            } else if (MAXPL == 3) {
+              // v u = 65536 v_hi u_hi + 256 (v_hi u_lo + v_lo u_hi) + v_lo u_lo
+              const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
+              const uint64_t db_hi = db_lo;                                                    // slot 0: u_hi
+              const uint64_t db_ul = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);   // slot 1: u_lo
+              mma_i8(d0, da_hi, db_hi, idesc, acc);
+              mma_i8(d0 + BN, da_hi, db_ul, idesc, acc);
+              mma_i8(d0 + BN, da_lo, db_hi, idesc, 1u);
+              mma_i8(d0 + 2 * BN, da_lo, db_ul, idesc, acc);
             } else {
               // v*u = 256*(v_hi*u'_hi + v_lo*u_hi) + (v_hi*u'_lo + v_lo*u_lo): the
               // accumulator columns [A256 | A1] take N = 2*BN rows of B at once
@@ -474,6 +537,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // every row of this warp's lane quadrant is past the last tile (small
         // or ragged P): nothing to reduce, just free the accumulator
         release_acc(&tempty[as], lane);
+      } else if (MAXPL == 3) {
+        uint8_t* out8 = reinterpret_cast<uint8_t*>(args.Mw) +
+                        mw8_offset(p, res, 0, pos, args.n_res, args.npos, args.Kp);
+        epilogue_u2<BN>(args, res, taddr, out_row, out8, col0, row_ok, &tempty[as], lane, stg_t, q * 32 + lane,
+                        half * kHalf);
       } else if (MAXPL == 2 && pl == 2) {
         uint8_t* out8 = reinterpret_cast<uint8_t*>(args.Mw) +
                         mw8_offset(p, res, 0, pos, args.n_res, args.npos, args.Kp);
@@ -708,6 +776,25 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   bool all16 = true;
   for (int r = 0; r < d.n_res; ++r) all16 = all16 && d.res[r].planes == 2;
   static const bool no_mc = getenv("RNSW_GEMM_NO_MC") != nullptr;  // A/B switch
+  // RNSW_GEMM_U2=1: the two-plane-bank variant (MAXPL 3) for every 16-bit
+  // layer, =2: where the bank stream dominates (4 K C >= 2 P C + 4 P K).  Off
+  // by default: on B200 it measured slower even at batch 1 (0.83 vs 0.63 ms
+  // for the VGG16 GEMMs) -- four N = 64 MMAs per k-step cost 1.5x the tensor
+  // time per output column of two N = 256 ones, and at small P the 128-row
+  // MMAs are mostly padding, so halving the bank bytes does not pay.
+  static const int u2_mode = getenv("RNSW_GEMM_U2") ? atoi(getenv("RNSW_GEMM_U2")) : 0;
+  if (maxpl == 2 && all16 && a.fast && u2_mode != 0) {
+    const double bank4 = 4.0 * Kp * Cp, act = (double)P * (2.0 * Cp + 4.0 * Kp);
+    const bool u2 = u2_mode == 1 || bank4 >= act;
+    if (u2) {
+      bn = 64;
+      a.num_kb = (Kp + bn - 1) / bn;
+      a.total_tiles = (int64_t)d.n_res * a.npos * a.num_pb * a.num_kb;
+      if (a.total_tiles >= (1ll << 31)) return cudaErrorInvalidValue;
+      a.div_kb = make_fastdiv((uint32_t)a.num_kb);
+      return run_gemm_bc<64, 3>(a, bc, V, U, np, nup, s);
+    }
+  }
   if (maxpl == 2 && all16 && a.num_pb >= 4 && !no_mc) {
     // CTA pairs over (pb, pb+1) with the filter planes multicast (see the kernel);
     // with only 2-3 tile blocks the pair's lockstep costs more than the shared

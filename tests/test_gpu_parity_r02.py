@@ -223,3 +223,22 @@ def test_requant_output_alignment():
                                                   vp(bank.data.data_ptr()), 9, 1, vp(raw.data_ptr() + 1),
                                                   vp(ws.data_ptr()), ws_bytes, _stream_ptr()))
     torch.cuda.synchronize()
+
+
+@pytest.mark.skipif(__import__("os").environ.get("RNSW_GEMM_U2") is not None, reason="already forced")
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_gemm_two_plane_bank_forced(mode):
+    """The GEMM's two-plane-bank variant (three accumulators; opt-in,
+    RNSW_GEMM_U2) on every 16-bit layer (1) or on the small-P ones (2): VGG16
+    batch 1 digests, the config-5 16-bit sweep and the wide-C cases match."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, RNSW_GEMM_U2=mode)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_configs.py"), os.path.join(here, "test_gpu_parity_r02.py"),
+                        "-k", "vgg16_batch1 or config5_sweep or gemm_wide or fused_requant"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
