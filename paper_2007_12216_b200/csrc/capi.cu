@@ -299,6 +299,7 @@ int rnsw_plan_create(rnsw_plan** out, int tile_m, int r, int n_res, const int32_
   if (e == cudaSuccess) e = cudaMemcpy(plan->host.d_plan, &d, sizeof(d), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = rnsw::build_kr_images(plan->host);
   if (e == cudaSuccess) e = rnsw::build_kra_images(plan->host);
+  if (e == cudaSuccess) e = rnsw::build_kra8_images(plan->host);
   if (e != cudaSuccess) {
     if (plan->host.d_plan) cudaFree(plan->host.d_plan);
     rnsw::free_kr_images(plan->host);

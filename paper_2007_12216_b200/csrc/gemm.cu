@@ -170,6 +170,17 @@ RNSW_DEV void sts8x2_swz(uint8_t* stg, int row, int col, const int32_t (&r)[16])
   *reinterpret_cast<uint4*>(stg + kBlockM * BN + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
 }
 
+// 8-bit residues [0, m) as ONE byte plane (the 8-bit Mw8, kernels.h mw8s_offset).
+template <int BN>
+RNSW_DEV void sts8_swz(uint8_t* stg, int row, int col, const int32_t (&r)[16]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) w[e] = pack4_lo(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]);
+  uint32_t off = row * BN + col;
+  off = BN == 128 ? swz128(off) : (off ^ (((off >> 7) & 3u) << 4));
+  *reinterpret_cast<uint4*>(stg + off) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 RNSW_DEV void store8x2(uint8_t* lo_row, uint8_t* hi_row, const int32_t (&r)[16]) {
   uint32_t lo[4], hi[4];
 #pragma unroll
@@ -313,8 +324,8 @@ RNSW_DEV void epilogue_u2(const GemmArgs& a, int res, uint32_t taddr, int16_t* o
 
 // 8-bit residues: one accumulator per column.
 template <int BN>
-RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, int col0, bool row_ok,
-                              uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
+RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, uint8_t* out8, int col0,
+                              bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 64 ? kHalf : 64;
   const FastMod fm = a.fm[res];
@@ -336,10 +347,23 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
         for (int e = 0; e < 16; ++e) r[e] = reduce_generic(v[j][e], a, res);
       }
       const int col = col0 + c0 + 16 * j;
-      if (stg != nullptr)
+      if (a.planar) {
+        // one byte plane of y mod m in [0, m)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] += r[e] < 0 ? fm.m : 0;
+        if (stg != nullptr) {
+          sts8_swz<BN>(stg, srow, scol0 + c0 + 16 * j, r);
+        } else if (row_ok && col < a.Kp) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) w[e] = pack4_lo(r[4 * e], r[4 * e + 1], r[4 * e + 2], r[4 * e + 3]);
+          *reinterpret_cast<uint4*>(out8 + col) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      } else if (stg != nullptr) {
         sts16_swz(stg, srow, scol0 + c0 + 16 * j, r);
-      else if (row_ok && col < a.Kp)
+      } else if (row_ok && col < a.Kp) {
         store16(out_row + col, r);
+      }
     }
   }
 }
@@ -548,7 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, out8, col0, row_ok, &tempty[as], lane, stg_t,
                                          q * 32 + lane, half * kHalf);
       } else {
-        epilogue_single<BN>(args, res, taddr, out_row, col0, row_ok, &tempty[as], lane, stg_t, q * 32 + lane,
+        uint8_t* out8 = reinterpret_cast<uint8_t*>(args.Mw) + mw8s_offset(p, res, pos, args.n_res, args.npos, args.Kp);
+        epilogue_single<BN>(args, res, taddr, out_row, out8, col0, row_ok, &tempty[as], lane, stg_t, q * 32 + lane,
                             half * kHalf);
       }
       if (Cfg::kTmaStore) {
@@ -556,8 +581,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, 256);
         if (warp == 4 && lane == 0) {
           if (args.planar) {
-            // both limb planes of the tile: slabs (pb * n_res + res) * 2 + {0, 1}
-            tma_store_3d(&tmM, stg_b, kb * BN, pos * kBlockM, (pb * args.n_res + res) * 2);
+            // both limb planes of the tile: slabs (pb * n_res + res) * 2 + {0, 1};
+            // 8-bit residues: the one plane, slab pb * n_res + res
+            tma_store_3d(&tmM, stg_b, kb * BN, pos * kBlockM, (pb * args.n_res + res) * (MAXPL == 1 ? 1 : 2));
           } else {
             const int row0 = (int)(((int64_t)pb * args.n_res * args.npos + res * args.npos + pos) * kBlockM);
 #pragma unroll
@@ -601,13 +627,13 @@ bool make_tmap_mw(CUtensorMap* tm, const void* base, int Kp, int64_t rows) {
 // Mw8 as a 2-D uint8 array [rows][Kp] (rows = limb-plane rows), box BN x 128.
 // Mw8 as [slab = (pb * n_res + res) * 2 + limb][pos * 128 + t][Kp]; one box =
 // both limb planes of an output tile (BN x 128 rows x 2), one store per tile.
-bool make_tmap_mw8_store(CUtensorMap* tm, const void* base, int Kp, int64_t rows, int bn, int npos) {
+bool make_tmap_mw8_store(CUtensorMap* tm, const void* base, int Kp, int64_t rows, int bn, int npos, int planes = 2) {
   auto encode = encode_fn();
   if (encode == nullptr) return false;
   const int64_t slab_rows = (int64_t)npos * kBlockM;
   cuuint64_t dims[3] = {(cuuint64_t)Kp, (cuuint64_t)slab_rows, (cuuint64_t)(rows / slab_rows)};
   cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(slab_rows * Kp)};
-  cuuint32_t box[3] = {(cuuint32_t)bn, (cuuint32_t)kBlockM, 2};
+  cuuint32_t box[3] = {(cuuint32_t)bn, (cuuint32_t)kBlockM, (cuuint32_t)planes};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, bn == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -665,7 +691,9 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   CUtensorMap tmM;
   const int64_t mw_rows = (a.P + kBlockM - 1) / kBlockM * (int64_t)a.n_res * a.npos * kBlockM;
   if (a.planar) {
-    if (!make_tmap_mw8_store(&tmM, a.Mw, a.Kp, mw_rows * 2, BN, a.npos)) return cudaErrorInvalidValue;
+    const int out_planes = MAXPL == 1 ? 1 : 2;
+    if (!make_tmap_mw8_store(&tmM, a.Mw, a.Kp, mw_rows * out_planes, BN, a.npos, out_planes))
+      return cudaErrorInvalidValue;
   } else if (!make_tmap_mw(&tmM, a.Mw, a.Kp, mw_rows)) {
     return cudaErrorInvalidValue;
   }
@@ -760,7 +788,7 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   // B 4 planes per stage)
   int bn;
   if (maxpl == 2) bn = Kp <= 64 ? 64 : 128;
-  else bn = Kp <= 64 ? 64 : (Kp <= 128 ? 128 : 256);
+  else bn = Kp <= 64 ? 64 : ((Kp <= 128 || planar) ? 128 : 256);
   if (maxpl == 2 && bc > 64) {
     bc = 64;
     a.nkc = Cp / bc;

@@ -37,6 +37,12 @@ __host__ __device__ inline int64_t mw8_offset(int64_t p, int res, int limb, int 
   return (((((p >> 7) * nres + res) * 2 + limb) * npos + pos) * 128 + (p & 127)) * (int64_t)Kp;
 }
 
+// Mw8 for 8-bit residues (the Kronecker output transform, output_kron.cu):
+// y mod m in [0, m) as one byte plane per residue, [ceil(P/128)][res][pos][128][Kp].
+__host__ __device__ inline int64_t mw8s_offset(int64_t p, int res, int pos, int nres, int npos, int Kp) {
+  return ((((p >> 7) * nres + res) * npos + pos) * 128 + (p & 127)) * (int64_t)Kp;
+}
+
 // Host-side mirror of the plan (kept next to the device copy).
 struct PlanHost {
   PlanDevice dev;         // host copy of the tables
@@ -60,6 +66,11 @@ struct PlanHost {
   int kra_npb;
   int kra_kp;
   size_t kra_bytes;
+  // ... for 8-bit plans: [rb][res][128 rows][kra8_kp] s8, residue r times W[r][0]
+  uint8_t* d_kra8;
+  int kra8_npb;
+  int kra8_kp;
+  size_t kra8_bytes;
 };
 
 // Build / release PlanHost::d_kr (input_umma.cu); a plan without it keeps
@@ -67,6 +78,7 @@ struct PlanHost {
 cudaError_t build_kr_images(PlanHost& plan);
 void free_kr_images(PlanHost& plan);
 cudaError_t build_kra_images(PlanHost& plan);
+cudaError_t build_kra8_images(PlanHost& plan);
 void free_kra_images(PlanHost& plan);
 
 cudaError_t launch_filter_transform(const PlanHost& plan, const int8_t* w, int C, int K, int Cp, int layout,

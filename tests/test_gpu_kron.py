@@ -88,3 +88,56 @@ def test_two_pass_output_transform_still_matches():
                         os.path.join(here, "test_gpu_kron.py"), "-k", "int32_layer or requant_layer"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+SYS8 = (251, 241, 239)
+
+
+@pytest.mark.parametrize("mods", [SYS8, (253, 251, 247), (251, 241), (251,), (7, 11, 13), (7, 11, 13, 17)])
+@pytest.mark.parametrize("tile_m,r", [(6, 3), (8, 3), (10, 3), (12, 3), (14, 3), (8, 5), (4, 3)])
+def test_int32_layer_8bit(mods, tile_m, r):
+    """8-bit residue systems (1-4 residues): every residue of a row block in
+    one CTA, mixed-radix digits folded into the reductions."""
+    import paper_2007_12216_b200 as rnsw
+
+    system = rnsw.RnsSystem(mods)
+    try:
+        rnsw.reduce_for_system(rnsw.cached_transforms(tile_m, r), system)
+    except rnsw.NotCoprime:
+        pytest.skip(f"moduli {mods} not compatible with F({tile_m},{r})")
+    rng = np.random.default_rng(tile_m * 7 + len(mods))
+    b, h, w, c, k = 2, 21, 17, 32, 48
+    wt = rng.integers(-128, 128, (r, r, c, k)).astype(np.int8)
+    x = rng.integers(-128, 128, (b, h, w, c)).astype(np.int8)
+    pad = r // 2
+    spec = rnsw.LayerSpec(h=h, w=w, c=c, k=k, r=r, padding=pad, batch=b, tile_m=tile_m)
+    got = rnsw.winograd_layer_conv(spec, wt, x, system, declared_bound=system.signed_bound)
+    assert np.array_equal(got, O.winograd_layer(x, wt, pad, tile_m, mods))
+
+
+@pytest.mark.parametrize("tile_m,pool", [(8, 1), (10, 0), (6, 1), (14, 1)])
+def test_requant_layer_8bit(tile_m, pool):
+    import torch
+    from oracle.vgg_ref import requant_pool
+    from paper_2007_12216_b200 import _native
+    from paper_2007_12216_b200.layer import _filters_on_device, _stream_ptr, plan_for
+    import paper_2007_12216_b200 as rnsw
+
+    rng = np.random.default_rng(tile_m)
+    b, h, c, k, shift = 2, 30, 64, 32, 8
+    plan = plan_for(rnsw.cached_transforms(tile_m, 3), rnsw.RnsSystem(SYS8))
+    x = rng.integers(0, 128, (b, h, h, c)).astype(np.int8)
+    w = rng.integers(-8, 9, (3, 3, c, k)).astype(np.int8)
+    bank = _filters_on_device(plan, torch.from_numpy(w).cuda(), c, k, _native.LAYOUT_NHWC)
+    l = _native.lib()
+    ws_bytes = l.rnsw_workspace_bytes(plan.handle, b, h, h, c, k, 1)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    oh = h // 2 if pool else h
+    out = torch.full((b, oh, oh, k), 77, dtype=torch.int8, device="cuda")
+    xd = torch.from_numpy(x).cuda()
+    vp = _native.c_void_p
+    _native.check(l.rnsw_conv_forward_requant(plan.handle, vp(xd.data_ptr()), b, h, h, c, k, 1,
+                                              vp(bank.data.data_ptr()), shift, pool, vp(out.data_ptr()),
+                                              vp(ws.data_ptr()), ws_bytes, _stream_ptr()))
+    want = requant_pool(oracle.direct_conv_c(x, w, 1), shift, bool(pool))
+    assert np.array_equal(out.cpu().numpy(), want)
