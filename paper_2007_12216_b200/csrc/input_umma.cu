@@ -47,8 +47,8 @@
 #define RNSW_K1_DIAG 0
 #endif
 // 1: the accumulator bias is added in the epilogue (one IADD per value)
-// -- measured 7% slower on conv1_2 than the bias MMAs, so off
-// instead of by two bias MMAs per unit (11% of the unit's tensor work)
+// instead of by two bias MMAs per unit (11% of the unit's tensor work) --
+// measured 7% slower on conv1_2 than the bias MMAs, so off
 #ifndef RNSW_K1_EPI_BIAS
 #define RNSW_K1_EPI_BIAS 0
 #endif

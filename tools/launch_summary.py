@@ -17,6 +17,7 @@ UNIT = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msec
 
 def kind_of(name: str) -> str:
     for key, kind in (("winograd_gemm", "gemm"), ("output_transform", "output_transform"), ("output_umma", "output_transform"),
+                      ("output_kron", "output_transform"), ("input_umma", "input_transform"),
                       ("input_transform", "input_transform"), ("smallc_product", "product"),
                       ("requant", "glue"), ("filter_transform", "filter_transform (setup, not in the step)")):
         if key in name:
