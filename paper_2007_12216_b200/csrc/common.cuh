@@ -352,6 +352,31 @@ RNSW_DEV void mma_i8_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, 
       "}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// Issue f(0) .. f(n-1), n <= 8, as a fully unrolled, branch-free sequence.
+// A runtime bound tested between consecutive tcgen05.mma instructions
+// (`#pragma unroll` + `if (ks < n)`) measured 50 instead of 32 cycles per
+// M=128 N=64 K=32 MMA on B200 (tools/k1_mma_probe.cu, K1 issue timing).
+template <int kN, typename F>
+RNSW_DEV void unrolled_steps(F& f) {
+#pragma unroll
+  for (int i = 0; i < kN; ++i) f(i);
+}
+template <typename F>
+RNSW_DEV void for_ksteps(int n, F&& f) {
+  switch (n) {
+    case 8: unrolled_steps<8>(f); break;
+    case 7: unrolled_steps<7>(f); break;
+    case 6: unrolled_steps<6>(f); break;
+    case 5: unrolled_steps<5>(f); break;
+    case 4: unrolled_steps<4>(f); break;
+    case 3: unrolled_steps<3>(f); break;
+    case 2: unrolled_steps<2>(f); break;
+    case 1: unrolled_steps<1>(f); break;
+    default:
+      for (int i = 0; i < n; ++i) f(i);
+  }
+}
+
 RNSW_DEV void mma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"

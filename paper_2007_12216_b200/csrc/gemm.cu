@@ -473,38 +473,68 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+#ifdef RNSW_GEMM_PROF
+      long long g_te = 0, g_f = 0, g_is = 0, g_0 = clock64(), g_mma = 0, g_cm = 0, g_tc = 0;
+#endif
       for (int64_t t = u_begin; t < args.total_tiles; t += u_step, ++it) {
+#ifdef RNSW_GEMM_PROF
+        long long g0 = clock64();
+#endif
         const int res = tile_coord((uint32_t)t, args).res;
         const int pl = args.planes[res];
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
+#ifdef RNSW_GEMM_PROF
+        long long g1 = clock64();
+        g_tc += g1 - g0;
+#endif
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
+#ifdef RNSW_GEMM_PROF
+        g_te += clock64() - g1;
+#endif
         const uint32_t d0 = tmem_base + as * Tr::kAccCols;
         for (int kc = 0; kc < args.nkc; ++kc) {
+#ifdef RNSW_GEMM_PROF
+          long long g2 = clock64();
+#endif
           mbar_wait(&full[stage], phase);
           tc_fence_after();
+#ifdef RNSW_GEMM_PROF
+          long long g3 = clock64();
+          g_f += g3 - g2;
+          g_mma += BC / 32 * ((MAXPL == 1 || pl == 1) ? 1 : (MAXPL == 3 ? 4 : 2));
+#endif
           const uint32_t a0 = smem_u32(stage_a(stage, 0));
           const uint32_t b0 = smem_u32(stage_b(stage, 0));
+          // one branch per stage, then a branch-free unrolled MMA sequence
+          // (a runtime test between consecutive MMAs costs tensor throughput)
+          if (MAXPL == 1 || pl == 1) {
 #pragma unroll
-          for (int k = 0; k < BC / 32; ++k) {
-            const uint32_t acc = (kc | k) != 0;
-            const uint64_t da_lo = umma_desc_kmajor(a0 + 32 * k, BC);
-            const uint64_t db_lo = umma_desc_kmajor(b0 + 32 * k, BC);
-            if (MAXPL == 1 || pl == 1) {
-              mma_i8(d0, da_lo, db_lo, idesc, acc);
-            } else if (MAXPL == 3) {
+            for (int k = 0; k < BC / 32; ++k)
+              mma_i8(d0, umma_desc_kmajor(a0 + 32 * k, BC), umma_desc_kmajor(b0 + 32 * k, BC), idesc,
+                     (kc | k) != 0);
+          } else if (MAXPL == 3) {
+#pragma unroll
+            for (int k = 0; k < BC / 32; ++k) {
               // v u = 65536 v_hi u_hi + 256 (v_hi u_lo + v_lo u_hi) + v_lo u_lo
+              const uint32_t acc = (kc | k) != 0;
+              const uint64_t da_lo = umma_desc_kmajor(a0 + 32 * k, BC);
               const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
-              const uint64_t db_hi = db_lo;                                                    // slot 0: u_hi
+              const uint64_t db_hi = umma_desc_kmajor(b0 + 32 * k, BC);                      // slot 0: u_hi
               const uint64_t db_ul = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);   // slot 1: u_lo
               mma_i8(d0, da_hi, db_hi, idesc, acc);
               mma_i8(d0 + BN, da_hi, db_ul, idesc, acc);
               mma_i8(d0 + BN, da_lo, db_hi, idesc, 1u);
               mma_i8(d0 + 2 * BN, da_lo, db_ul, idesc, acc);
-            } else {
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < BC / 32; ++k) {
               // v*u = 256*(v_hi*u'_hi + v_lo*u_hi) + (v_hi*u'_lo + v_lo*u_lo): the
               // accumulator columns [A256 | A1] take N = 2*BN rows of B at once
+              const uint32_t acc = (kc | k) != 0;
+              const uint64_t da_lo = umma_desc_kmajor(a0 + 32 * k, BC);
               const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
               const uint64_t db_p = umma_desc_kmajor(b0 + 32 * k, BC);                         // [u'_hi ; u'_lo]
               const uint64_t db_u = umma_desc_kmajor(b0 + 2 * Cfg::kBPlaneBytes + 32 * k, BC);  // [u_hi ; u_lo]
@@ -516,13 +546,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit_mc(&empty[stage], (uint16_t)0x3);
           else
             mma_commit(&empty[stage]);
+#ifdef RNSW_GEMM_PROF
+          g_is += clock64() - g3;
+#endif
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
+#ifdef RNSW_GEMM_PROF
+        long long g4 = clock64();
+#endif
         mma_commit(&tfull[as]);
+#ifdef RNSW_GEMM_PROF
+        g_cm += clock64() - g4;
+#endif
       }
+#ifdef RNSW_GEMM_PROF
+      if (blockIdx.x < 2 && it > 0) printf("GEMMPROF2 cta %d tile_coord %lld commit %lld\n", blockIdx.x, g_tc, g_cm);
+#endif
+#ifdef RNSW_GEMM_PROF
+      if (blockIdx.x < 2 && it > 0)
+        printf("GEMMPROF cta %d BN %d BC %d tiles %d mmas %lld total %lld wait_tempty %lld wait_full %lld issue %lld (cyc/mma %.1f)\n",
+               blockIdx.x, BN, BC, it, g_mma, clock64() - g_0, g_te, g_f, g_is, (double)(clock64() - g_0) / g_mma);
+#endif
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: 8 warps = 4 TMEM lane quadrants x 2 column halves ----------------

@@ -34,6 +34,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -46,6 +47,11 @@
 #ifndef RNSW_K1_DIAG
 #define RNSW_K1_DIAG 0
 #endif
+// 9 = no TMEM loads in the epilogue, 10 = 9 without stores
+#define RNSW_K1_ONE_MMA (RNSW_K1_DIAG == 3 || (RNSW_K1_DIAG >= 5 && RNSW_K1_DIAG <= 8))
+#define RNSW_K1_NO_STORE (RNSW_K1_DIAG == 1 || (RNSW_K1_DIAG >= 5 && RNSW_K1_DIAG <= 8) || RNSW_K1_DIAG >= 10)
+// 11 = no staging / bulk stores; each epilogue lane writes its 64 bytes straight to global (wrong layout)
+#define RNSW_K1_NO_TMEM_LD (RNSW_K1_DIAG == 9 || RNSW_K1_DIAG == 10)
 // 1: the accumulator bias is added in the epilogue (one IADD per value)
 // instead of by two bias MMAs per unit (11% of the unit's tensor work) --
 // measured 7% slower on conv1_2 than the bias MMAs, so off
@@ -57,9 +63,17 @@ namespace rnsw {
 
 namespace {
 
-constexpr int kUThreads = 384;
 constexpr int kGroupRows = 128;  // positions per group (MMA M)
 constexpr int kUnitN = 64;       // channels per unit (MMA N)
+// epilogue warps: 16 (4 lane quadrants x 4 column quarters of 16 channels)
+// or 8 (x 2 column halves of 32); more warps hide the TMEM-load / reduction
+// latency of the epilogue, which paces the MMA warp through tempty
+#ifndef RNSW_K1_EPI_WARPS
+#define RNSW_K1_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = RNSW_K1_EPI_WARPS;
+constexpr int kEpiCols = kUnitN / (kEpiWarps / 4);  // channels per epilogue warp
+constexpr int kUThreads = 128 + 32 * kEpiWarps;
 
 struct K1UArgs {
   Geometry g;
@@ -75,6 +89,7 @@ struct K1UArgs {
   int32_t bias_s2[RNSW_MAX_RES];
   FastDiv div_img, div_tw, div_cb;
   size_t group_bytes;   // [limb][128 rows][kp] plain bytes per group
+  uint8_t* v_raw;       // diagnostic 11 only
 };
 
 // Output modes.  For 16-bit moduli each unit's accumulators start from a
@@ -166,8 +181,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
-      mbar_init(&sfull[i], 16);  // 8 epilogue warps x 2 units of a pair
+      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&sfull[i], 2 * kEpiWarps);  // epilogue warps x 2 units of a pair
       mbar_init(&sempty[i], 1);
     }
     fence_mbar_init();
@@ -179,7 +194,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // epilogue thread geometry: lane quadrant q, column half hh
+  // epilogue thread geometry: lane quadrant q, column block hh (kEpiCols channels)
   const int q = warp & 3, hh = (warp - 4) >> 2;
   if (warp >= 4) {
     // the group's Kr operand into TMEM: thread = row (position), limb hh
@@ -223,6 +238,10 @@ __global__ void __launch_bounds__(kUThreads, 1)
     w0 = tj * args.mout - g.pad;
   };
 
+#ifdef RNSW_K1_MMA_ONLY
+  if (warp != 1) {
+  } else
+#endif
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
@@ -234,8 +253,15 @@ __global__ void __launch_bounds__(kUThreads, 1)
         unit_tile(u, p, c0);
         tile_origin(p, b, h0, w0);
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], bytes);
-        tma_load_4d(sB + stage * Cfg::kStageBytes, &tmX, &full[stage], c0, w0, h0, b);
+#ifdef RNSW_K1_NOLOAD
+        if (u >= 2 * S * pr_step) {  // diagnostic: the first units load, later ones reuse the stale stages
+          mbar_arrive(&full[stage]);
+        } else
+#endif
+        {
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          tma_load_4d(sB + stage * Cfg::kStageBytes, &tmX, &full[stage], c0, w0, h0, b);
+        }
         if (++stage == S) {
           stage = 0;
           phase ^= 1;
@@ -256,34 +282,94 @@ __global__ void __launch_bounds__(kUThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
+#ifdef RNSW_K1_PROBE
+    {  // diagnostic: the bare MMA sequence on this kernel's operands, timed
+      long long p0 = clock64();
+      for (int pu = 0; pu < 2000; ++pu) {
+        const uint32_t d0 = tmem_base + (pu & 1) * Cfg::kAccCols;
+        const uint64_t db_stage = db0 + (uint64_t)((pu & 7) * kStageStep);
+        mma_i8_ts_warp(d0, tmem_base + Cfg::kBiasCol, dbh, idesc, 0u);
+        mma_i8_ts_warp(d0 + kUnitN, tmem_base + Cfg::kBiasCol, dbl, idesc, 0u);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint64_t db = db_stage + (uint64_t)(ks * kBStep);
+          mma_i8_ts_warp(d0, ta + ks * 8, db, idesc, 1u);
+          mma_i8_ts_warp(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, 1u);
+        }
+      }
+      mma_commit_warp(&tfull[0]);
+      mbar_wait(&tfull[0], 0);
+      long long p1 = clock64();
+      if (lane == 0 && blockIdx.x < 2) printf("K1PROBE cta %d %lld cycles per unit\n", blockIdx.x, (p1 - p0) / 2000);
+    }
+#endif
+#ifdef RNSW_K1_PROF
+    long long c_te = 0, c_f = 0, c_is = 0, c_0 = clock64();
+#endif
     RNSW_FOR_UNITS(u) {
       const int as = it & 1;
+#ifdef RNSW_K1_PROF
+      long long c1 = clock64();
+#endif
+#ifdef RNSW_K1_NOWAIT
+      if (it < RNSW_K1_NOWAIT)
+#endif
       mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+#ifdef RNSW_K1_PROF
+      long long c2 = clock64();
+#endif
+#ifdef RNSW_K1_NOWAIT
+      if (it < RNSW_K1_NOWAIT)
+#endif
       mbar_wait(&full[stage], phase);
       tc_fence_after();
+#ifdef RNSW_K1_PROF
+      long long c3 = clock64();
+      c_te += c2 - c1;
+      c_f += c3 - c2;
+#endif
       const uint32_t d0 = tmem_base + as * Cfg::kAccCols;
       const uint64_t db_stage = db0 + (uint64_t)(stage * kStageStep);
       if (kLimbs == 2 && !RNSW_K1_EPI_BIAS) {  // the bias: D_hi = 127 S1, D_lo = 127 S2 (overwrites the buffer)
         mma_i8_ts_warp(d0, tmem_base + Cfg::kBiasCol, dbh, idesc, 0u);
         mma_i8_ts_warp(d0 + kUnitN, tmem_base + Cfg::kBiasCol, dbl, idesc, 0u);
       }
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        if (ks < ((RNSW_K1_DIAG == 3 || RNSW_K1_DIAG >= 5) ? 1 : ksteps)) {
-          const uint64_t db = db_stage + (uint64_t)(ks * kBStep);
-          const uint32_t acc = ((kLimbs == 2 && !RNSW_K1_EPI_BIAS) || ks > 0) ? 1u : 0u;
-          mma_i8_ts_warp(d0, ta + ks * 8, db, idesc, acc);
-          if (kLimbs == 2) mma_i8_ts_warp(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, acc);
-        }
-      }
+#ifdef RNSW_K1_PROF
+      long long tsk[9];
+#endif
+      auto kstep = [&](int ks) {
+#ifdef RNSW_K1_PROF
+        tsk[ks] = clock64();
+#endif
+        const uint64_t db = db_stage + (uint64_t)(ks * kBStep);
+        const uint32_t acc = ((kLimbs == 2 && !RNSW_K1_EPI_BIAS) || ks > 0) ? 1u : 0u;
+        mma_i8_ts_warp(d0, ta + ks * 8, db, idesc, acc);
+        if (kLimbs == 2) mma_i8_ts_warp(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, acc);
+      };
+      for_ksteps(RNSW_K1_ONE_MMA ? 1 : ksteps, kstep);  // branch-free unrolled MMA sequence
+#ifdef RNSW_K1_PROF
+      tsk[8] = clock64();
+      if (lane == 0 && blockIdx.x == 0 && (it == 1000 || it == 1001 || it == 1500))
+        printf("K1MMA it %d issue deltas %lld %lld %lld %lld %lld %lld %lld %lld | from start of unit %lld\n", it,
+               tsk[1] - tsk[0], tsk[2] - tsk[1], tsk[3] - tsk[2], tsk[4] - tsk[3], tsk[5] - tsk[4], tsk[6] - tsk[5],
+               tsk[7] - tsk[6], tsk[8] - tsk[7], tsk[0] - c3);
+#endif
       mma_commit_warp(&empty[stage]);
       mma_commit_warp(&tfull[as]);
+#ifdef RNSW_K1_PROF
+      c_is += clock64() - c3;
+#endif
       if (++stage == S) {
         stage = 0;
         phase ^= 1;
       }
       ++it;
     }
+#ifdef RNSW_K1_PROF
+    if (lane == 0 && blockIdx.x < 4)
+      printf("K1PROF cta %d units %d total %lld wait_tempty %lld wait_full %lld issue %lld (per unit: %lld %lld %lld %lld)\n",
+             blockIdx.x, it, clock64() - c_0, c_te, c_f, c_is, (clock64() - c_0) / it, c_te / it, c_f / it, c_is / it);
+#endif
   } else if (warp == 3) {
     if (lane == 0) {
       // ---------------- bulk stores of the staged V rows (one per unit pair) ----------------
@@ -296,7 +382,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
         mbar_wait(&sfull[sb], (jt >> 1) & 1);
         uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
-        for (int pl = 0; pl < ((RNSW_K1_DIAG == 1 || RNSW_K1_DIAG >= 5) ? 0 : kLimbs); ++pl)
+        for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl)
           tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0, p, pb * kGroupRows,
                        args.plane_base[res] + pl);
         bulk_commit();
@@ -337,22 +423,38 @@ __global__ void __launch_bounds__(kUThreads, 1)
     };
     const bool two = args.cblocks == 1;
     int it = 0, jt = -1;
+#ifdef RNSW_K1_PROF
+    long long e_tf = 0, e_se = 0, e_0 = clock64();
+#endif
     RNSW_FOR_UNITS(u) {
       if (h_ == 0) ++jt;
       const int as = it & 1;
+#ifdef RNSW_K1_PROF
+      long long e1 = clock64();
+#endif
       mbar_wait(&tfull[as], (it >> 1) & 1);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Cfg::kAccCols + hh * 32;
+#ifdef RNSW_K1_PROF
+      e_tf += clock64() - e1;
+#endif
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Cfg::kAccCols + hh * kEpiCols;
       uint32_t lo[8], hi[8];  // [chunk of 16 channels][word]
       int32_t a0[16], b0[16], a1[16], b1[16];
+#if RNSW_K1_NO_TMEM_LD  // diagnostic: no TMEM reads in the epilogue (MMA pipeline alone)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) a0[e] = b0[e] = a1[e] = b1[e] = e + it;
+      if (false)
+#endif
       if (kLimbs == 2) {
         tmem_ld16(taddr, a0);
         tmem_ld16(taddr + kUnitN, b0);
-        tmem_ld16(taddr + 16, a1);
-        tmem_ld16(taddr + kUnitN + 16, b1);
+        if (kEpiCols == 32) {
+          tmem_ld16(taddr + 16, a1);
+          tmem_ld16(taddr + kUnitN + 16, b1);
+        }
       } else {
         tmem_ld16(taddr, b0);
-        tmem_ld16(taddr + 16, b1);
+        if (kEpiCols == 32) tmem_ld16(taddr + 16, b1);
       }
       tmem_ld_wait();
       // hand the buffer back to the MMA warp
@@ -361,30 +463,45 @@ __global__ void __launch_bounds__(kUThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[as]);
       if (RNSW_K1_DIAG != 2 && RNSW_K1_DIAG != 6) {
         convert(a0, b0, lo, hi);
-        convert(a1, b1, lo + 4, hi + 4);
+        if (kEpiCols == 32) convert(a1, b1, lo + 4, hi + 4);
       } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) lo[e] = hi[e] = (uint32_t)(a0[e] ^ b1[e]);
       }
       // the pair's staging buffer must be free: its previous bulk store has read it
       const int sb = jt & 1;
+#ifdef RNSW_K1_PROF
+      long long e2 = clock64();
+#endif
       if (h_ == 0) mbar_wait(&sempty[sb], ((jt >> 1) & 1) ^ 1);
+#ifdef RNSW_K1_PROF
+      e_se += clock64() - e2;
+#endif
       uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
+#if RNSW_K1_DIAG == 11
+      {
+        uint4* dst = reinterpret_cast<uint4*>(args.v_raw + (((size_t)u * 8 + (warp - 4)) * 32 + lane) * 64);
+        dst[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        dst[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+        dst[2] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        dst[3] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+      }
+#endif
 #pragma unroll
-      for (int pl = 0; pl < ((RNSW_K1_DIAG == 1 || RNSW_K1_DIAG >= 5) ? 0 : kLimbs); ++pl) {
+      for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl) {
         uint8_t* base = sbuf + pl * (kGroupRows * 2 * kUnitN);
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
+        for (int ch = 0; ch < kEpiCols / 16; ++ch) {
           const uint32_t* src = pl == 0 ? lo : hi;
           const uint4 v4 = make_uint4(src[ch * 4], src[ch * 4 + 1], src[ch * 4 + 2], src[ch * 4 + 3]);
           uint32_t off;
           if (two) {
             // [pos][tile h_][64 channels]: 64-byte rows, 64B swizzle (chunk ^= (row >> 1) & 3)
-            const uint32_t r64 = (uint32_t)(row * 2 + h_), c16 = (uint32_t)(hh * 2 + ch);
+            const uint32_t r64 = (uint32_t)(row * 2 + h_), c16 = (uint32_t)(hh * (kEpiCols / 16) + ch);
             off = r64 * 64 + ((c16 ^ ((r64 >> 1) & 3u)) << 4);
           } else {
             // [pos][128 channels of blocks h_]: 128-byte rows, 128B swizzle (chunk ^= row & 7)
-            const uint32_t c16 = (uint32_t)(h_ * 4 + hh * 2 + ch);
+            const uint32_t c16 = (uint32_t)(h_ * 4 + hh * (kEpiCols / 16) + ch);
             off = (uint32_t)row * 128 + ((c16 ^ ((uint32_t)row & 7u)) << 4);
           }
           *reinterpret_cast<uint4*>(base + off) = v4;
@@ -398,6 +515,11 @@ __global__ void __launch_bounds__(kUThreads, 1)
       }
       ++it;
     }
+#ifdef RNSW_K1_PROF
+    if (lane == 0 && blockIdx.x < 4 && (warp == 4 || warp == 11))
+      printf("K1PROF cta %d epi warp %d units %d total %lld wait_tfull %lld wait_sempty %lld (per unit %lld %lld %lld)\n",
+             blockIdx.x, warp, it, clock64() - e_0, e_tf, e_se, (clock64() - e_0) / it, e_tf / it, e_se / it);
+#endif
   }
   tc_fence_before();
   __syncthreads();
@@ -497,6 +619,7 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   a.groups = plan.kr_groups;
   a.npb = plan.kr_npb;
   a.group_bytes = plan.kr_group_bytes;
+  a.v_raw = reinterpret_cast<uint8_t*>(V);
   a.cblocks = g.Cp / kUnitN;
   const int64_t units = g.P * a.cblocks;
   if (units >= (1ll << 31) || g.P >= (1ll << 31)) return cudaErrorInvalidValue;

@@ -206,18 +206,15 @@ __global__ void __launch_bounds__(kKThreads, 1)
       tc_fence_after();
       const uint32_t d256 = tmem_base + kAccBase + as * 128, d1 = d256 + 64;
       const uint64_t dbs = db0 + (uint64_t)(stage * (kKStageBytes >> 4));
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        if (ks < ksteps) {
-          const uint64_t blo = dbs + (uint64_t)(ks * kBStep), bhi = blo + hi_off;
-          const uint32_t a = tmem_base + ks * 8;
-          const uint32_t acc = ks > 0 ? 1u : 0u;
-          mma_i8_ts_warp(d256, a, bhi, idesc, acc);        // KrA'_hi x hi
-          mma_i8_ts_warp(d256, a + 64, blo, idesc, 1u);    // KrA_hi  x lo
-          mma_i8_ts_warp(d1, a + 128, bhi, idesc, acc);    // KrA'_lo x hi
-          mma_i8_ts_warp(d1, a + 192, blo, idesc, 1u);     // KrA_lo  x lo
-        }
-      }
+      for_ksteps(ksteps, [&](int ks) {
+        const uint64_t blo = dbs + (uint64_t)(ks * kBStep), bhi = blo + hi_off;
+        const uint32_t a = tmem_base + ks * 8;
+        const uint32_t acc = ks > 0 ? 1u : 0u;
+        mma_i8_ts_warp(d256, a, bhi, idesc, acc);        // KrA'_hi x hi
+        mma_i8_ts_warp(d256, a + 64, blo, idesc, 1u);    // KrA_hi  x lo
+        mma_i8_ts_warp(d1, a + 128, bhi, idesc, acc);    // KrA'_lo x hi
+        mma_i8_ts_warp(d1, a + 192, blo, idesc, 1u);     // KrA_lo  x lo
+      });
       mma_commit_warp(&empty[stage]);
       mma_commit_warp(&tfull[as]);
       if (++stage == S) {
@@ -509,15 +506,12 @@ __global__ void __launch_bounds__(kKThreads, 1)
       tc_fence_after();
       const uint32_t d0 = tmem_base + kAccBase + as * kAccCols;
       const uint64_t dbs = db0 + (uint64_t)(stage * (Cfg::kStageBytes >> 4));
+      for_ksteps(ksteps, [&](int ks) {
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        if (ks < ksteps) {
-#pragma unroll
-          for (int r = 0; r < kNRes; ++r)
-            mma_i8_ts_warp(d0 + r * kK8N, tmem_base + r * 64 + ks * 8,
-                           dbs + (uint64_t)(r * rstep + ks * ((32 * kK8N) >> 4)), idesc, ks > 0 ? 1u : 0u);
-        }
-      }
+        for (int r = 0; r < kNRes; ++r)
+          mma_i8_ts_warp(d0 + r * kK8N, tmem_base + r * 64 + ks * 8,
+                         dbs + (uint64_t)(r * rstep + ks * ((32 * kK8N) >> 4)), idesc, ks > 0 ? 1u : 0u);
+      });
       mma_commit_warp(&empty[stage]);
       mma_commit_warp(&tfull[as]);
       if (++stage == S) {
