@@ -435,6 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // instructions go out together instead of back to back from one thread
     int stage = 0;
     uint32_t phase = 0;
+#ifdef RNSW_GEMM_NOLOAD
+    int nfill = 0;
+#endif
     for (int64_t t = u_begin; t < args.total_tiles; t += u_step) {
       const TileCoord tc = tile_coord((uint32_t)t, args);
       const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
@@ -445,6 +448,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
       for (int kc = 0; kc < args.nkc; ++kc) {
         mbar_wait(&empty[stage], phase ^ 1);
+#ifdef RNSW_GEMM_NOLOAD  // diagnostic: after two rounds of the ring, stages are reused without loads
+        if (++nfill > 2 * S) {
+          if (lane == 0) mbar_arrive(&full[stage]);
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+          continue;
+        }
+#endif
         if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
         __syncwarp();
         if (lane < pl) {
@@ -585,6 +599,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
+#ifdef RNSW_GEMM_NOEPI  // diagnostic: hand the accumulator straight back (no reads, no stores)
+      release_acc(&tempty[as], lane);
+      continue;
+#endif
       const int64_t p = (int64_t)pb * kBlockM + q * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * Tr::kAccCols + half * kHalf;
       int16_t* out_row = args.Mw + mw_offset(p, res * args.npos + pos, args.n_res * args.npos, args.Kp);

@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -149,10 +150,22 @@ __global__ void __launch_bounds__(kThr, 2)
     issue_p1();
   }
 
+#ifdef RNSW_K4_PROF
+  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt0 = clock64();
+  int pn = 0;
+#define K4T(i) { long long _c = clock64(); pc[i] += _c - pl_; pl_ = _c; }
+#else
+#define K4T(i)
+#endif
   for (int64_t u = blockIdx.x; u < args.units; u += u_step) {
+#ifdef RNSW_K4_PROF
+    long long pl_ = clock64();
+    ++pn;
+#endif
     const int p = unit_p(u), k0 = (int)(u - (int64_t)p * args.kblocks) * kKB;
     // ---- pass 1 (issued before the previous unit's stores) ----
     mbar_wait(my_bar, ph_mma);
+    K4T(0)
     ph_mma ^= 1;
     tc_fence_after();
     // the second group's barrier means all of pass 1 is done: A1 is free
@@ -203,9 +216,11 @@ __global__ void __launch_bounds__(kThr, 2)
       tmem_ld_wait();
       body(3, hB, lB);
     }
+    K4T(1)
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
+    K4T(2)
 
     // ---- pass 2 into the same columns (pass 1 has been read) ----
     if (warp == 0) {
@@ -223,9 +238,11 @@ __global__ void __launch_bounds__(kThr, 2)
       }
       mma_commit_warp(&bar[2]);
     }
+    K4T(3)
     mbar_wait(my_bar, ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
+    K4T(4)
 
     // ---- epilogue 2: lane row (k, a) = (2q + lane/16, lane % 16) of channel blocks mb = 2h, 2h+1 ----
     const int b_img = (int)fdiv((uint32_t)p, args.div_img);
@@ -288,8 +305,10 @@ __global__ void __launch_bounds__(kThr, 2)
       }
       }
     }
+    K4T(5)
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
+    K4T(6)
     if (warp == 0 && u + u_step < args.units) {
       tc_fence_after();
       issue_p1();  // the next unit's pass 1 overlaps these stores
@@ -335,8 +354,15 @@ __global__ void __launch_bounds__(kThr, 2)
         *reinterpret_cast<uint32_t*>(args.out8 + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 4 * wq) = word;
       }
     }
+    K4T(7)
   }
 
+#ifdef RNSW_K4_PROF
+  if (lane == 0 && blockIdx.x < 2 && (warp == 0 || warp == 1 || warp == 4) && pn > 0)
+    printf("K4PROF cta %d warp %d units %d per-unit cycles: total %lld | wait_p1 %lld epi1 %lld bar1 %lld p2issue %lld wait_p2 %lld epi2 %lld bar2 %lld stores+p1issue %lld\n",
+           blockIdx.x, warp, pn, (clock64() - pt0) / pn, pc[0] / pn, pc[1] / pn, pc[2] / pn, pc[3] / pn, pc[4] / pn,
+           pc[5] / pn, pc[6] / pn, pc[7] / pn);
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {

@@ -17,4 +17,5 @@ for f in $R/paper_2007_12216_b200/build/*.o; do
   fi
 done
 nvcc -shared -gencode arch=compute_100a,code=sm_100a $objs -o $R/ab/$name.so -lcudart
+rm -rf $R/ab/obj_$name
 echo built ab/$name.so
