@@ -51,6 +51,7 @@
 #define RNSW_K1_ONE_MMA (RNSW_K1_DIAG == 3 || (RNSW_K1_DIAG >= 5 && RNSW_K1_DIAG <= 8))
 #define RNSW_K1_NO_STORE (RNSW_K1_DIAG == 1 || (RNSW_K1_DIAG >= 5 && RNSW_K1_DIAG <= 8) || RNSW_K1_DIAG >= 10)
 // 11 = no staging / bulk stores; each epilogue lane writes its 64 bytes straight to global (wrong layout)
+// 12 = no staging writes (the bulk stores still run, on stale staging)
 #define RNSW_K1_NO_TMEM_LD (RNSW_K1_DIAG == 9 || RNSW_K1_DIAG == 10)
 // 1: the accumulator bias is added in the epilogue (one IADD per value)
 // instead of by two bias MMAs per unit (11% of the unit's tensor work) --
@@ -90,6 +91,7 @@ struct K1UArgs {
   FastDiv div_img, div_tw, div_cb;
   size_t group_bytes;   // [limb][128 rows][kp] plain bytes per group
   uint8_t* v_raw;       // diagnostic 11 only
+  int pair128;          // Cp == 64 and P even: a unit pair's two tiles are one 128-byte V row
 };
 
 // Output modes.  For 16-bit moduli each unit's accumulators start from a
@@ -383,7 +385,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
         uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
         for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl)
-          tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0, p, pb * kGroupRows,
+          tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0,
+                       (two && args.pair128) ? (p >> 1) : p, pb * kGroupRows,
                        args.plane_base[res] + pl);
         bulk_commit();
         bulk_wait_read<0>();  // the staging buffer may be rewritten
@@ -488,15 +491,22 @@ __global__ void __launch_bounds__(kUThreads, 1)
       }
 #endif
 #pragma unroll
-      for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl) {
+      for (int pl = 0; pl < ((RNSW_K1_NO_STORE || RNSW_K1_DIAG == 12) ? 0 : kLimbs); ++pl) {
         uint8_t* base = sbuf + pl * (kGroupRows * 2 * kUnitN);
 #pragma unroll
         for (int ch = 0; ch < kEpiCols / 16; ++ch) {
           const uint32_t* src = pl == 0 ? lo : hi;
           const uint4 v4 = make_uint4(src[ch * 4], src[ch * 4 + 1], src[ch * 4 + 2], src[ch * 4 + 3]);
           uint32_t off;
-          if (two) {
-            // [pos][tile h_][64 channels]: 64-byte rows, 64B swizzle (chunk ^= (row >> 1) & 3)
+          if (two && args.pair128) {
+            // [pos][tiles 2k, 2k+1][64 channels] as one 128-byte row under the
+            // 128B swizzle: the 32 positions of a warp spread over all 32
+            // banks (64-byte rows under the 64B swizzle put them on 4 chunk
+            // columns, 8-way conflicts)
+            const uint32_t c16 = (uint32_t)(h_ * 4 + hh * (kEpiCols / 16) + ch);
+            off = (uint32_t)row * 128 + ((c16 ^ ((uint32_t)row & 7u)) << 4);
+          } else if (two) {
+            // odd P: [pos][tile h_][64 channels], 64-byte rows, 64B swizzle (chunk ^= (row >> 1) & 3)
             const uint32_t r64 = (uint32_t)(row * 2 + h_), c16 = (uint32_t)(hh * (kEpiCols / 16) + ch);
             off = r64 * 64 + ((c16 ^ ((r64 >> 1) & 3u)) << 4);
           } else {
@@ -668,8 +678,9 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   CUtensorMap tmV2;
   {
     // V as (Cp, P, npos, planes); a unit pair's box = 64 channels x 2 tiles x
-    // 128 positions x 1 plane (Cp = 64, 64B swizzle) or 128 channels x 1 tile
-    // x 128 positions x 1 plane (128B swizzle)
+    // 128 positions x 1 plane (Cp = 64: with P even one 128-byte row per
+    // position, 128B swizzle; odd P 64B swizzle) or 128 channels x 1 tile x
+    // 128 positions x 1 plane (128B swizzle)
     const int npos = d.n * d.n;
     cuuint64_t dims[4] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P, (cuuint64_t)npos, (cuuint64_t)d.n_planes};
 #if RNSW_K1_DIAG == 4
@@ -679,11 +690,23 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
     cuuint64_t strides[3] = {(cuuint64_t)g.Cp, (cuuint64_t)g.P * g.Cp, (cuuint64_t)g.P * g.Cp * npos};
 #endif
     cuuint32_t es[4] = {1, 1, 1, 1};
-    cuuint32_t box[4] = {(cuuint32_t)kUnitN, 2, (cuuint32_t)kGroupRows, 1};
-    if (encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
+    a.pair128 = (g.Cp == 64 && (g.P & 1) == 0) ? 1 : 0;
+    if (a.pair128) {
+      // tile pairs as 128-byte rows: (2 Cp, P / 2, npos, planes)
+      cuuint64_t dims2[4] = {(cuuint64_t)(2 * g.Cp), (cuuint64_t)(g.P / 2), (cuuint64_t)npos, (cuuint64_t)d.n_planes};
+      cuuint64_t strides2[3] = {(cuuint64_t)(2 * g.Cp), (cuuint64_t)g.P * g.Cp, (cuuint64_t)g.P * g.Cp * npos};
+      cuuint32_t boxp[4] = {(cuuint32_t)(2 * kUnitN), 1, (cuuint32_t)kGroupRows, 1};
+      if (encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims2, strides2, boxp, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    } else {
+      cuuint32_t box[4] = {(cuuint32_t)kUnitN, 2, (cuuint32_t)kGroupRows, 1};
+      if (encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    }
     cuuint32_t box2[4] = {(cuuint32_t)(2 * kUnitN), 1, (cuuint32_t)kGroupRows, 1};
     if (g.Cp >= 128 && encode(&tmV2, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims, strides, box2, es,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
