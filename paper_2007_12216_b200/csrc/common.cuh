@@ -264,6 +264,13 @@ RNSW_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
 RNSW_DEV void mbar_arrive_cluster(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
 }
+// Arrive on an mbarrier of another CTA of the cluster with the default
+// (.release.cta) semantics, as CUTLASS's ClusterBarrier does: enough for
+// handing TMEM back across a CTA pair (the tcgen05 fences order the TMEM
+// accesses), without the cluster-scope release / acquire cost.
+RNSW_DEV void mbar_arrive_remote(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
 // Wait (acquire, cluster scope): the arrivals may come from other CTAs.
 RNSW_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
@@ -315,6 +322,51 @@ RNSW_DEV void tmem_alloc(uint32_t* dst_smem) {
 template <uint32_t kCols>
 RNSW_DEV void tmem_dealloc(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+
+// ---- CTA pairs (cta_group::2): one MMA spans the TMEM of both CTAs of a
+// 2-CTA cluster (M = 256, each CTA's TMEM holds its 128 rows; B is split
+// along N, each CTA's shared memory holding its N/2 columns at the same
+// offset).  Only the even CTA issues; loads of both CTAs complete on its
+// mbarrier; commits multicast to both.
+template <uint32_t kCols>
+RNSW_DEV void tmem_alloc_2sm(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <uint32_t kCols>
+RNSW_DEV void tmem_dealloc_2sm(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+// 4-D tensor load into this CTA's shared memory whose transaction bytes
+// complete on the pair leader's mbarrier (leader_bar: shared::cluster address)
+RNSW_DEV void tma_load_4d_2sm(void* dst, const void* desc, uint32_t leader_bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// A from tensor memory, B from shared memory, across the CTA pair (warp-collective issue)
+RNSW_DEV void mma_i8_ts_warp_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// commit the pair's prior MMAs to the mbarrier at this offset in both CTAs
+RNSW_DEV void mma_commit_warp_2sm(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
 }
 
 // D[tmem] (+)= A[smem] * B[smem], s8 x s8 -> s32, one elected thread.

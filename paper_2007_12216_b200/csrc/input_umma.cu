@@ -53,6 +53,13 @@
 // 11 = no staging / bulk stores; each epilogue lane writes its 64 bytes straight to global (wrong layout)
 // 12 = no staging writes (the bulk stores still run, on stale staging)
 #define RNSW_K1_NO_TMEM_LD (RNSW_K1_DIAG == 9 || RNSW_K1_DIAG == 10)
+// 1: the epilogue writes the staging tile with st.async (async proxy, 16
+// transaction bytes each on the staging buffer's mbarrier; needs a cluster
+// launch) instead of st.shared + fence.proxy.async + arrive -- measured 1.55x
+// slower, so off
+#ifndef RNSW_K1_STASYNC
+#define RNSW_K1_STASYNC 0
+#endif
 // 1: the accumulator bias is added in the epilogue (one IADD per value)
 // instead of by two bias MMAs per unit (11% of the unit's tensor work) --
 // measured 7% slower on conv1_2 than the bias MMAs, so off
@@ -130,11 +137,16 @@ struct K1UConfig {
       1024 + (size_t)kStages * kStageBytes + 2 * (size_t)kStgBytes + kBiasBytes + 256;
 };
 
-template <int kMode>
+// kPair: a 2-CTA cluster serves both 128-position blocks of a residue (N*N >
+// 128): one cta_group::2 MMA of M = 256 per K-step and limb, A = each CTA's
+// block of Kr in its own TMEM, B = the patch split by channels (32 per CTA),
+// so each SM loads and the tensor core reads half of the patch per unit.
+template <int kMode, bool kPair>
 __global__ void __launch_bounds__(kUThreads, 1)
     input_umma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmV,
                       const __grid_constant__ CUtensorMap tmV2, const uint8_t* __restrict__ kr, K1UArgs args) {
   constexpr int kLimbs = kMode == kSym8 ? 1 : 2;
+  constexpr int kBN = kPair ? kUnitN / 2 : kUnitN;  // patch channels (B columns) in this CTA's shared memory
   using Cfg = K1UConfig<kLimbs>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -152,15 +164,19 @@ __global__ void __launch_bounds__(kUThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int group = (int)(blockIdx.x % args.groups);
+  const uint32_t crank = kPair ? cluster_ctarank() : 0u;
+  const int cid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // cluster (or CTA) id
+  const int ncl = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int group = cid % args.groups;
   // units come in pairs (2k, 2k+1): two consecutive tiles when Cp = 64, else
   // two consecutive 64-channel blocks of one tile (Cp is a multiple of 128)
-  const int pr_begin = (int)(blockIdx.x / args.groups), pr_step = (int)(gridDim.x / args.groups);
+  const int pr_begin = cid / args.groups, pr_step = ncl / args.groups;
   const int npairs = (args.units + 1) / 2;
 #define RNSW_FOR_UNITS(u)                                              \
   for (int pr_ = pr_begin; pr_ < npairs; pr_ += pr_step)               \
     for (int h_ = 0, u = 2 * pr_; h_ < 2 && u < args.units; ++h_, ++u)
-  const int res = args.res_of[group], pb = args.pb_of[group];
+  const int res = args.res_of[group], pb = kPair ? (int)crank : args.pb_of[group];
+  const int kr_group = kPair ? res * args.npb + pb : group;  // Kr image of (residue, position block)
   const Geometry& g = args.g;
   const FastMod fm = args.fm[res];
 
@@ -168,8 +184,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
     // bias B operands: row k of B_hi = beta_k (sum S1), of B_lo = gamma_k
     // (sum S2); uniform rows, so the swizzle is moot
     const int s1 = args.bias_s1[res], s2 = args.bias_s2[res];
-    for (int i = threadIdx.x; i < 2 * 32 * kUnitN / 4; i += kUThreads) {
-      const int k = (i % (32 * kUnitN / 4)) / (kUnitN / 4), sum = i < 32 * kUnitN / 4 ? s1 : s2;
+    for (int i = threadIdx.x; i < 2 * 32 * kBN / 4; i += kUThreads) {
+      const int k = (i % (32 * kBN / 4)) / (kBN / 4), sum = i < 32 * kBN / 4 ? s1 : s2;
       const int beta = sum / 32 + (k < (sum % 32) ? 1 : 0);
       reinterpret_cast<uint32_t*>(sBias)[i] = (uint32_t)(uint8_t)(int8_t)beta * 0x01010101u;
     }
@@ -183,13 +199,18 @@ __global__ void __launch_bounds__(kUThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
-      mbar_init(&sfull[i], 2 * kEpiWarps);  // epilogue warps x 2 units of a pair
+      mbar_init(&tempty[i], kPair ? 2 * kEpiWarps : kEpiWarps);  // kPair: both CTAs' epilogue warps
+      mbar_init(&sfull[i], RNSW_K1_STASYNC ? 1 : 2 * kEpiWarps);  // store warp (tx bytes) / epilogue warps x 2 units
       mbar_init(&sempty[i], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if (kPair)
+      tmem_alloc_2sm<Cfg::kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  }
   fence_proxy_async();  // bias operands (generic stores) -> visible to the MMA (async proxy)
   tc_fence_before();
   __syncthreads();
@@ -204,7 +225,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
     const int row = q * 32 + lane;
     const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16);
     if (hh < kLimbs) {
-      const uint4* src = reinterpret_cast<const uint4*>(kr + (size_t)group * args.group_bytes +
+      const uint4* src = reinterpret_cast<const uint4*>(kr + (size_t)kr_group * args.group_bytes +
                                                         ((size_t)hh * kGroupRows + row) * args.kp);
       for (int c8 = 0; c8 < args.kp / 32; ++c8) {  // 8 columns = 32 K bytes per store
         const uint4 w0 = __ldg(src + 2 * c8), w1 = __ldg(src + 2 * c8 + 1);
@@ -220,7 +241,10 @@ __global__ void __launch_bounds__(kUThreads, 1)
     tmem_st_wait();
   }
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    cluster_sync();  // both CTAs' Kr in TMEM and barriers initialised before the pair's first MMA / remote arrival
+  else
+    __syncthreads();
   tc_fence_after();
 
   // unit -> tile, channel offset
@@ -247,7 +271,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      const uint32_t bytes = (uint32_t)(args.npos * kUnitN);
+      const uint32_t bytes = (uint32_t)(args.npos * kBN);
       int stage = 0;
       uint32_t phase = 0;
       RNSW_FOR_UNITS(u) {
@@ -260,7 +284,12 @@ __global__ void __launch_bounds__(kUThreads, 1)
           mbar_arrive(&full[stage]);
         } else
 #endif
-        {
+        if (kPair) {
+          // this CTA's 32 channels; the bytes of both halves complete on the leader's barrier
+          if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+          tma_load_4d_2sm(sB + stage * Cfg::kStageBytes, &tmX, mapa_shared(smem_u32(&full[stage]), 0),
+                          c0 + (int)crank * kBN, w0, h0, b);
+        } else {
           mbar_arrive_expect_tx(&full[stage], bytes);
           tma_load_4d(sB + stage * Cfg::kStageBytes, &tmX, &full[stage], c0, w0, h0, b);
         }
@@ -270,14 +299,22 @@ __global__ void __launch_bounds__(kUThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && (!kPair || crank == 0)) {
     // ---------------- MMA issuer (warp-collective: descriptors stay uniform) ----------------
-    constexpr uint32_t idesc = idesc_i8x(128, kUnitN, true, true, false, true);  // A K-major (TMEM), B MN-major
+    // kPair: M = 256 over the CTA pair, N = 64 split 32 + 32 (32B-swizzled halves)
+    constexpr uint32_t idesc = idesc_i8x(kPair ? 256 : 128, kUnitN, true, true, false, true);  // A K-major (TMEM), B MN-major
     // descriptors advance by adding the byte offset / 16 to the start-address field
-    const uint64_t db0 = umma_desc_mn_sw64(smem_u32(sB), 16);
-    const uint64_t dbh = umma_desc_mn_sw64(smem_u32(sBias), 16);
-    const uint64_t dbl = umma_desc_mn_sw64(smem_u32(sBias + 32 * kUnitN), 16);
-    constexpr uint32_t kBStep = (32 * kUnitN) >> 4;  // one K-step of the patch
+    const uint64_t db0 = kPair ? umma_desc_mn_sw32(smem_u32(sB), 1024) : umma_desc_mn_sw64(smem_u32(sB), 16);
+    const uint64_t dbh = kPair ? umma_desc_mn_sw32(smem_u32(sBias), 1024) : umma_desc_mn_sw64(smem_u32(sBias), 16);
+    const uint64_t dbl = kPair ? umma_desc_mn_sw32(smem_u32(sBias + 32 * kBN), 1024)
+                               : umma_desc_mn_sw64(smem_u32(sBias + 32 * kBN), 16);
+    constexpr uint32_t kBStep = (32 * kBN) >> 4;  // one K-step of the patch
+    auto mma_ts = [&](uint32_t d, uint32_t a, uint64_t bd, uint32_t id, uint32_t acc) {
+      if (kPair)
+        mma_i8_ts_warp_2sm(d, a, bd, id, acc);
+      else
+        mma_i8_ts_warp(d, a, bd, id, acc);
+    };
     constexpr uint32_t kStageStep = Cfg::kStageBytes >> 4;
     const uint32_t ta = tmem_base + Cfg::kACol;
     const int ksteps = args.ksteps;
@@ -285,7 +322,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
     uint32_t phase = 0;
     int it = 0;
 #ifdef RNSW_K1_PROBE
-    {  // diagnostic: the bare MMA sequence on this kernel's operands, timed
+    if (!kPair) {  // diagnostic: the bare MMA sequence on this kernel's operands, timed
       long long p0 = clock64();
       for (int pu = 0; pu < 2000; ++pu) {
         const uint32_t d0 = tmem_base + (pu & 1) * Cfg::kAccCols;
@@ -316,7 +353,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
 #ifdef RNSW_K1_NOWAIT
       if (it < RNSW_K1_NOWAIT)
 #endif
-      mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);  // kPair: releases from both CTAs
 #ifdef RNSW_K1_PROF
       long long c2 = clock64();
 #endif
@@ -333,8 +370,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
       const uint32_t d0 = tmem_base + as * Cfg::kAccCols;
       const uint64_t db_stage = db0 + (uint64_t)(stage * kStageStep);
       if (kLimbs == 2 && !RNSW_K1_EPI_BIAS) {  // the bias: D_hi = 127 S1, D_lo = 127 S2 (overwrites the buffer)
-        mma_i8_ts_warp(d0, tmem_base + Cfg::kBiasCol, dbh, idesc, 0u);
-        mma_i8_ts_warp(d0 + kUnitN, tmem_base + Cfg::kBiasCol, dbl, idesc, 0u);
+        mma_ts(d0, tmem_base + Cfg::kBiasCol, dbh, idesc, 0u);
+        mma_ts(d0 + kUnitN, tmem_base + Cfg::kBiasCol, dbl, idesc, 0u);
       }
 #ifdef RNSW_K1_PROF
       long long tsk[9];
@@ -345,8 +382,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
 #endif
         const uint64_t db = db_stage + (uint64_t)(ks * kBStep);
         const uint32_t acc = ((kLimbs == 2 && !RNSW_K1_EPI_BIAS) || ks > 0) ? 1u : 0u;
-        mma_i8_ts_warp(d0, ta + ks * 8, db, idesc, acc);
-        if (kLimbs == 2) mma_i8_ts_warp(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, acc);
+        mma_ts(d0, ta + ks * 8, db, idesc, acc);
+        if (kLimbs == 2) mma_ts(d0 + kUnitN, ta + 64 + ks * 8, db, idesc, acc);
       };
       for_ksteps(RNSW_K1_ONE_MMA ? 1 : ksteps, kstep);  // branch-free unrolled MMA sequence
 #ifdef RNSW_K1_PROF
@@ -356,8 +393,13 @@ __global__ void __launch_bounds__(kUThreads, 1)
                tsk[1] - tsk[0], tsk[2] - tsk[1], tsk[3] - tsk[2], tsk[4] - tsk[3], tsk[5] - tsk[4], tsk[6] - tsk[5],
                tsk[7] - tsk[6], tsk[8] - tsk[7], tsk[0] - c3);
 #endif
-      mma_commit_warp(&empty[stage]);
-      mma_commit_warp(&tfull[as]);
+      if (kPair) {
+        mma_commit_warp_2sm(&empty[stage]);
+        mma_commit_warp_2sm(&tfull[as]);
+      } else {
+        mma_commit_warp(&empty[stage]);
+        mma_commit_warp(&tfull[as]);
+      }
 #ifdef RNSW_K1_PROF
       c_is += clock64() - c3;
 #endif
@@ -381,6 +423,13 @@ __global__ void __launch_bounds__(kUThreads, 1)
         int p, c0;
         unit_tile(2 * pr, p, c0);
         const int sb = jt & 1;
+        if (RNSW_K1_STASYNC && !RNSW_K1_NO_STORE && RNSW_K1_DIAG != 12) {
+          // the pair's staging bytes arrive as st.async transactions
+          const uint32_t nun = 2 * pr + 1 < args.units ? 2u : 1u;
+          mbar_arrive_expect_tx(&sfull[sb], nun * (uint32_t)(kLimbs * kGroupRows * kUnitN));
+        } else if (RNSW_K1_STASYNC) {
+          mbar_arrive(&sfull[sb]);
+        }
         mbar_wait(&sfull[sb], (jt >> 1) & 1);
         uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
@@ -460,10 +509,15 @@ __global__ void __launch_bounds__(kUThreads, 1)
         if (kEpiCols == 32) tmem_ld16(taddr + 16, b1);
       }
       tmem_ld_wait();
-      // hand the buffer back to the MMA warp
+      // hand the buffer back to the MMA warp (kPair: the leader CTA's barrier)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (lane == 0) {
+        if (kPair)
+          mbar_arrive_remote(mapa_shared(smem_u32(&tempty[as]), 0));
+        else
+          mbar_arrive(&tempty[as]);
+      }
       if (RNSW_K1_DIAG != 2 && RNSW_K1_DIAG != 6) {
         convert(a0, b0, lo, hi);
         if (kEpiCols == 32) convert(a1, b1, lo + 4, hi + 4);
@@ -514,14 +568,19 @@ __global__ void __launch_bounds__(kUThreads, 1)
             const uint32_t c16 = (uint32_t)(h_ * 4 + hh * (kEpiCols / 16) + ch);
             off = (uint32_t)row * 128 + ((c16 ^ ((uint32_t)row & 7u)) << 4);
           }
-          *reinterpret_cast<uint4*>(base + off) = v4;
+          if (RNSW_K1_STASYNC)
+            st_async_v4(smem_u32(base + off), v4, smem_u32(&sfull[sb]));
+          else
+            *reinterpret_cast<uint4*>(base + off) = v4;
         }
       }
-      fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&sfull[sb]);
-        if (h_ == 0 && u + 1 >= args.units) mbar_arrive(&sfull[sb]);  // a lone last unit
+      if (!RNSW_K1_STASYNC) {
+        fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&sfull[sb]);
+          if (h_ == 0 && u + 1 >= args.units) mbar_arrive(&sfull[sb]);  // a lone last unit
+        }
       }
       ++it;
     }
@@ -532,10 +591,16 @@ __global__ void __launch_bounds__(kUThreads, 1)
 #endif
   }
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    cluster_sync();  // the pair's last MMAs and TMEM reads are done in both CTAs
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    if (kPair)
+      tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
+    else
+      tmem_dealloc<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -626,7 +691,12 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   a.kp = plan.kr_kp;
   a.ksteps = plan.kr_kp / 32;
   a.limbs = plan.kr_limbs;
-  a.groups = plan.kr_groups;
+  // CTA pairs (cta_group::2) when a residue has two 128-position blocks
+  // (opt-in, RNSW_K1_PAIR=1: measured equal or slower -- K1 is not bound by
+  // its patch reads)
+  static const bool want_pair = getenv("RNSW_K1_PAIR") != nullptr;
+  const bool pair = want_pair && plan.kr_npb == 2;
+  a.groups = pair ? d.n_res : plan.kr_groups;
   a.npb = plan.kr_npb;
   a.group_bytes = plan.kr_group_bytes;
   a.v_raw = reinterpret_cast<uint8_t*>(V);
@@ -635,8 +705,8 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   if (units >= (1ll << 31) || g.P >= (1ll << 31)) return cudaErrorInvalidValue;
   a.units = (int)units;
   for (int gi = 0; gi < a.groups; ++gi) {
-    a.res_of[gi] = gi / a.npb;
-    a.pb_of[gi] = gi % a.npb;
+    a.res_of[gi] = pair ? gi : gi / a.npb;
+    a.pb_of[gi] = pair ? 0 : gi % a.npb;  // pair: the CTA's rank in its cluster
   }
   for (int r = 0; r < d.n_res; ++r) {
     a.plane_base[r] = d.res[r].plane_base;
@@ -665,14 +735,14 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   if (encode == nullptr) return cudaErrorInvalidValue;
   CUtensorMap tmX, tmV;
   {
-    // x NHWC as (C, W, H, B); box = 64 channels x N x N x 1
+    // x NHWC as (C, W, H, B); box = 64 channels x N x N x 1 (pair: 32 channels per CTA, 32B swizzle)
     cuuint64_t dims[4] = {(cuuint64_t)g.C, (cuuint64_t)g.W, (cuuint64_t)g.H, (cuuint64_t)g.B};
     cuuint64_t strides[3] = {(cuuint64_t)g.C, (cuuint64_t)g.W * g.C, (cuuint64_t)g.H * g.W * g.C};
-    cuuint32_t box[4] = {(cuuint32_t)kUnitN, (cuuint32_t)d.n, (cuuint32_t)d.n, 1};
+    cuuint32_t box[4] = {(cuuint32_t)(pair ? kUnitN / 2 : kUnitN), (cuuint32_t)d.n, (cuuint32_t)d.n, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     if (encode(&tmX, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(x), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+               CU_TENSOR_MAP_INTERLEAVE_NONE, pair ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
   CUtensorMap tmV2;
@@ -714,8 +784,10 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
       return cudaErrorInvalidValue;
     if (g.Cp < 128) tmV2 = tmV;
   }
+  // one CTA (or CTA pair) per SM (pair) spread evenly over the groups
   const int sms = num_sms_current();
-  const int per_group = sms / a.groups > 0 ? sms / a.groups : 1;
+  const int slots = pair ? sms / 2 : sms;
+  const int per_group = slots / a.groups > 0 ? slots / a.groups : 1;
   int64_t grid = (int64_t)per_group * a.groups;
   const int64_t need = (int64_t)((a.units + 1) / 2) * a.groups;
   if (grid > need) grid = need;
@@ -723,13 +795,36 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   auto run = [&](auto kern, size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)grid, kUThreads, smem, s>>>(tmX, tmV, tmV2, plan.d_kr, a);
-    return cudaGetLastError();
+    if (!pair && !RNSW_K1_STASYNC) {
+      kern<<<(unsigned)grid, kUThreads, smem, s>>>(tmX, tmV, tmV2, plan.d_kr, a);
+      return cudaGetLastError();
+    }
+    // a cluster launch (st.async into the CTA's own shared memory needs the
+    // shared::cluster window)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(pair ? 2 * grid : grid));
+    cfg.blockDim = dim3(kUThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pair ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmX, tmV, tmV2, plan.d_kr, a);
   };
+  if (pair) {
+    if (plan.kr_limbs == 2)
+      return relaxed ? run(input_umma_kernel<kRel16, true>, K1UConfig<2>::kSmem)
+                     : run(input_umma_kernel<kSym16, true>, K1UConfig<2>::kSmem);
+    return run(input_umma_kernel<kSym8, true>, K1UConfig<1>::kSmem);
+  }
   if (plan.kr_limbs == 2)
-    return relaxed ? run(input_umma_kernel<kRel16>, K1UConfig<2>::kSmem)
-                   : run(input_umma_kernel<kSym16>, K1UConfig<2>::kSmem);
-  return run(input_umma_kernel<kSym8>, K1UConfig<1>::kSmem);
+    return relaxed ? run(input_umma_kernel<kRel16, false>, K1UConfig<2>::kSmem)
+                   : run(input_umma_kernel<kSym16, false>, K1UConfig<2>::kSmem);
+  return run(input_umma_kernel<kSym8, false>, K1UConfig<1>::kSmem);
 }
 
 }  // namespace rnsw

@@ -99,3 +99,16 @@ def test_mma_sync_input_transform_still_matches():
                         os.path.join(here, "test_gpu_k1u.py"), "-k", "input_transform_matches"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.skipif(os.environ.get("RNSW_K1_PAIR") is not None, reason="already the alternate path")
+def test_cta_pair_input_transform_still_matches():
+    """RNSW_K1_PAIR=1 runs K1 as 2-CTA clusters (cta_group::2 MMAs of M = 256,
+    the patch split by channels between the pair) where a residue has two
+    128-position blocks: rerun the stage and whole-layer checks on it."""
+    env = dict(os.environ, RNSW_K1_PAIR="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_k1u.py"), "-k", "not still"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
