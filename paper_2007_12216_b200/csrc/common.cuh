@@ -360,6 +360,33 @@ RNSW_DEV void mma_i8_ts_warp_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_de
       "}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// 3-D tensor load into this CTA's shared memory, bytes completing on the
+// pair leader's mbarrier
+RNSW_DEV void tma_load_3d_2sm(void* dst, const void* desc, uint32_t leader_bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// both operands from shared memory, across the CTA pair, one issuing thread
+RNSW_DEV void mma_i8_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// one issuing thread: commit the pair's prior MMAs to the mbarrier at this offset in both CTAs
+RNSW_DEV void mma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
 // commit the pair's prior MMAs to the mbarrier at this offset in both CTAs
 RNSW_DEV void mma_commit_warp_2sm(uint64_t* bar) {
   asm volatile(

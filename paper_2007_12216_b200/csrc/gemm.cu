@@ -117,9 +117,11 @@ constexpr int stage_bytes(int bn, int maxpl) {
   return a_planes(maxpl) * kBlockM * BC + b_planes(maxpl) * bn * BC;
 }
 
-template <int BN, int BC, int MAXPL, bool TS = true, int SB = 1>
+template <int BN, int BC, int MAXPL, bool TS = true, int SB = 1, bool CG2 = false>
 struct GemmConfig {
-  static constexpr int kStageBytes = stage_bytes<BC>(BN, MAXPL);
+  // CG2 (CTA pair, cta_group::2): each CTA stages its two V planes and two of
+  // the four filter planes (its N half of both MMAs' B operands)
+  static constexpr int kStageBytes = CG2 ? 2 * kBlockM * BC + 2 * BN * BC : stage_bytes<BC>(BN, MAXPL);
   // BN <= 128: the epilogue stages each output tile in shared memory (int16,
   // 128B-swizzled boxes of 64 columns) and writes it with TMA bulk tensor
   // stores; per-thread 16-byte stores of 128 scattered rows were the GEMM's
@@ -213,16 +215,23 @@ RNSW_DEV void store16(int16_t* dst, const int32_t (&r)[16]) {
   d[1] = *reinterpret_cast<const int4*>(&o[8]);
 }
 
-RNSW_DEV void release_acc(uint64_t* bar, int lane) {
+// remote != 0: the barrier lives in the CTA pair's leader (its shared::cluster address)
+RNSW_DEV void release_acc(uint64_t* bar, int lane, uint32_t remote = 0) {
   tc_fence_before();
   __syncwarp();
-  if (lane == 0) mbar_arrive(bar);
+  if (lane == 0) {
+    if (remote != 0)
+      mbar_arrive_remote(remote);
+    else
+      mbar_arrive(bar);
+  }
 }
 
 // 16-bit residues: two accumulators (A256, A1) per column.
 template <int BN, int ACC_COLS>
 RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, uint8_t* out8, int col0,
-                             bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
+                             bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0,
+                             uint32_t trem = 0) {
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 32 ? kHalf : 32;  // 2 x 32 registers in flight
   const FastMod fm = a.fm[res];
@@ -235,7 +244,7 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
       tmem_ld16(taddr + BN + c0 + 16 * j, lo[j]);
     }
     tmem_ld_wait();
-    if (c0 + kBatch >= kHalf) release_acc(tempty, lane);
+    if (c0 + kBatch >= kHalf) release_acc(tempty, lane, trem);
 #pragma unroll
     for (int j = 0; j < kBatch / 16; ++j) {
       int32_t r[16];
@@ -284,7 +293,8 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
 // recombination red(A65536) r65536 + red(A256) 256 + A1 stay below 2^28.
 template <int BN>
 RNSW_DEV void epilogue_u2(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, uint8_t* out8, int col0,
-                          bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
+                          bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0,
+                             uint32_t trem = 0) {
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 16 ? kHalf : 16;
   const FastMod fm = a.fm[res];
@@ -297,7 +307,7 @@ RNSW_DEV void epilogue_u2(const GemmArgs& a, int res, uint32_t taddr, int16_t* o
     tmem_ld16(taddr + BN + c0, h1);
     tmem_ld16(taddr + 2 * BN + c0, lo);
     tmem_ld_wait();
-    if (c0 + kBatch >= kHalf) release_acc(tempty, lane);
+    if (c0 + kBatch >= kHalf) release_acc(tempty, lane, trem);
     int32_t r[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -325,7 +335,8 @@ RNSW_DEV void epilogue_u2(const GemmArgs& a, int res, uint32_t taddr, int16_t* o
 // 8-bit residues: one accumulator per column.
 template <int BN>
 RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_t* out_row, uint8_t* out8, int col0,
-                              bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0) {
+                              bool row_ok, uint64_t* tempty, int lane, uint8_t* stg, int srow, int scol0,
+                             uint32_t trem = 0) {
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 64 ? kHalf : 64;
   const FastMod fm = a.fm[res];
@@ -335,7 +346,7 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
 #pragma unroll
     for (int j = 0; j < kBatch / 16; ++j) tmem_ld16(taddr + c0 + 16 * j, v[j]);
     tmem_ld_wait();
-    if (c0 + kBatch >= kHalf) release_acc(tempty, lane);
+    if (c0 + kBatch >= kHalf) release_acc(tempty, lane, trem);
 #pragma unroll
     for (int j = 0; j < kBatch / 16; ++j) {
       int32_t r[16];
@@ -375,11 +386,19 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
 // operand traffic, not by the tensor pipe: profiles/r01_gemm_*).  A stage is
 // refilled only after both CTAs' MMAs released it (empty barriers count 2,
 // MMA commits multicast to the pair).
+// MC = 3 (16-bit plans): the same tile pairs as one cta_group::2 MMA of
+// M = 256 -- each CTA stages its own V tile and only its N half of the filter
+// planes (u'_hi, u_hi on the even CTA, u'_lo, u_lo on the odd one), loads
+// complete on the even CTA's barrier, the even CTA issues, commits multicast
+// to both, and both CTAs' epilogues release the accumulators to the even CTA.
 template <int BN, int BC, int MAXPL, int MC, bool TS, int SB>
 __global__ void __launch_bounds__(kThreads, 1)
     winograd_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                          const __grid_constant__ CUtensorMap tmM, GemmArgs args) {
-  using Cfg = GemmConfig<BN, BC, MAXPL, TS, SB>;
+  constexpr bool CG2 = MC == 3;
+  constexpr int CS = MC == 1 ? 1 : 2;  // CTAs per cluster
+  static_assert(!CG2 || MAXPL == 2, "CTA-pair MMAs: 16-bit plans only");
+  using Cfg = GemmConfig<BN, BC, MAXPL, TS, SB, CG2>;
   using Tr = GemmTraits<BN, MAXPL>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -393,28 +412,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int rank = MC == 2 ? (int)cluster_ctarank() : 0;
-  // work units: (kb fastest, pb group of MC tiles, pos, res); this CTA takes
-  // pb = MC * unit_pb + rank of every unit of its cluster
-  const int64_t u_begin = blockIdx.x / MC, u_step = gridDim.x / MC;
+  const int rank = CS == 2 ? (int)cluster_ctarank() : 0;
+  // work units: (kb fastest, pb group of CS tiles, pos, res); this CTA takes
+  // pb = CS * unit_pb + rank of every unit of its cluster
+  const int64_t u_begin = blockIdx.x / CS, u_step = gridDim.x / CS;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmU);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], MC);
+      mbar_init(&empty[i], MC == 2 ? 2 : 1);  // CG2: the leader's multicast commit
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
+      mbar_init(&tempty[i], CG2 ? 16 : 8);  // CG2: both CTAs' epilogue warps
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<Tr::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if (CG2)
+      tmem_alloc_2sm<Tr::kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<Tr::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  if (MC == 2)
-    cluster_sync();  // the peer multicasts into this CTA's stages and barriers
+  if (CS == 2)
+    cluster_sync();  // the peer multicasts / completes into this CTA's stages and barriers
   else
     __syncthreads();
   tc_fence_after();
@@ -427,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
      // so slots 0-1 and 2-3 are each one 2*BN-row K-major operand; 8-bit: [0] u
   // MAXPL 3: [0] u_hi, [1] u_lo (bank planes 1, 0)
   auto bslot = [&](int b, int pl) { return (MAXPL == 2 && pl == 2) ? 3 - b : (MAXPL == 3 ? 1 - b : b); };
+  const uint32_t lead_bar0 = CG2 ? mapa_shared(smem_u32(&full[0]), 0) : 0u;  // the leader's full[0]
 
   if (warp == 0) {
     // ---------------- TMA producer (whole warp) ----------------
@@ -440,12 +465,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     for (int64_t t = u_begin; t < args.total_tiles; t += u_step) {
       const TileCoord tc = tile_coord((uint32_t)t, args);
-      const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
+      const int kb = tc.kb, pb = CS * tc.pb + rank, pos = tc.pos, res = tc.res;
       const int pl = args.planes[res];
       const int upl = MAXPL == 3 ? 2 : (pl == 2 ? 4 : 1);
-      const int nb = MC == 2 ? 2 : upl;        // filter planes this CTA loads
-      const int b0 = MC == 2 ? 2 * rank : 0;   // first of them
-      const uint32_t bytes = (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
+      const int nb = MC == 2 ? 2 : (CG2 ? 2 : upl);  // filter planes this CTA loads
+      const int b0 = MC == 2 ? 2 * rank : 0;          // first of them (MC = 2)
+      // CG2: the leader's barrier counts both CTAs' A planes and filter halves
+      const uint32_t bytes = CG2 ? (uint32_t)(2 * (pl * Cfg::kAPlaneBytes + 2 * Cfg::kBPlaneBytes))
+                                 : (uint32_t)(pl * Cfg::kAPlaneBytes + upl * Cfg::kBPlaneBytes);
       for (int kc = 0; kc < args.nkc; ++kc) {
         mbar_wait(&empty[stage], phase ^ 1);
 #ifdef RNSW_GEMM_NOLOAD  // diagnostic: after two rounds of the ring, stages are reused without loads
@@ -459,9 +486,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
 #endif
-        if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+        if (lane == 0 && (!CG2 || rank == 0)) mbar_arrive_expect_tx(&full[stage], bytes);
         __syncwarp();
-        if (lane < pl) {
+        if (CG2) {
+          // bank planes 0 u_lo, 1 u_hi, 2 u'_lo, 3 u'_hi; slot 0 = this CTA's N half
+          // of [u'_hi ; u'_lo] (MMA 1), slot 1 = its half of [u_hi ; u_lo] (MMA 2)
+          const uint32_t lb = lead_bar0 + (uint32_t)stage * 8u;
+          if (lane < 2) {
+            tma_load_3d_2sm(stage_a(stage, lane), &tmV, lb, kc * BC, pb * kBlockM,
+                            (args.plane_base[res] + lane) * args.npos + pos);
+          } else if (lane < 4) {
+            const int slot = lane - 2, b = (slot == 0 ? 3 : 1) - rank;
+            tma_load_3d_2sm(stage_b(stage, slot), &tmU, lb, kc * BC, kb * BN,
+                            (args.uplane_base[res] + b) * args.npos + pos);
+          }
+        } else if (lane < pl) {
           tma_load_3d(stage_a(stage, lane), &tmV, &full[stage], kc * BC, pb * kBlockM,
                       (args.plane_base[res] + lane) * args.npos + pos);
         } else if (lane < pl + nb) {
@@ -480,10 +519,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && (!CG2 || rank == 0)) {
       // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc = idesc_i8(kBlockM, BN);
-      constexpr uint32_t idesc2 = idesc_i8(kBlockM, 2 * BN);  // 16-bit: [A256 | A1] in one MMA
+      constexpr uint32_t idesc2 = idesc_i8(CG2 ? 2 * kBlockM : kBlockM, 2 * BN);  // 16-bit: [A256 | A1] in one MMA
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -523,7 +562,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = smem_u32(stage_b(stage, 0));
           // one branch per stage, then a branch-free unrolled MMA sequence
           // (a runtime test between consecutive MMAs costs tensor throughput)
-          if (MAXPL == 1 || pl == 1) {
+          if (CG2) {
+#pragma unroll
+            for (int k = 0; k < BC / 32; ++k) {
+              // M = 256 over the pair; B = the two CTAs' N halves at the same offsets
+              const uint32_t acc = (kc | k) != 0;
+              const uint64_t da_lo = umma_desc_kmajor(a0 + 32 * k, BC);
+              const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
+              const uint64_t db_p = umma_desc_kmajor(b0 + 32 * k, BC);                      // u'_hi | u'_lo half
+              const uint64_t db_u = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);  // u_hi | u_lo half
+              mma_i8_2sm(d0, da_hi, db_p, idesc2, acc);
+              mma_i8_2sm(d0, da_lo, db_u, idesc2, 1u);
+            }
+          } else if (MAXPL == 1 || pl == 1) {
 #pragma unroll
             for (int k = 0; k < BC / 32; ++k)
               mma_i8(d0, umma_desc_kmajor(a0 + 32 * k, BC), umma_desc_kmajor(b0 + 32 * k, BC), idesc,
@@ -556,7 +607,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_i8(d0, da_lo, db_u, idesc2, 1u);
             }
           }
-          if (MC == 2)
+          if (CG2)
+            mma_commit_2sm(&empty[stage]);
+          else if (MC == 2)
             mma_commit_mc(&empty[stage], (uint16_t)0x3);
           else
             mma_commit(&empty[stage]);
@@ -571,7 +624,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef RNSW_GEMM_PROF
         long long g4 = clock64();
 #endif
-        mma_commit(&tfull[as]);
+        if (CG2)
+          mma_commit_2sm(&tfull[as]);
+        else
+          mma_commit(&tfull[as]);
 #ifdef RNSW_GEMM_PROF
         g_cm += clock64() - g4;
 #endif
@@ -593,14 +649,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     int it = 0;
     for (int64_t t = u_begin; t < args.total_tiles; t += u_step, ++it) {
       const TileCoord tc = tile_coord((uint32_t)t, args);
-      const int kb = tc.kb, pb = MC * tc.pb + rank, pos = tc.pos, res = tc.res;
+      const int kb = tc.kb, pb = CS * tc.pb + rank, pos = tc.pos, res = tc.res;
       const int pl = args.planes[res];
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
+      // CG2: the accumulators are released to the leader CTA's barrier
+      const uint32_t rel_remote = CG2 ? mapa_shared(smem_u32(&tempty[as]), 0) : 0u;
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
 #ifdef RNSW_GEMM_NOEPI  // diagnostic: hand the accumulator straight back (no reads, no stores)
-      release_acc(&tempty[as], lane);
+      release_acc(&tempty[as], lane, CG2 ? rel_remote : 0u);
       continue;
 #endif
       const int64_t p = (int64_t)pb * kBlockM + q * 32 + lane;
@@ -625,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!quad_live) {
         // every row of this warp's lane quadrant is past the last tile (small
         // or ragged P): nothing to reduce, just free the accumulator
-        release_acc(&tempty[as], lane);
+        release_acc(&tempty[as], lane, CG2 ? rel_remote : 0u);
       } else if (MAXPL == 3) {
         uint8_t* out8 = reinterpret_cast<uint8_t*>(args.Mw) +
                         mw8_offset(p, res, 0, pos, args.n_res, args.npos, args.Kp);
@@ -635,7 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* out8 = reinterpret_cast<uint8_t*>(args.Mw) +
                         mw8_offset(p, res, 0, pos, args.n_res, args.npos, args.Kp);
         epilogue_limbs<BN, Tr::kAccCols>(args, res, taddr, out_row, out8, col0, row_ok, &tempty[as], lane, stg_t,
-                                         q * 32 + lane, half * kHalf);
+                                         q * 32 + lane, half * kHalf, CG2 ? rel_remote : 0u);
       } else {
         uint8_t* out8 = reinterpret_cast<uint8_t*>(args.Mw) + mw8s_offset(p, res, pos, args.n_res, args.npos, args.Kp);
         epilogue_single<BN>(args, res, taddr, out_row, out8, col0, row_ok, &tempty[as], lane, stg_t, q * 32 + lane,
@@ -663,10 +721,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG2)
+    cluster_sync();  // the pair's MMAs and both CTAs' TMEM reads are done
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<Tr::kTmemCols>(tmem_base);
+    if (CG2)
+      tmem_dealloc_2sm<Tr::kTmemCols>(tmem_base);
+    else
+      tmem_dealloc<Tr::kTmemCols>(tmem_base);
   }
   if (MC == 2) cluster_sync();  // no CTA leaves while its peer may still signal it
 }
@@ -749,7 +813,8 @@ namespace {
 template <int BN, int BC, int MAXPL, int MC, bool TS, int SB>
 cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_planes, int n_uplanes,
                      cudaStream_t s) {
-  using Cfg = GemmConfig<BN, BC, MAXPL, TS, SB>;
+  using Cfg = GemmConfig<BN, BC, MAXPL, TS, SB, MC == 3>;
+  constexpr int CS = MC == 1 ? 1 : 2;  // CTAs per cluster
   CUtensorMap tmV, tmU;
   if (!make_tmap(&tmV, V, a.Cp, a.P, (int64_t)n_planes * a.npos, BC, kBlockM)) return cudaErrorInvalidValue;
   if (!make_tmap(&tmU, U, a.Cp, a.K, (int64_t)n_uplanes * a.npos, BC, BN)) return cudaErrorInvalidValue;
@@ -766,9 +831,9 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmemBytes);
   if (e != cudaSuccess) return e;
   const int num_sms = num_sms_current();
-  int64_t grid = a.total_tiles * MC < num_sms ? a.total_tiles * MC : num_sms;
-  grid = grid / MC * MC;
-  if (grid < MC) grid = MC;
+  int64_t grid = a.total_tiles * CS < num_sms ? a.total_tiles * CS : num_sms;
+  grid = grid / CS * CS;
+  if (grid < CS) grid = CS;
   if (MC == 1) {
     kern<<<(unsigned)grid, kThreads, Cfg::kSmemBytes, s>>>(tmV, tmU, tmM, a);
     return cudaGetLastError();
@@ -780,7 +845,7 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = MC;
+  attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -869,6 +934,12 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   bool all16 = true;
   for (int r = 0; r < d.n_res; ++r) all16 = all16 && d.res[r].planes == 2;
   static const bool no_mc = getenv("RNSW_GEMM_NO_MC") != nullptr;  // A/B switch
+  // CTA pairs as cta_group::2 MMAs of M = 256 (each CTA stages half of the
+  // filter planes) for C >= 256, where the operand stream bounds the GEMM
+  // (VGG16 conv4_2: -15%, conv3_2: -5%); multicast pairs for smaller C
+  // (+3% on conv2_x).  RNSW_GEMM_CG2=0/1 forces either.
+  static const char* cg2_env = getenv("RNSW_GEMM_CG2");
+  const bool cg2 = cg2_env != nullptr ? atoi(cg2_env) != 0 : Cp >= 256;
   // RNSW_GEMM_U2=1: the two-plane-bank variant (MAXPL 3) for every 16-bit
   // layer, =2: where the bank stream dominates (4 K C >= 2 P C + 4 P K).  Off
   // by default: on B200 it measured slower even at batch 1 (0.83 vs 0.63 ms
@@ -888,13 +959,17 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
       return run_gemm_bc<64, 3>(a, bc, V, U, np, nup, s);
     }
   }
-  if (maxpl == 2 && all16 && a.num_pb >= 4 && !no_mc) {
+  if (maxpl == 2 && all16 && (a.num_pb >= 4 || (cg2 && a.num_pb >= 2)) && !no_mc) {
     // CTA pairs over (pb, pb+1) with the filter planes multicast (see the kernel);
     // with only 2-3 tile blocks the pair's lockstep costs more than the shared
     // filter bytes save (VGG16 conv5 at batch 256: -10% without pairs)
     const int num_pbu = (a.num_pb + 1) / 2;
     a.total_tiles = (int64_t)d.n_res * a.npos * num_pbu * a.num_kb;
     a.div_pb = make_fastdiv((uint32_t)num_pbu);
+    if (cg2) {
+      if (bn == 64) return run_gemm_bc<64, 2, 3>(a, bc, V, U, np, nup, s);
+      return run_gemm_bc<128, 2, 3>(a, bc, V, U, np, nup, s);
+    }
     if (bn == 64) return run_gemm_bc<64, 2, 2>(a, bc, V, U, np, nup, s);
     return run_gemm_bc<128, 2, 2>(a, bc, V, U, np, nup, s);
   }

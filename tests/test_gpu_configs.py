@@ -191,3 +191,22 @@ def test_alternate_kernel_paths_in_subprocess():
                         "-k", "vgg16_batch1 or fused_glue or fused_requant or config5_sweep"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.skipif(__import__("os").environ.get("RNSW_GEMM_CG2") is not None, reason="already forced")
+@pytest.mark.parametrize("cg2", ["0", "1"])
+def test_gemm_pair_modes_in_subprocess(cg2):
+    """RNSW_GEMM_CG2=1 runs every paired 16-bit GEMM as cta_group::2 MMAs of
+    M = 256 (default only for C >= 256), =0 every pair as a multicast pair:
+    rerun the VGG16 batch checks and the fused-epilogue sweep on each."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, RNSW_GEMM_CG2=cg2)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_configs.py"),
+                        "-k", "vgg16_batch or fused_glue or fused_requant"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
