@@ -60,6 +60,9 @@
 #ifndef RNSW_K1_STASYNC
 #define RNSW_K1_STASYNC 0
 #endif
+#ifndef RNSW_K1_DEFER
+#define RNSW_K1_DEFER 1
+#endif
 // 1: the accumulator bias is added in the epilogue (one IADD per value)
 // instead of by two bias MMAs per unit (11% of the unit's tensor work) --
 // measured 7% slower on conv1_2 than the bias MMAs, so off
@@ -475,6 +478,20 @@ __global__ void __launch_bounds__(kUThreads, 1)
     };
     const bool two = args.cblocks == 1;
     int it = 0, jt = -1;
+    // deferred staging hand-off (RNSW_K1_DEFER): a unit's fence.proxy.async +
+    // sfull arrive happen after the next unit's TMEM loads and conversion, so
+    // the warp does not stall on its own st.shared completing
+    int pend_sb = -1, pend_extra = 0;
+    auto hand_off = [&]() {
+      if (pend_sb < 0) return;
+      fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sfull[pend_sb]);
+        if (pend_extra) mbar_arrive(&sfull[pend_sb]);  // a lone last unit
+      }
+      pend_sb = -1;
+    };
 #ifdef RNSW_K1_PROF
     long long e_tf = 0, e_se = 0, e_0 = clock64();
 #endif
@@ -527,6 +544,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
       }
       // the pair's staging buffer must be free: its previous bulk store has read it
       const int sb = jt & 1;
+      if (RNSW_K1_DEFER) hand_off();  // the previous unit's staging, now surely written
 #ifdef RNSW_K1_PROF
       long long e2 = clock64();
 #endif
@@ -575,15 +593,13 @@ __global__ void __launch_bounds__(kUThreads, 1)
         }
       }
       if (!RNSW_K1_STASYNC) {
-        fence_proxy_async();  // staging writes -> visible to the bulk-copy engine
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&sfull[sb]);
-          if (h_ == 0 && u + 1 >= args.units) mbar_arrive(&sfull[sb]);  // a lone last unit
-        }
+        pend_sb = sb;
+        pend_extra = (h_ == 0 && u + 1 >= args.units) ? 1 : 0;
+        if (!RNSW_K1_DEFER) hand_off();
       }
       ++it;
     }
+    hand_off();  // the last unit's
 #ifdef RNSW_K1_PROF
     if (lane == 0 && blockIdx.x < 4 && (warp == 4 || warp == 11))
       printf("K1PROF cta %d epi warp %d units %d total %lld wait_tfull %lld wait_sempty %lld (per unit %lld %lld %lld)\n",
