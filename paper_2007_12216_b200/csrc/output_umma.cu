@@ -38,6 +38,18 @@
 namespace rnsw {
 namespace {
 
+// Waits for the MMA batches: with RNSW_K4_SLEEP=ns the waiting warps suspend
+// in mbarrier.try_wait (woken when the phase completes) instead of spinning,
+// leaving issue slots to the co-resident CTA
+#ifndef RNSW_K4_SLEEP
+#define RNSW_K4_SLEEP 0
+#endif
+#if RNSW_K4_SLEEP
+#define K4_WAIT(b, ph) mbar_wait_sleep(b, ph, RNSW_K4_SLEEP)
+#else
+#define K4_WAIT(b, ph) mbar_wait(b, ph)
+#endif
+
 constexpr int kKB = 32;     // output channels per work unit
 constexpr int kThr = 256;   // 8 warps: TMEM lane quadrant q = warp & 3, half h = warp >> 2
 constexpr int kOpBytes = 4096;  // one MMA A operand: 32 K rows x 128 bytes
@@ -164,7 +176,7 @@ __global__ void __launch_bounds__(kThr, 2)
 #endif
     const int p = unit_p(u), k0 = (int)(u - (int64_t)p * args.kblocks) * kKB;
     // ---- pass 1 (issued before the previous unit's stores) ----
-    mbar_wait(my_bar, ph_mma);
+    K4_WAIT(my_bar, ph_mma);
     K4T(0)
     ph_mma ^= 1;
     tc_fence_after();
@@ -253,7 +265,7 @@ __global__ void __launch_bounds__(kThr, 2)
       mma_commit_warp(&bar[2]);
     }
     K4T(3)
-    mbar_wait(my_bar, ph_mma);
+    K4_WAIT(my_bar, ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
     K4T(4)
