@@ -919,7 +919,14 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   int bn;
   if (maxpl == 2) bn = Kp <= 64 ? 64 : 128;
   else bn = Kp <= 64 ? 64 : ((Kp <= 128 || planar) ? 128 : 256);
-  if (maxpl == 2 && bc > 64) {
+  // CTA-pair (cta_group::2) GEMMs with C >= 512 keep 128-byte channel chunks
+  // (3 stages of 64 KB: conv4_2 -6%, conv5 -2%); C = 256 is faster with
+  // 64-byte chunks (6 stages; +10% with 128)
+  static const char* cg2_env0 = getenv("RNSW_GEMM_CG2");
+  const bool cg2_planned = (cg2_env0 != nullptr ? atoi(cg2_env0) != 0 : Cp >= 256) && (P + kBlockM - 1) / kBlockM >= 2 &&
+                           getenv("RNSW_GEMM_NO_MC") == nullptr;
+  const bool cg2_bc128 = cg2_planned && Cp >= 512 && Cp % 128 == 0;
+  if (maxpl == 2 && bc > 64 && !cg2_bc128) {
     bc = 64;
     a.nkc = Cp / bc;
   }
