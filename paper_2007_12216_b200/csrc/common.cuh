@@ -489,6 +489,13 @@ RNSW_DEV void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+// 32 lanes x 32 bit, 8 consecutive columns per thread.
+RNSW_DEV void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
 RNSW_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // 32 lanes x 32 bit: the same value into 16 consecutive columns of this

@@ -41,6 +41,9 @@ namespace {
 // Waits for the MMA batches: with RNSW_K4_SLEEP=ns the waiting warps suspend
 // in mbarrier.try_wait (woken when the phase completes) instead of spinning,
 // leaving issue slots to the co-resident CTA
+#ifndef RNSW_K4_EPI2_PIPE
+#define RNSW_K4_EPI2_PIPE 1
+#endif
 #ifndef RNSW_K4_SLEEP
 #define RNSW_K4_SLEEP 0
 #endif
@@ -331,6 +334,76 @@ __global__ void __launch_bounds__(kThr, 2)
         }
       }
       };
+#if RNSW_K4_EPI2_PIPE
+      // software-pipelined by half blocks: columns 8 hf .. 8 hf + 7 of one
+      // channel block are reduced while the next half's TMEM loads fly (two
+      // 32-register sets, the same peak as one 16-column block)
+      auto emit = [&](int mbi, int hf, const int32_t (&H0)[8], const int32_t (&L0)[8], const int32_t (&H1)[8],
+                      const int32_t (&L1)[8]) {
+        const int mb = 2 * h + mbi, kl = mb * 8 + kk8;
+        constexpr int kNb = 8;
+        int32_t qv[kNb];
+#pragma unroll
+        for (int e = 0; e < kNb; ++e) {
+          const int32_t n0 = H0[e] * 256 + L0[e];
+          const int32_t d0 = (int32_t)(__umulhi((uint32_t)n0, mul0) * fm0.negm + (uint32_t)n0);
+          const int32_t d1 = red_pos_biased(d0 * negw10 + (H1[e] * 256 + L1[e]), fm1);
+          const uint32_t x = (uint32_t)d0 + m0 * (uint32_t)d1;
+          const bool neg = x > signed_bound;
+          if constexpr (kMode == 0)
+            qv[e] = (int32_t)((int32_t)x > (int32_t)signed_bound ? x - dyn_range : x);
+          else if constexpr (kMode == 1)
+            qv[e] = neg ? 0 : min((int32_t)(x >> args.shift), 127);
+          else
+            qv[e] = neg ? 0 : (int32_t)x;
+        }
+        const int nb = hf == 0 ? 8 : 6;  // columns b = 8 hf + e < 14
+        if constexpr (kMode == 3) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            if (2 * c >= nb) break;
+            int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
+            m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
+            m2 = min(m2 >> args.shift, 127);
+            if ((a & 1) == 0 && a < 14) smem[kOffOut + ((a >> 1) * 7 + 4 * hf + c) * kPixB + kl] = (uint8_t)m2;
+          }
+        } else if constexpr (kMode == 1) {
+          if (a < 14) {
+#pragma unroll
+            for (int e = 0; e < kNb; ++e)
+              if (e < nb) smem[kOffOut + (a * 14 + 8 * hf + e) * kPixB + kl] = (uint8_t)qv[e];
+          }
+        } else {
+          int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
+          if (a < 14) {
+#pragma unroll
+            for (int e = 0; e < kNb; ++e)
+              if (e < nb) ys[(a * 14 + 8 * hf + e) * kPixW + kl] = qv[e];
+          }
+        }
+      };
+      auto load = [&](int mbi, int hf, int32_t (&H0)[8], int32_t (&L0)[8], int32_t (&H1)[8], int32_t (&L1)[8]) {
+        const uint32_t ta = tbase + ((uint32_t)(32 * q) << 16) + (2 * h + mbi) * 32 + 8 * hf;
+        tmem_ld8(ta, H0);
+        tmem_ld8(ta + 16, L0);
+        tmem_ld8(ta + 128, H1);
+        tmem_ld8(ta + 144, L1);
+      };
+      int32_t aH0[8], aL0[8], aH1[8], aL1[8], bH0[8], bL0[8], bH1[8], bL1[8];
+      load(0, 0, aH0, aL0, aH1, aL1);
+      tmem_ld_wait();
+      load(0, 1, bH0, bL0, bH1, bL1);
+      emit(0, 0, aH0, aL0, aH1, aL1);
+      tmem_ld_wait();
+      load(1, 0, aH0, aL0, aH1, aL1);
+      emit(0, 1, bH0, bL0, bH1, bL1);
+      tmem_ld_wait();
+      load(1, 1, bH0, bL0, bH1, bL1);
+      emit(1, 0, aH0, aL0, aH1, aL1);
+      tmem_ld_wait();
+      emit(1, 1, bH0, bL0, bH1, bL1);
+      (void)epi2_block;
+#else
       if constexpr (kMode == 1) {
         epi2_block(0);
         epi2_block(1);
@@ -338,6 +411,7 @@ __global__ void __launch_bounds__(kThr, 2)
 #pragma unroll 1
         for (int mbi = 0; mbi < 2; ++mbi) epi2_block(mbi);
       }
+#endif
     }
     K4T(5)
     tc_fence_before();
