@@ -33,6 +33,12 @@
 #include "common.cuh"
 #include "kernels.h"
 
+// 1: the whole-layer 16-bit epilogue is software-pipelined by 16-column chunks
+#ifndef RNSW_GEMM_EPI_PIPE
+#define RNSW_GEMM_EPI_PIPE 1
+#endif
+
+
 namespace rnsw {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -235,6 +241,33 @@ RNSW_DEV void epilogue_limbs(const GemmArgs& a, int res, uint32_t taddr, int16_t
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 32 ? kHalf : 32;  // 2 x 32 registers in flight
   const FastMod fm = a.fm[res];
+  if (RNSW_GEMM_EPI_PIPE && a.fast2 && a.pos_out && a.planar && stg != nullptr && kHalf % 16 == 0) {
+    // the whole-layer (VGG16) path, software-pipelined by 16-column chunks:
+    // the next chunk's TMEM loads fly while this one is reduced and staged
+    constexpr int kN = kHalf / 16;
+    const int32_t pb = pos_bias(fm);
+    int32_t buf[2][2][16];
+    tmem_ld16(taddr, buf[0][0]);
+    tmem_ld16(taddr + BN, buf[0][1]);
+    tmem_ld_wait();
+    if (kN == 1) release_acc(tempty, lane, trem);
+#pragma unroll
+    for (int j = 0; j < kN; ++j) {
+      if (j + 1 < kN) {
+        tmem_ld16(taddr + 16 * (j + 1), buf[(j + 1) & 1][0]);
+        tmem_ld16(taddr + BN + 16 * (j + 1), buf[(j + 1) & 1][1]);
+      }
+      int32_t r[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) r[e] = red_pos_biased(buf[j & 1][0][e] * 256 + buf[j & 1][1][e] + pb, fm);
+      sts8x2_swz<BN>(stg, srow, scol0 + 16 * j, r);
+      if (j + 1 < kN) {
+        tmem_ld_wait();
+        if (j + 2 == kN) release_acc(tempty, lane, trem);  // every column of this thread is in registers
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (int c0 = 0; c0 < kHalf; c0 += kBatch) {
     int32_t hi[kBatch / 16][16], lo[kBatch / 16][16];
