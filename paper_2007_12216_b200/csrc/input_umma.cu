@@ -63,6 +63,9 @@
 #ifndef RNSW_K1_DEFER
 #define RNSW_K1_DEFER 1
 #endif
+#ifndef RNSW_K1_EPI_PIPE
+#define RNSW_K1_EPI_PIPE 0
+#endif
 // 1: the accumulator bias is added in the epilogue (one IADD per value)
 // instead of by two bias MMAs per unit (11% of the unit's tensor work) --
 // measured 7% slower on conv1_2 than the bias MMAs, so off
@@ -514,17 +517,26 @@ __global__ void __launch_bounds__(kUThreads, 1)
       for (int e = 0; e < 16; ++e) a0[e] = b0[e] = a1[e] = b1[e] = e + it;
       if (false)
 #endif
+      // (RNSW_K1_EPI_PIPE: the second 16-channel chunk's loads fly while the
+      // first chunk is converted; the buffer is released after the second wait)
+      constexpr bool kPipe = RNSW_K1_EPI_PIPE && kEpiCols == 32 && !RNSW_K1_NO_TMEM_LD &&
+                             RNSW_K1_DIAG != 2 && RNSW_K1_DIAG != 6;
       if (kLimbs == 2) {
         tmem_ld16(taddr, a0);
         tmem_ld16(taddr + kUnitN, b0);
         if (kEpiCols == 32) {
+          if (kPipe) tmem_ld_wait();
           tmem_ld16(taddr + 16, a1);
           tmem_ld16(taddr + kUnitN + 16, b1);
         }
       } else {
         tmem_ld16(taddr, b0);
-        if (kEpiCols == 32) tmem_ld16(taddr + 16, b1);
+        if (kEpiCols == 32) {
+          if (kPipe) tmem_ld_wait();
+          tmem_ld16(taddr + 16, b1);
+        }
       }
+      if (kPipe) convert(a0, b0, lo, hi);
       tmem_ld_wait();
       // hand the buffer back to the MMA warp (kPair: the leader CTA's barrier)
       tc_fence_before();
@@ -536,7 +548,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
           mbar_arrive(&tempty[as]);
       }
       if (RNSW_K1_DIAG != 2 && RNSW_K1_DIAG != 6) {
-        convert(a0, b0, lo, hi);
+        if (!kPipe) convert(a0, b0, lo, hi);
         if (kEpiCols == 32) convert(a1, b1, lo + 4, hi + 4);
       } else {
 #pragma unroll
