@@ -14,6 +14,13 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef RNSW_SMALLC_MINB
+#define RNSW_SMALLC_MINB 4  // C = 3 planar: 64 registers, 4 CTAs (32 warps) per SM to cover the V16 load latency (-7% vs 77 registers, 3 CTAs)
+#endif
+#ifndef RNSW_SMALLC_AHEAD
+#define RNSW_SMALLC_AHEAD 8
+#endif
+
 namespace rnsw {
 namespace {
 
@@ -24,7 +31,7 @@ namespace {
 // transform reads (kernels.h mw8_offset).
 // kC3: C == 3 (VGG16 conv1_1), the zero fourth channel is skipped.
 template <int kPL, bool kPlanar = false, bool kC3 = false>
-__global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* __restrict__ plan, int P, int K,
+__global__ void __launch_bounds__(256, kC3 ? RNSW_SMALLC_MINB : 2) smallc_product_kernel(const PlanDevice* __restrict__ plan, int P, int K,
                                                              int Kp, int Cp, const int16_t* __restrict__ V16,
                                                              const int8_t* __restrict__ U, int16_t* __restrict__ Mw,
                                                              int tiles_per_cta) {
@@ -62,7 +69,7 @@ __global__ void __launch_bounds__(256) smallc_product_kernel(const PlanDevice* _
   const uint2* src = reinterpret_cast<const uint2*>(V16) + ((int64_t)r * P + p_begin) * npos + pos;
   const int rp = r * npos + pos, nrp = nres * npos;
   // V16 rows of 8 tiles are loaded together ahead of their products
-  constexpr int kAhead = 8;
+  constexpr int kAhead = RNSW_SMALLC_AHEAD;
   uint8_t* out8 = nullptr;  // Mw8 row of the current tile (advances by Kp within a block of 128 tiles)
   for (int p0 = p_begin; p0 < p_end; p0 += kAhead) {
     uint2 wv[kAhead];
