@@ -63,6 +63,12 @@
 #ifndef RNSW_K1_DEFER
 #define RNSW_K1_DEFER 1
 #endif
+#ifndef RNSW_K1_STAGES
+#define RNSW_K1_STAGES 8
+#endif
+#ifndef RNSW_K1_NSTG
+#define RNSW_K1_NSTG 2
+#endif
 #ifndef RNSW_K1_EPI_PIPE
 #define RNSW_K1_EPI_PIPE 0
 #endif
@@ -129,7 +135,8 @@ enum K1UMode { kSym8 = 0, kSym16 = 1, kRel16 = 2 };
 template <int kLimbs>
 struct K1UConfig {
   static constexpr int kStageBytes = 256 * kUnitN;  // K <= 256 pixel rows x 64 channel bytes
-  static constexpr int kStages = 8;
+  static constexpr int kStages = RNSW_K1_STAGES;
+  static constexpr int kNStg = RNSW_K1_NSTG;  // staging buffers (unit pairs in flight to the bulk stores)
   // staging per unit PAIR (two tiles x 64 channels, or one tile x 128): the
   // bulk stores then write 128-byte rows instead of 64-byte ones
   static constexpr int kStgBytes = kLimbs * kGroupRows * 2 * kUnitN;
@@ -140,7 +147,7 @@ struct K1UConfig {
   static constexpr int kTmemCols = kLimbs == 2 ? 512 : 256;
   static_assert(kBiasCol + 8 <= kTmemCols, "TMEM");
   static constexpr size_t kSmem =
-      1024 + (size_t)kStages * kStageBytes + 2 * (size_t)kStgBytes + kBiasBytes + 256;
+      1024 + (size_t)kStages * kStageBytes + kNStg * (size_t)kStgBytes + kBiasBytes + 256;
 };
 
 // kPair: a 2-CTA cluster serves both 128-position blocks of a residue (N*N >
@@ -160,14 +167,14 @@ __global__ void __launch_bounds__(kUThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sB = smem;                          // [S][256 rows][64 bytes]
   uint8_t* stg = sB + S * Cfg::kStageBytes;    // [2][plane][128 rows][64 bytes]
-  uint8_t* sBias = stg + 2 * Cfg::kStgBytes;   // [B_hi | B_lo] 32 rows x 64 bytes each
+  uint8_t* sBias = stg + Cfg::kNStg * Cfg::kStgBytes;   // [B_hi | B_lo] 32 rows x 64 bytes each
   uint64_t* full = reinterpret_cast<uint64_t*>(sBias + Cfg::kBiasBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;   // staging buffer written by the 8 epilogue warps
-  uint64_t* sempty = sfull + 2;   // staging buffer read by its bulk store
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
+  uint64_t* sempty = sfull + Cfg::kNStg;   // staging buffer read by its bulk store
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + Cfg::kNStg);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = kPair ? cluster_ctarank() : 0u;
@@ -206,6 +213,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kPair ? 2 * kEpiWarps : kEpiWarps);  // kPair: both CTAs' epilogue warps
+    }
+    for (int i = 0; i < Cfg::kNStg; ++i) {
       mbar_init(&sfull[i], RNSW_K1_STASYNC ? 1 : 2 * kEpiWarps);  // store warp (tx bytes) / epilogue warps x 2 units
       mbar_init(&sempty[i], 1);
     }
@@ -428,7 +437,8 @@ __global__ void __launch_bounds__(kUThreads, 1)
       for (int pr = pr_begin; pr < npairs; pr += pr_step, ++jt) {
         int p, c0;
         unit_tile(2 * pr, p, c0);
-        const int sb = jt & 1;
+        const int sb = jt % Cfg::kNStg;
+        const uint32_t sph = (uint32_t)(jt / Cfg::kNStg) & 1u;
         if (RNSW_K1_STASYNC && !RNSW_K1_NO_STORE && RNSW_K1_DIAG != 12) {
           // the pair's staging bytes arrive as st.async transactions
           const uint32_t nun = 2 * pr + 1 < args.units ? 2u : 1u;
@@ -436,7 +446,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
         } else if (RNSW_K1_STASYNC) {
           mbar_arrive(&sfull[sb]);
         }
-        mbar_wait(&sfull[sb], (jt >> 1) & 1);
+        mbar_wait(&sfull[sb], sph);
         uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
         for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl)
@@ -555,12 +565,13 @@ __global__ void __launch_bounds__(kUThreads, 1)
         for (int e = 0; e < 8; ++e) lo[e] = hi[e] = (uint32_t)(a0[e] ^ b1[e]);
       }
       // the pair's staging buffer must be free: its previous bulk store has read it
-      const int sb = jt & 1;
+      const int sb = jt % Cfg::kNStg;
+      const uint32_t sph = (uint32_t)(jt / Cfg::kNStg) & 1u;
       if (RNSW_K1_DEFER) hand_off();  // the previous unit's staging, now surely written
 #ifdef RNSW_K1_PROF
       long long e2 = clock64();
 #endif
-      if (h_ == 0) mbar_wait(&sempty[sb], ((jt >> 1) & 1) ^ 1);
+      if (h_ == 0) mbar_wait(&sempty[sb], sph ^ 1u);
 #ifdef RNSW_K1_PROF
       e_se += clock64() - e2;
 #endif
