@@ -373,6 +373,38 @@ RNSW_DEV void epilogue_single(const GemmArgs& a, int res, uint32_t taddr, int16_
   constexpr int kHalf = BN / 2;
   constexpr int kBatch = kHalf < 64 ? kHalf : 64;
   const FastMod fm = a.fm[res];
+  if (RNSW_GEMM_EPI_PIPE && a.fast && a.planar && stg != nullptr && kHalf % 32 == 0) {
+    // 8-bit whole-layer path, software-pipelined by 32-column chunks (two
+    // x16 loads in flight while the previous 32 columns are reduced)
+    constexpr int kN = kHalf / 32;
+    int32_t buf[2][2][16];
+    tmem_ld16(taddr, buf[0][0]);
+    tmem_ld16(taddr + 16, buf[0][1]);
+    tmem_ld_wait();
+    if (kN == 1) release_acc(tempty, lane, trem);
+#pragma unroll
+    for (int j = 0; j < kN; ++j) {
+      if (j + 1 < kN) {
+        tmem_ld16(taddr + 32 * (j + 1), buf[(j + 1) & 1][0]);
+        tmem_ld16(taddr + 32 * (j + 1) + 16, buf[(j + 1) & 1][1]);
+      }
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        int32_t r[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          r[e] = red_fast(buf[j & 1][hf][e], fm);
+          r[e] += r[e] < 0 ? fm.m : 0;  // one byte plane of y mod m in [0, m)
+        }
+        sts8_swz<BN>(stg, srow, scol0 + 32 * j + 16 * hf, r);
+      }
+      if (j + 1 < kN) {
+        tmem_ld_wait();
+        if (j + 2 == kN) release_acc(tempty, lane, trem);
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (int c0 = 0; c0 < kHalf; c0 += kBatch) {
     int32_t v[kBatch / 16][16];

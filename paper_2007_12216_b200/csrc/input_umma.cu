@@ -66,6 +66,9 @@
 #ifndef RNSW_K1_STAGES
 #define RNSW_K1_STAGES 8
 #endif
+#ifndef RNSW_K1_STAGES8
+#define RNSW_K1_STAGES8 4
+#endif
 #ifndef RNSW_K1_NSTG
 #define RNSW_K1_NSTG 2
 #endif
@@ -135,7 +138,9 @@ enum K1UMode { kSym8 = 0, kSym16 = 1, kRel16 = 2 };
 template <int kLimbs>
 struct K1UConfig {
   static constexpr int kStageBytes = 256 * kUnitN;  // K <= 256 pixel rows x 64 channel bytes
-  static constexpr int kStages = RNSW_K1_STAGES;
+  // 8-bit plans: 4 stages, so two CTAs (256 TMEM columns each) fit per SM --
+  // their small layers are latency-bound (BASELINE configs 1, 3, 5)
+  static constexpr int kStages = kLimbs == 1 ? RNSW_K1_STAGES8 : RNSW_K1_STAGES;
   static constexpr int kNStg = RNSW_K1_NSTG;  // staging buffers (unit pairs in flight to the bulk stores)
   // staging per unit PAIR (two tiles x 64 channels, or one tile x 128): the
   // bulk stores then write 128-byte rows instead of 64-byte ones
@@ -825,7 +830,10 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   }
   // one CTA (or CTA pair) per SM (pair) spread evenly over the groups
   const int sms = num_sms_current();
-  const int slots = pair ? sms / 2 : sms;
+  // co-resident CTAs per SM: 2 for the 8-bit plans when their shared memory fits twice
+  const size_t smem_need = plan.kr_limbs == 2 ? K1UConfig<2>::kSmem : K1UConfig<1>::kSmem;
+  const int per_sm = (!pair && plan.kr_limbs == 1 && 2 * (smem_need + 1024) <= 228 * 1024) ? 2 : 1;
+  const int slots = pair ? sms / 2 : sms * per_sm;
   const int per_group = slots / a.groups > 0 ? slots / a.groups : 1;
   int64_t grid = (int64_t)per_group * a.groups;
   const int64_t need = (int64_t)((a.units + 1) / 2) * a.groups;
