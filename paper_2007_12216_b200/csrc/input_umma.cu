@@ -63,14 +63,22 @@
 #ifndef RNSW_K1_DEFER
 #define RNSW_K1_DEFER 1
 #endif
+#ifndef RNSW_K1_STORE_LAG
+#define RNSW_K1_STORE_LAG 0
+#endif
+// 1 (default): the tile-pair staging rows under the 128B swizzle (conflict-free
+// stores); 0: plain rows (measured 17% slower)
+#ifndef RNSW_K1_STG_SWZ
+#define RNSW_K1_STG_SWZ 1
+#endif
 #ifndef RNSW_K1_STAGES
-#define RNSW_K1_STAGES 8
+#define RNSW_K1_STAGES (RNSW_K1_STORE_LAG ? 7 : 8)  // 3 staging buffers: one stage less fits in 227 KB
 #endif
 #ifndef RNSW_K1_STAGES8
 #define RNSW_K1_STAGES8 4
 #endif
 #ifndef RNSW_K1_NSTG
-#define RNSW_K1_NSTG 2
+#define RNSW_K1_NSTG (RNSW_K1_STORE_LAG ? 3 : 2)
 #endif
 #ifndef RNSW_K1_EPI_PIPE
 #define RNSW_K1_EPI_PIPE 0
@@ -439,6 +447,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
       // ---------------- bulk stores of the staged V rows (one per unit pair) ----------------
       const bool two = args.cblocks == 1;
       int jt = 0;
+      int lag_sb = -1, lag_p = 0, lag_c0 = 0;  // RNSW_K1_STORE_LAG: the staged pair not yet stored
       for (int pr = pr_begin; pr < npairs; pr += pr_step, ++jt) {
         int p, c0;
         unit_tile(2 * pr, p, c0);
@@ -452,15 +461,35 @@ __global__ void __launch_bounds__(kUThreads, 1)
           mbar_arrive(&sfull[sb]);
         }
         mbar_wait(&sfull[sb], sph);
-        uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
+        auto store_pair = [&](int sbx, int px, int c0x) {
+          uint8_t* sbuf = stg + sbx * Cfg::kStgBytes;
+#pragma unroll
+          for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl)
+            tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0x,
+                         (two && args.pair128) ? (px >> 1) : px, pb * kGroupRows, args.plane_base[res] + pl);
+          bulk_commit();
+          bulk_wait_read<0>();  // the staging buffer may be rewritten
+          mbar_arrive(&sempty[sbx]);
+        };
+        if (RNSW_K1_STORE_LAG) {
+          // store the PREVIOUS pair now that this one is staged too: the bulk
+          // copy then reads staging written a pair-time ago (reading staging
+          // right after its st.shared + proxy fence measured ~20% slower)
+          if (lag_sb >= 0) store_pair(lag_sb, lag_p, lag_c0);
+          lag_sb = sb;
+          lag_p = p;
+          lag_c0 = c0;
+        } else {
+          store_pair(sb, p, c0);
+        }
+      }
+      if (RNSW_K1_STORE_LAG && lag_sb >= 0) {
+        uint8_t* sbuf = stg + lag_sb * Cfg::kStgBytes;
 #pragma unroll
         for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl)
-          tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0,
-                       (two && args.pair128) ? (p >> 1) : p, pb * kGroupRows,
-                       args.plane_base[res] + pl);
+          tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), lag_c0,
+                       (two && args.pair128) ? (lag_p >> 1) : lag_p, pb * kGroupRows, args.plane_base[res] + pl);
         bulk_commit();
-        bulk_wait_read<0>();  // the staging buffer may be rewritten
-        mbar_arrive(&sempty[sb]);
       }
       bulk_wait<0>();
     }
@@ -604,7 +633,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
             // banks (64-byte rows under the 64B swizzle put them on 4 chunk
             // columns, 8-way conflicts)
             const uint32_t c16 = (uint32_t)(h_ * 4 + hh * (kEpiCols / 16) + ch);
-            off = (uint32_t)row * 128 + ((c16 ^ ((uint32_t)row & 7u)) << 4);
+            off = (uint32_t)row * 128 + (RNSW_K1_STG_SWZ ? ((c16 ^ ((uint32_t)row & 7u)) << 4) : (c16 << 4));
           } else if (two) {
             // odd P: [pos][tile h_][64 channels], 64-byte rows, 64B swizzle (chunk ^= (row >> 1) & 3)
             const uint32_t r64 = (uint32_t)(row * 2 + h_), c16 = (uint32_t)(hh * (kEpiCols / 16) + ch);
@@ -811,7 +840,7 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
       cuuint64_t strides2[3] = {(cuuint64_t)(2 * g.Cp), (cuuint64_t)g.P * g.Cp, (cuuint64_t)g.P * g.Cp * npos};
       cuuint32_t boxp[4] = {(cuuint32_t)(2 * kUnitN), 1, (cuuint32_t)kGroupRows, 1};
       if (encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims2, strides2, boxp, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                 RNSW_K1_STG_SWZ ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     } else {
