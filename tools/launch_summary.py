@@ -29,8 +29,11 @@ text = open(sys.argv[1]).read()
 rows = list(csv.DictReader(io.StringIO(text[text.index('"ID"'):])))
 launch = defaultdict(dict)
 for r in rows:
-    launch[(r["ID"], r["Kernel Name"])][r["Metric Name"]] = float(r["Metric Value"].replace(",", "")) * UNIT.get(
-        r["Metric Unit"].strip().lower(), 1.0)
+    try:
+        val = float(r["Metric Value"].replace(",", ""))
+    except ValueError:  # "n/a" (e.g. a DRAM counter ncu could not collect for a launch)
+        continue
+    launch[(r["ID"], r["Kernel Name"])][r["Metric Name"]] = val * UNIT.get(r["Metric Unit"].strip().lower(), 1.0)
 per = defaultdict(lambda: [0, 0.0, 0.0])
 for (lid, name), m in launch.items():
     k = kind_of(name)
