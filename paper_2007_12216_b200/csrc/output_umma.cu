@@ -44,6 +44,9 @@ namespace {
 #ifndef RNSW_K4_EPI2_PIPE
 #define RNSW_K4_EPI2_PIPE 1
 #endif
+#ifndef RNSW_K4_EARLY_P1
+#define RNSW_K4_EARLY_P1 1
+#endif
 #ifndef RNSW_K4_SLEEP
 #define RNSW_K4_SLEEP 0
 #endif
@@ -93,7 +96,8 @@ __global__ void __launch_bounds__(kThr, 2)
   // 1024-byte aligned, derived from the shared array so stores stay STS
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffOut + ((out_bytes(kMode) + 15) & ~15));
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+  uint64_t* bar_tfree = bar + 3;  // RNSW_K4_EARLY_P1: every warp has read its pass-2 accumulators
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
@@ -103,6 +107,7 @@ __global__ void __launch_bounds__(kThr, 2)
     mbar_init(&bar[0], 1);  // Mw8 boxes landed
     mbar_init(&bar[1], 1);  // MMA batch for warps 0-3 complete
     mbar_init(&bar[2], 1);  // MMA batch for warps 4-7 complete (implies bar[1]: commits track all prior MMAs)
+    mbar_init(bar_tfree, kThr / 32);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<256>(tslot);
@@ -145,7 +150,7 @@ __global__ void __launch_bounds__(kThr, 2)
   const int64_t u_step = gridDim.x;
   // each MMA batch is committed in two halves, one per warp group (h), so the
   // first group starts its epilogue while the second half still runs
-  uint32_t ph_tma = 0, ph_mma = 0;
+  uint32_t ph_tma = 0, ph_mma = 0, ph_tfree = 0;
   uint64_t* my_bar = &bar[1 + h];
   auto issue_p1 = [&]() {  // warp 0: pass 1 into the 256 TMEM columns once the boxes landed
     mbar_wait(&bar[0], ph_tma);
@@ -401,6 +406,21 @@ __global__ void __launch_bounds__(kThr, 2)
       load(1, 1, bH0, bL0, bH1, bL1);
       emit(1, 0, aH0, aL0, aH1, aL1);
       tmem_ld_wait();
+      if (RNSW_K4_EARLY_P1 && kMode == 3) {
+        // (pooled mode only: -1 to -2% there, +2% on the unpooled layers)
+        // this warp's TMEM reads are done: once all are, warp 0 issues the
+        // next unit's pass 1 over the same columns (it then overlaps the
+        // rest of epilogue 2 and the stores, not only the stores)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_tfree);
+        if (warp == 0 && u + u_step < args.units) {
+          mbar_wait(bar_tfree, ph_tfree);
+          tc_fence_after();
+          issue_p1();
+        }
+        ph_tfree ^= 1;
+      }
       emit(1, 1, bH0, bL0, bH1, bL1);
       (void)epi2_block;
 #else
@@ -417,7 +437,7 @@ __global__ void __launch_bounds__(kThr, 2)
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
     K4T(6)
-    if (warp == 0 && u + u_step < args.units) {
+    if (!(RNSW_K4_EARLY_P1 && RNSW_K4_EPI2_PIPE && kMode == 3) && warp == 0 && u + u_step < args.units) {
       tc_fence_after();
       issue_p1();  // the next unit's pass 1 overlaps these stores
     }
