@@ -921,7 +921,9 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
 template <int BN, int MAXPL, int MC, bool TS>
 cudaError_t run_gemm_bc_ts(const GemmArgs& a, int bc, const int8_t* V, const int8_t* U, int n_planes,
                            int n_uplanes, cudaStream_t s) {
-  if (TS && a.nkc <= 2) {
+  // two staging tiles also for CTA pairs with 64-byte chunks (C = 256: -2 to
+  // -3%; with 128-byte chunks the stages they cost hurt, +20%)
+  if (TS && (a.nkc <= 2 || (MC == 3 && bc == 64))) {
     switch (bc) {
       case 32: return run_gemm<BN, 32, MAXPL, MC, TS, 2>(a, V, U, n_planes, n_uplanes, s);
       case 64: return run_gemm<BN, 64, MAXPL, MC, TS, 2>(a, V, U, n_planes, n_uplanes, s);
