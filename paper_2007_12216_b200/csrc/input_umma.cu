@@ -53,18 +53,8 @@
 // 11 = no staging / bulk stores; each epilogue lane writes its 64 bytes straight to global (wrong layout)
 // 12 = no staging writes (the bulk stores still run, on stale staging)
 #define RNSW_K1_NO_TMEM_LD (RNSW_K1_DIAG == 9 || RNSW_K1_DIAG == 10)
-// 1: the epilogue writes the staging tile with st.async (async proxy, 16
-// transaction bytes each on the staging buffer's mbarrier; needs a cluster
-// launch) instead of st.shared + fence.proxy.async + arrive -- measured 1.55x
-// slower, so off
-#ifndef RNSW_K1_STASYNC
-#define RNSW_K1_STASYNC 0
-#endif
 #ifndef RNSW_K1_DEFER
 #define RNSW_K1_DEFER 1
-#endif
-#ifndef RNSW_K1_STORE_LAG
-#define RNSW_K1_STORE_LAG 0
 #endif
 // 1 (default): the tile-pair staging rows under the 128B swizzle (conflict-free
 // stores); 0: plain rows (measured 17% slower)
@@ -72,13 +62,13 @@
 #define RNSW_K1_STG_SWZ 1
 #endif
 #ifndef RNSW_K1_STAGES
-#define RNSW_K1_STAGES (RNSW_K1_STORE_LAG ? 7 : 8)  // 3 staging buffers: one stage less fits in 227 KB
+#define RNSW_K1_STAGES 8
 #endif
 #ifndef RNSW_K1_STAGES8
 #define RNSW_K1_STAGES8 4
 #endif
 #ifndef RNSW_K1_NSTG
-#define RNSW_K1_NSTG (RNSW_K1_STORE_LAG ? 3 : 2)
+#define RNSW_K1_NSTG 2
 #endif
 #ifndef RNSW_K1_EPI_PIPE
 #define RNSW_K1_EPI_PIPE 0
@@ -228,7 +218,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
       mbar_init(&tempty[i], kPair ? 2 * kEpiWarps : kEpiWarps);  // kPair: both CTAs' epilogue warps
     }
     for (int i = 0; i < Cfg::kNStg; ++i) {
-      mbar_init(&sfull[i], RNSW_K1_STASYNC ? 1 : 2 * kEpiWarps);  // store warp (tx bytes) / epilogue warps x 2 units
+      mbar_init(&sfull[i], 2 * kEpiWarps);  // epilogue warps x 2 units of a pair
       mbar_init(&sempty[i], 1);
     }
     fence_mbar_init();
@@ -447,49 +437,20 @@ __global__ void __launch_bounds__(kUThreads, 1)
       // ---------------- bulk stores of the staged V rows (one per unit pair) ----------------
       const bool two = args.cblocks == 1;
       int jt = 0;
-      int lag_sb = -1, lag_p = 0, lag_c0 = 0;  // RNSW_K1_STORE_LAG: the staged pair not yet stored
       for (int pr = pr_begin; pr < npairs; pr += pr_step, ++jt) {
         int p, c0;
         unit_tile(2 * pr, p, c0);
         const int sb = jt % Cfg::kNStg;
         const uint32_t sph = (uint32_t)(jt / Cfg::kNStg) & 1u;
-        if (RNSW_K1_STASYNC && !RNSW_K1_NO_STORE && RNSW_K1_DIAG != 12) {
-          // the pair's staging bytes arrive as st.async transactions
-          const uint32_t nun = 2 * pr + 1 < args.units ? 2u : 1u;
-          mbar_arrive_expect_tx(&sfull[sb], nun * (uint32_t)(kLimbs * kGroupRows * kUnitN));
-        } else if (RNSW_K1_STASYNC) {
-          mbar_arrive(&sfull[sb]);
-        }
         mbar_wait(&sfull[sb], sph);
-        auto store_pair = [&](int sbx, int px, int c0x) {
-          uint8_t* sbuf = stg + sbx * Cfg::kStgBytes;
-#pragma unroll
-          for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl)
-            tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0x,
-                         (two && args.pair128) ? (px >> 1) : px, pb * kGroupRows, args.plane_base[res] + pl);
-          bulk_commit();
-          bulk_wait_read<0>();  // the staging buffer may be rewritten
-          mbar_arrive(&sempty[sbx]);
-        };
-        if (RNSW_K1_STORE_LAG) {
-          // store the PREVIOUS pair now that this one is staged too: the bulk
-          // copy then reads staging written a pair-time ago (reading staging
-          // right after its st.shared + proxy fence measured ~20% slower)
-          if (lag_sb >= 0) store_pair(lag_sb, lag_p, lag_c0);
-          lag_sb = sb;
-          lag_p = p;
-          lag_c0 = c0;
-        } else {
-          store_pair(sb, p, c0);
-        }
-      }
-      if (RNSW_K1_STORE_LAG && lag_sb >= 0) {
-        uint8_t* sbuf = stg + lag_sb * Cfg::kStgBytes;
+        uint8_t* sbuf = stg + sb * Cfg::kStgBytes;
 #pragma unroll
         for (int pl = 0; pl < (RNSW_K1_NO_STORE ? 0 : kLimbs); ++pl)
-          tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), lag_c0,
-                       (two && args.pair128) ? (lag_p >> 1) : lag_p, pb * kGroupRows, args.plane_base[res] + pl);
+          tma_store_4d(two ? &tmV : &tmV2, sbuf + pl * (kGroupRows * 2 * kUnitN), c0,
+                       (two && args.pair128) ? (p >> 1) : p, pb * kGroupRows, args.plane_base[res] + pl);
         bulk_commit();
+        bulk_wait_read<0>();  // the staging buffer may be rewritten
+        mbar_arrive(&sempty[sb]);
       }
       bulk_wait<0>();
     }
@@ -643,17 +604,12 @@ __global__ void __launch_bounds__(kUThreads, 1)
             const uint32_t c16 = (uint32_t)(h_ * 4 + hh * (kEpiCols / 16) + ch);
             off = (uint32_t)row * 128 + ((c16 ^ ((uint32_t)row & 7u)) << 4);
           }
-          if (RNSW_K1_STASYNC)
-            st_async_v4(smem_u32(base + off), v4, smem_u32(&sfull[sb]));
-          else
-            *reinterpret_cast<uint4*>(base + off) = v4;
+          *reinterpret_cast<uint4*>(base + off) = v4;
         }
       }
-      if (!RNSW_K1_STASYNC) {
-        pend_sb = sb;
-        pend_extra = (h_ == 0 && u + 1 >= args.units) ? 1 : 0;
-        if (!RNSW_K1_DEFER) hand_off();
-      }
+      pend_sb = sb;
+      pend_extra = (h_ == 0 && u + 1 >= args.units) ? 1 : 0;
+      if (!RNSW_K1_DEFER) hand_off();
       ++it;
     }
     hand_off();  // the last unit's
@@ -871,20 +827,18 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   auto run = [&](auto kern, size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (!pair && !RNSW_K1_STASYNC) {
+    if (!pair) {
       kern<<<(unsigned)grid, kUThreads, smem, s>>>(tmX, tmV, tmV2, plan.d_kr, a);
       return cudaGetLastError();
     }
-    // a cluster launch (st.async into the CTA's own shared memory needs the
-    // shared::cluster window)
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(pair ? 2 * grid : grid));
+    cfg.gridDim = dim3((unsigned)(2 * grid));
     cfg.blockDim = dim3(kUThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = pair ? 2 : 1;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
