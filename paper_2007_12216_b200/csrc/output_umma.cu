@@ -31,6 +31,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -75,6 +76,7 @@ struct UArgs {
   int32_t* y;
   int shift;
   int vec16;           // int8 output: K % 16 == 0 and out8 16-byte aligned -> 16-byte stores
+  int tma_out;         // int8 NHWC output through a TMA bulk tensor store of the staged tile (needs vec16)
   int kblocks;
   int64_t units;       // P * kblocks work units (tile, 32-channel block)
   int32_t negw10;      // -W[1][0] (kept opaque to the compiler: one IMAD per digit)
@@ -91,7 +93,8 @@ struct UArgs {
 // waits on the same pass-2 completion and barriers.)
 template <int kMode>
 __global__ void __launch_bounds__(kThr, 2)
-    output_umma_kernel(const PlanDevice* __restrict__ plan, const __grid_constant__ CUtensorMap tm, UArgs args) {
+    output_umma_kernel(const PlanDevice* __restrict__ plan, const __grid_constant__ CUtensorMap tm,
+                       const __grid_constant__ CUtensorMap tmo, UArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned, derived from the shared array so stores stay STS
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -101,6 +104,12 @@ __global__ void __launch_bounds__(kThr, 2)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
+  // staged byte of pixel px, channel kl (int8 modes): TMA-store layout = dense
+  // 32-byte pixel rows under the 32B swizzle (16-byte chunk ^= pixel bit 2);
+  // else kPixB-byte rows for the per-thread stores
+  auto stg_off = [&](int px, int kl) {
+    return args.tma_out ? px * 32 + (kl ^ (((px >> 2) & 1) << 4)) : px * kPixB + kl;
+  };
 
   if (tid == 0) {
     tma_prefetch_desc(&tm);
@@ -251,6 +260,7 @@ __global__ void __launch_bounds__(kThr, 2)
 #endif
     }
     K4T(1)
+    if (kMode != 0 && args.tma_out && tid == 0) bulk_wait_read<0>();  // the previous tile's bulk store has read the staging
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -324,12 +334,12 @@ __global__ void __launch_bounds__(kThr, 2)
           int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
           m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
           m2 = min(m2 >> args.shift, 127);
-          if ((a & 1) == 0 && a < 14) smem[kOffOut + ((a >> 1) * 7 + c) * kPixB + kl] = (uint8_t)m2;
+          if ((a & 1) == 0 && a < 14) smem[kOffOut + stg_off((a >> 1) * 7 + c, kl)] = (uint8_t)m2;
         }
       } else if constexpr (kMode == 1) {
         if (a < 14) {
 #pragma unroll
-          for (int b = 0; b < 14; ++b) smem[kOffOut + (a * 14 + b) * kPixB + kl] = (uint8_t)qv[b];
+          for (int b = 0; b < 14; ++b) smem[kOffOut + stg_off(a * 14 + b, kl)] = (uint8_t)qv[b];
         }
       } else {
         int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
@@ -370,13 +380,13 @@ __global__ void __launch_bounds__(kThr, 2)
             int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
             m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
             m2 = min(m2 >> args.shift, 127);
-            if ((a & 1) == 0 && a < 14) smem[kOffOut + ((a >> 1) * 7 + 4 * hf + c) * kPixB + kl] = (uint8_t)m2;
+            if ((a & 1) == 0 && a < 14) smem[kOffOut + stg_off((a >> 1) * 7 + 4 * hf + c, kl)] = (uint8_t)m2;
           }
         } else if constexpr (kMode == 1) {
           if (a < 14) {
 #pragma unroll
             for (int e = 0; e < kNb; ++e)
-              if (e < nb) smem[kOffOut + (a * 14 + 8 * hf + e) * kPixB + kl] = (uint8_t)qv[e];
+              if (e < nb) smem[kOffOut + stg_off(a * 14 + 8 * hf + e, kl)] = (uint8_t)qv[e];
           }
         } else {
           int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
@@ -434,6 +444,7 @@ __global__ void __launch_bounds__(kThr, 2)
 #endif
     }
     K4T(5)
+    if (kMode != 0 && args.tma_out) fence_proxy_async();  // staging writes -> visible to the bulk store
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
     K4T(6)
@@ -443,7 +454,16 @@ __global__ void __launch_bounds__(kThr, 2)
     }
 
     // ---- stores ----
-    if constexpr (kMode == 0) {
+    if (kMode != 0 && args.tma_out) {
+      // one bulk tensor store of the staged tile (clipped at the image edges
+      // and at K); the staging is rewritten only after the next epilogue 1,
+      // by when thread 0 has waited for the read
+      constexpr int side = kMode == 3 ? 7 : 14;
+      if (tid == 0) {
+        tma_store_4d(&tmo, smem + kOffOut, k0, tj * side, ti * side, b_img);
+        bulk_commit();
+      }
+    } else if constexpr (kMode == 0) {
       const int32_t* ys = reinterpret_cast<const int32_t*>(smem + kOffOut);
       if (g.layout == 0) {
         for (int idx = tid; idx < 196 * kKB; idx += kThr) {
@@ -485,6 +505,7 @@ __global__ void __launch_bounds__(kThr, 2)
     K4T(7)
   }
 
+  if (kMode != 0 && args.tma_out && tid == 0) bulk_wait<0>();
 #ifdef RNSW_K4_PROF
   if (lane == 0 && blockIdx.x < 2 && (warp == 0 || warp == 1 || warp == 4) && pn > 0)
     printf("K4PROF cta %d warp %d units %d per-unit cycles: total %lld | wait_p1 %lld epi1 %lld bar1 %lld p2issue %lld wait_p2 %lld epi2 %lld bar2 %lld stores+p1issue %lld\n",
@@ -539,6 +560,25 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
   a.y = y;
   a.shift = shift;
   a.vec16 = out8 != nullptr && (g.K & 15) == 0 && (reinterpret_cast<uintptr_t>(out8) & 15) == 0;
+  // int8 NHWC output: one TMA bulk tensor store per tile (RNSW_K4_STG_STORES=1: the per-thread stores)
+  static const bool stg_stores = getenv("RNSW_K4_STG_STORES") != nullptr;
+  CUtensorMap tmo;
+  memset(&tmo, 0, sizeof(tmo));
+  a.tma_out = 0;
+  if (a.vec16 && !stg_stores) {
+    const bool pooled = pool != 0;
+    const int oh = pooled ? g.Ho / 2 : g.Ho, ow = pooled ? g.Wo / 2 : g.Wo, side = pooled ? 7 : 14;
+    auto encode = encode_fn();
+    if (encode != nullptr) {
+      cuuint64_t dims[4] = {(cuuint64_t)g.K, (cuuint64_t)ow, (cuuint64_t)oh, (cuuint64_t)g.B};
+      cuuint64_t strides[3] = {(cuuint64_t)g.K, (cuuint64_t)ow * g.K, (cuuint64_t)oh * ow * g.K};
+      cuuint32_t box[4] = {(cuuint32_t)kKB, (cuuint32_t)side, (cuuint32_t)side, 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      a.tma_out = encode(&tmo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, out8, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS ? 1 : 0;
+    }
+  }
   a.kblocks = (g.K + kKB - 1) / kKB;
   a.units = g.P * a.kblocks;
   if (a.units >= (1ll << 31)) return cudaErrorInvalidValue;  // FastDiv range
@@ -560,7 +600,7 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
     if (e != cudaSuccess) return e;
     const int per_sm = (228 * 1024) / (smem + 1024) >= 2 ? 2 : 1;
     const unsigned grid = (unsigned)std::min<int64_t>(a.units, (int64_t)per_sm * num_sms);
-    kern<<<grid, kThr, smem, s>>>(plan.d_plan, tm, a);
+    kern<<<grid, kThr, smem, s>>>(plan.d_plan, tm, tmo, a);
     return cudaGetLastError();
   };
   if (mode == 0) return launch(output_umma_kernel<0>, smem_bytes(0));
