@@ -48,6 +48,9 @@ namespace {
 #ifndef RNSW_K4_EARLY_P1
 #define RNSW_K4_EARLY_P1 1
 #endif
+#ifndef RNSW_K4_EARLY_P1_ALL
+#define RNSW_K4_EARLY_P1_ALL 0
+#endif
 #ifndef RNSW_K4_SLEEP
 #define RNSW_K4_SLEEP 0
 #endif
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(kThr, 2)
       load(1, 1, bH0, bL0, bH1, bL1);
       emit(1, 0, aH0, aL0, aH1, aL1);
       tmem_ld_wait();
-      if (RNSW_K4_EARLY_P1 && kMode == 3) {
+      if (RNSW_K4_EARLY_P1 && (kMode == 3 || RNSW_K4_EARLY_P1_ALL)) {
         // (pooled mode only: -1 to -2% there, +2% on the unpooled layers)
         // this warp's TMEM reads are done: once all are, warp 0 issues the
         // next unit's pass 1 over the same columns (it then overlaps the
@@ -448,7 +451,8 @@ __global__ void __launch_bounds__(kThr, 2)
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
     K4T(6)
-    if (!(RNSW_K4_EARLY_P1 && RNSW_K4_EPI2_PIPE && kMode == 3) && warp == 0 && u + u_step < args.units) {
+    if (!(RNSW_K4_EARLY_P1 && RNSW_K4_EPI2_PIPE && (kMode == 3 || RNSW_K4_EARLY_P1_ALL)) && warp == 0 &&
+        u + u_step < args.units) {
       tc_fence_after();
       issue_p1();  // the next unit's pass 1 overlaps these stores
     }
