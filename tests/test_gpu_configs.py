@@ -210,3 +210,21 @@ def test_gemm_pair_modes_in_subprocess(cg2):
                         "-k", "vgg16_batch or fused_glue or fused_requant"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.skipif(__import__("os").environ.get("RNSW_K4_STG_STORES") is not None, reason="already forced")
+def test_k4_per_thread_stores_in_subprocess():
+    """RNSW_K4_STG_STORES=1 keeps the two-pass output transform's per-thread
+    16-byte stores instead of its TMA bulk tensor store of each staged tile:
+    rerun the fused-glue checks (pooled and unpooled int8 tiles, ragged
+    edges) on that path."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, RNSW_K4_STG_STORES="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_configs.py"), "-k", "vgg16_batch1 or fused_glue or fused_requant"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
