@@ -953,6 +953,8 @@ cudaError_t run_gemm_bc(const GemmArgs& a, int bc, const int8_t* V, const int8_t
 cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp, int K,
                                  int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out, bool planar) {
   const PlanDevice& d = plan.dev;
+  // a handful of tiles: the transposed GEMM (channels on the MMA rows, half the bank bytes)
+  if (gemm_t_ok(d, P, Cp, planar, pos_out)) return launch_winograd_gemm_t(plan, V, U, P, Cp, K, Kp, Mw, s);
   GemmArgs a{};
   a.P = P;
   a.K = K;

@@ -89,6 +89,11 @@ cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, cons
                                    cudaStream_t s, bool relaxed = false);
 // pos_out: 16-bit residues as y mod m in [0, m) instead of symmetric (whole-layer
 // path only; the stage API keeps the reference's symmetric residues)
+// K3 for small P (gemm_t.cu): output channels on the MMA rows, tiles on the
+// columns, only the u limb planes of the bank (three accumulators).
+bool gemm_t_ok(const PlanDevice& d, int64_t P, int Cp, bool planar, bool pos_out);
+cudaError_t launch_winograd_gemm_t(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp, int K,
+                                   int Kp, int16_t* Mw, cudaStream_t s);
 cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const int8_t* U, int64_t P, int Cp,
                                  int K, int Kp, int bc, int16_t* Mw, cudaStream_t s, bool pos_out = false,
                                  bool planar = false);
