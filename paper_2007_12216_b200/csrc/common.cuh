@@ -4,11 +4,52 @@
 //  * thin inline-PTX wrappers for mbarrier / TMA / tcgen05.
 #pragma once
 #include <cstdint>
+#include <utility>
+
 #include <cuda_runtime.h>
 
 #include "plan.h"
 
 #define RNSW_DEV __device__ __forceinline__
+
+// ---- programmatic dependent launch (PDL) ----
+// Every kernel of the layer chain lets its successor launch early
+// (pdl_trigger, first thing) and waits for its predecessor's results
+// (pdl_wait) after a prologue that touches only constants (TMEM allocation,
+// barrier setup, plan / operator tables), so a successor's prologue overlaps
+// its predecessor's tail.  Without the launch attribute both are no-ops.
+RNSW_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+RNSW_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Host: launch with the PDL attribute (unless RNSW_PDL=0) and an optional
+// cluster dimension.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
+                             Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = (unsigned)cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // Modular arithmetic.  Residues are kept in the symmetric range

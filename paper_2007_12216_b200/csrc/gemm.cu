@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool CG2 = MC == 3;
   constexpr int CS = MC == 1 ? 1 : 2;  // CTAs per cluster
   static_assert(!CG2 || MAXPL == 2, "CTA-pair MMAs: 16-bit plans only");
+  pdl_trigger();
   using Cfg = GemmConfig<BN, BC, MAXPL, TS, SB, CG2>;
   using Tr = GemmTraits<BN, MAXPL>;
   constexpr int S = Cfg::kStages;
@@ -508,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // V (and the Mw buffer's previous readers) from the previous kernels
 
   auto stage_a = [&](int s, int pl) { return smem + s * Cfg::kStageBytes + pl * Cfg::kAPlaneBytes; };
   auto stage_b = [&](int s, int pl) {
@@ -899,23 +901,7 @@ cudaError_t run_gemm(const GemmArgs& a, const int8_t* V, const int8_t* U, int n_
   int64_t grid = a.total_tiles * CS < num_sms ? a.total_tiles * CS : num_sms;
   grid = grid / CS * CS;
   if (grid < CS) grid = CS;
-  if (MC == 1) {
-    kern<<<(unsigned)grid, kThreads, Cfg::kSmemBytes, s>>>(tmV, tmU, tmM, a);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmV, tmU, tmM, a);
+  return launch_ex(kern, dim3((unsigned)grid), dim3(kThreads), Cfg::kSmemBytes, s, CS, tmV, tmU, tmM, a);
 }
 
 template <int BN, int MAXPL, int MC, bool TS>

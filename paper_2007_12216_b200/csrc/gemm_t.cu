@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmU);
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   // unit u -> (residue, position, 128-channel block kb), kb fastest
   auto unit_coord = [&](int64_t u, int& res, int& pos, int& kb) {
@@ -233,8 +235,7 @@ cudaError_t run_gemm_t(const GemmTArgs& a, const int8_t* V, const int8_t* U, int
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
   if (e != cudaSuccess) return e;
   const int64_t grid = std::min<int64_t>(a.units, num_sms_current());
-  kern<<<(unsigned)grid, kTThreads, Cfg::kSmem, s>>>(tmU, tmV, a);
-  return cudaGetLastError();
+  return launch_ex(kern, dim3((unsigned)grid), dim3(kTThreads), Cfg::kSmem, s, 1, tmU, tmV, a);
 }
 
 }  // namespace

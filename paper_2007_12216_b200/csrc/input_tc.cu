@@ -61,6 +61,8 @@ __global__ void __launch_bounds__(128, 4) input_transform_tc_kernel(const PlanDe
                                                                  const __grid_constant__ CUtensorMap tmVout) {
   __shared__ int32_t BT16[RNSW_MAX_RES * 256];
   __shared__ __align__(1024) uint32_t OWT[2][256][16];
+  pdl_trigger();
+  pdl_wait();  // the previous kernel's activations / its use of V
   const int N = plan->n, M = plan->m_out, npos = N * N, nres = plan->n_res;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, tq = lane & 3;
   const int ncb = (g.Cp + kCTAChannels - 1) / kCTAChannels;
@@ -311,18 +313,19 @@ cudaError_t launch_input_transform_tc(const PlanHost& plan, const Geometry& g, c
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const bool full = g.layout == 0 && (g.C & 63) == 0;
+  cudaError_t e;
   if (plan.dev.res[0].planes == 2) {
     if (full)
-      input_transform_tc_kernel<2, false, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+      e = launch_ex(input_transform_tc_kernel<2, false, true>, dim3(grid), dim3(128), 0, s, 1, (const PlanDevice*)plan.d_plan, g, x, V, tm);
     else
-      input_transform_tc_kernel<2, false, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+      e = launch_ex(input_transform_tc_kernel<2, false, false>, dim3(grid), dim3(128), 0, s, 1, (const PlanDevice*)plan.d_plan, g, x, V, tm);
   } else {
     if (full)
-      input_transform_tc_kernel<1, false, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+      e = launch_ex(input_transform_tc_kernel<1, false, true>, dim3(grid), dim3(128), 0, s, 1, (const PlanDevice*)plan.d_plan, g, x, V, tm);
     else
-      input_transform_tc_kernel<1, false, false><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, tm);
+      e = launch_ex(input_transform_tc_kernel<1, false, false>, dim3(grid), dim3(128), 0, s, 1, (const PlanDevice*)plan.d_plan, g, x, V, tm);
   }
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_input_transform_compact(const PlanHost& plan, const Geometry& g, const int8_t* x, int16_t* V16,
@@ -331,11 +334,12 @@ cudaError_t launch_input_transform_compact(const PlanHost& plan, const Geometry&
   dim3 grid((unsigned)((g.P + 3) / 4));
   int8_t* V = reinterpret_cast<int8_t*>(V16);
   CUtensorMap unused{};
+  cudaError_t e;
   if (plan.dev.res[0].planes == 2)
-    input_transform_tc_kernel<2, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, unused);
+    e = launch_ex(input_transform_tc_kernel<2, true>, dim3(grid), dim3(128), 0, s, 1, (const PlanDevice*)plan.d_plan, g, x, V, unused);
   else
-    input_transform_tc_kernel<1, true><<<grid, 128, 0, s>>>(plan.d_plan, g, x, V, unused);
-  return cudaGetLastError();
+    e = launch_ex(input_transform_tc_kernel<1, true>, dim3(grid), dim3(128), 0, s, 1, (const PlanDevice*)plan.d_plan, g, x, V, unused);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace rnsw

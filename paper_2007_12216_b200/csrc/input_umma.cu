@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
                       const __grid_constant__ CUtensorMap tmV2, const uint8_t* __restrict__ kr, K1UArgs args) {
   constexpr int kLimbs = kMode == kSym8 ? 1 : 2;
   constexpr int kBN = kPair ? kUnitN / 2 : kUnitN;  // patch channels (B columns) in this CTA's shared memory
+  pdl_trigger();
   using Cfg = K1UConfig<kLimbs>;
   constexpr int S = Cfg::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -264,6 +265,7 @@ __global__ void __launch_bounds__(kUThreads, 1)
   else
     __syncthreads();
   tc_fence_after();
+  pdl_wait();  // the previous kernel's activations (and its use of V) are complete from here on
 
   // unit -> tile, channel offset
   auto unit_tile = [&](int u, int& p, int& c0) {
@@ -827,23 +829,8 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
   auto run = [&](auto kern, size_t smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (!pair) {
-      kern<<<(unsigned)grid, kUThreads, smem, s>>>(tmX, tmV, tmV2, plan.d_kr, a);
-      return cudaGetLastError();
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * grid));
-    cfg.blockDim = dim3(kUThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, tmX, tmV, tmV2, plan.d_kr, a);
+    return launch_ex(kern, dim3((unsigned)(pair ? 2 * grid : grid)), dim3(kUThreads), smem, s, pair ? 2 : 1, tmX, tmV,
+                     tmV2, (const uint8_t*)plan.d_kr, a);
   };
   if (pair) {
     if (plan.kr_limbs == 2)

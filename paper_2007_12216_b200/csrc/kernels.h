@@ -89,6 +89,9 @@ cudaError_t launch_input_transform(const PlanHost& plan, const Geometry& g, cons
                                    cudaStream_t s, bool relaxed = false);
 // pos_out: 16-bit residues as y mod m in [0, m) instead of symmetric (whole-layer
 // path only; the stage API keeps the reference's symmetric residues)
+// Tile count of the layer being launched (capi.cu): gates programmatic dependent launch.
+void pdl_layer_hint(int64_t P);
+
 // K3 for small P (gemm_t.cu): output channels on the MMA rows, tiles on the
 // columns, only the u limb planes of the bank (three accumulators).
 bool gemm_t_ok(const PlanDevice& d, int64_t P, int Cp, bool planar, bool pos_out);

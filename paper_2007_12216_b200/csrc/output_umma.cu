@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kThr, 2)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
+  pdl_trigger();
   // staged byte of pixel px, channel kl (int8 modes): TMA-store layout = dense
   // 32-byte pixel rows under the 32B swizzle (16-byte chunk ^= pixel bit 2);
   // else kPixB-byte rows for the per-thread stores
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(kThr, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
+  pdl_wait();  // Mw8 and the output buffer's previous users
 
   const int32_t negw10 = args.negw10;
   const uint32_t mul0 = args.mul0;
@@ -604,8 +606,7 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
     if (e != cudaSuccess) return e;
     const int per_sm = (228 * 1024) / (smem + 1024) >= 2 ? 2 : 1;
     const unsigned grid = (unsigned)std::min<int64_t>(a.units, (int64_t)per_sm * num_sms);
-    kern<<<grid, kThr, smem, s>>>(plan.d_plan, tm, tmo, a);
-    return cudaGetLastError();
+    return launch_ex(kern, dim3(grid), dim3(kThr), (size_t)smem, s, 1, (const PlanDevice*)plan.d_plan, tm, tmo, a);
   };
   if (mode == 0) return launch(output_umma_kernel<0>, smem_bytes(0));
   if (mode == 1) return launch(output_umma_kernel<1>, smem_bytes(1));

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(256, kC3 ? RNSW_SMALLC_MINB : 2) smallc_produc
                                                              int Kp, int Cp, const int16_t* __restrict__ V16,
                                                              const int8_t* __restrict__ U, int16_t* __restrict__ Mw,
                                                              int tiles_per_cta) {
+  pdl_trigger();
   const int N = plan->n, npos = N * N, nres = plan->n_res;
   const int kgroups = Kp >> 3;
   const int slot = blockIdx.x * blockDim.x + threadIdx.x;
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(256, kC3 ? RNSW_SMALLC_MINB : 2) smallc_produc
     }
   }
   const int32_t bias = kPL == 2 ? pos_bias(fm) : fm.off;
+  pdl_wait();  // V16 from the input transform
   const int p_begin = blockIdx.z * tiles_per_cta, p_end = min(P, p_begin + tiles_per_cta);
   const uint2* src = reinterpret_cast<const uint2*>(V16) + ((int64_t)r * P + p_begin) * npos + pos;
   const int rp = r * npos + pos, nrp = nres * npos;
@@ -138,15 +140,16 @@ cudaError_t launch_smallc_product(const PlanHost& plan, const Geometry& g, const
   const int64_t per_tile = (int64_t)bx * d.n_res;
   const int tpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, g.P * per_tile / (148 * 4)));
   dim3 grid(bx, d.n_res, (unsigned)((g.P + tpc - 1) / tpc));
+  cudaError_t e;
   if (d.res[0].planes == 2 && planar && g.C == 3)
-    smallc_product_kernel<2, true, true><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+    e = launch_ex(smallc_product_kernel<2, true, true>, grid, dim3(256), 0, s, 1, (const PlanDevice*)plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
   else if (d.res[0].planes == 2 && planar)
-    smallc_product_kernel<2, true><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+    e = launch_ex(smallc_product_kernel<2, true>, grid, dim3(256), 0, s, 1, (const PlanDevice*)plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
   else if (d.res[0].planes == 2)
-    smallc_product_kernel<2><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+    e = launch_ex(smallc_product_kernel<2>, grid, dim3(256), 0, s, 1, (const PlanDevice*)plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
   else
-    smallc_product_kernel<1><<<grid, 256, 0, s>>>(plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
-  return cudaGetLastError();
+    e = launch_ex(smallc_product_kernel<1>, grid, dim3(256), 0, s, 1, (const PlanDevice*)plan.d_plan, (int)g.P, g.K, g.Kp, g.Cp, V16, U, Mw, tpc);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace rnsw
