@@ -18,7 +18,8 @@
 //
 // Warps: 0 TMA producer, 1 MMA issuer, 2-5 epilogue (TMEM lane quadrant
 // warp & 3; warp 2 also owns the TMEM allocation).  Accumulators are double
-// buffered (2 x 3 x Np <= 512 TMEM columns).
+// buffered while 2 x 3 x Np <= 512 TMEM columns (Np <= 80), single buffered
+// above (Np 96-128: the next unit's MMAs wait for the epilogue's TMEM reads).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -33,7 +34,6 @@ namespace {
 
 constexpr int kTThreads = 192;
 constexpr int kTBC = 128;     // channel chunk (bytes) per stage: 128B-swizzled K-major rows
-constexpr int kTStages = 4;
 
 struct GemmTArgs {
   int P, K, Kp, Cp, npos, n_res, nkc, num_kb;
@@ -52,8 +52,11 @@ struct GemmTConfig {
   static constexpr int kBPlane = NP * kTBC;   // one V limb plane: NP tile rows
   static constexpr int kStage = 2 * kAPlane + 2 * kBPlane;
   static constexpr int kAccCols = 3 * NP;     // D65536 | D256 | D1
-  static constexpr size_t kSmem = 1024 + (size_t)kTStages * kStage + 256;
-  static_assert(2 * kAccCols <= 512, "accumulators exceed TMEM");
+  static constexpr int kNB = 2 * kAccCols <= 512 ? 2 : 1;  // accumulator buffers
+  static constexpr int kStages = NP <= 80 ? 4 : 3;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * kStage + 256;
+  static_assert(kNB * kAccCols <= 512, "accumulators exceed TMEM");
+  static_assert(kSmem <= 227 * 1024, "stages exceed shared memory");
 };
 
 template <int NP>
@@ -61,7 +64,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
     winograd_gemm_t_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmV,
                            GemmTArgs args) {
   using Cfg = GemmTConfig<NP>;
-  constexpr int S = kTStages;
+  constexpr int S = Cfg::kStages;
+  constexpr int NB = Cfg::kNB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStage);
@@ -133,8 +137,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
     uint32_t phase = 0;
     int it = 0;
     for (int64_t u = blockIdx.x; u < args.units; u += gridDim.x, ++it) {
-      const int as = it & 1;
-      mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+      const int as = it % NB;
+      mbar_wait(&tempty[as], ((it / NB) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d65536 = tmem_base + as * Cfg::kAccCols, d256 = d65536 + NP, d1 = d65536 + 2 * NP;
       for (int kc = 0; kc < args.nkc; ++kc) {
@@ -168,8 +172,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
     for (int64_t u = blockIdx.x; u < args.units; u += gridDim.x, ++it) {
       int res, pos, kb;
       unit_coord(u, res, pos, kb);
-      const int as = it & 1;
-      mbar_wait(&tfull[as], (it >> 1) & 1);
+      const int as = it % NB;
+      mbar_wait(&tfull[as], (it / NB) & 1);
       tc_fence_after();
       const FastMod fm = args.fm[res];
       const int32_t r65536 = args.r65536[res], pb = pos_bias(fm);
@@ -241,9 +245,9 @@ cudaError_t run_gemm_t(const GemmTArgs& a, const int8_t* V, const int8_t* U, int
 }  // namespace
 
 bool gemm_t_ok(const PlanDevice& d, int64_t P, int Cp, bool planar, bool pos_out) {
-  // RNSW_GEMM_T=0: never; =N: up to N tiles (default 48, at most 80)
+  // RNSW_GEMM_T=0: never; =N: up to N tiles (default 48, at most 128)
   static const char* env = getenv("RNSW_GEMM_T");
-  static const int max_p = env != nullptr ? std::min(atoi(env), 80) : 48;
+  static const int max_p = env != nullptr ? std::min(atoi(env), 128) : 48;
   if (!planar || !pos_out || P > max_p || Cp % kTBC != 0 || Cp > 8192 || !d.fast) return false;
   for (int r = 0; r < d.n_res; ++r)
     if (d.res[r].planes != 2) return false;
@@ -278,7 +282,9 @@ cudaError_t launch_winograd_gemm_t(const PlanHost& plan, const int8_t* V, const 
   if (P <= 32) return run_gemm_t<32>(a, V, U, np, nup, s);
   if (P <= 48) return run_gemm_t<48>(a, V, U, np, nup, s);
   if (P <= 64) return run_gemm_t<64>(a, V, U, np, nup, s);
-  return run_gemm_t<80>(a, V, U, np, nup, s);
+  if (P <= 80) return run_gemm_t<80>(a, V, U, np, nup, s);
+  if (P <= 96) return run_gemm_t<96>(a, V, U, np, nup, s);
+  return run_gemm_t<128>(a, V, U, np, nup, s);
 }
 
 }  // namespace rnsw

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 SYS16 = (4001, 4331)
 
-# (h, w, c, k, batch, tile_m): P = batch * ceil(h/m) * ceil(w/m) <= 48
+# (h, w, c, k, batch, tile_m): P = batch * ceil(h/m) * ceil(w/m); P > 48 runs forced below
 CASES = [
     (14, 14, 128, 64, 1, 14),    # P = 1
     (28, 28, 256, 96, 3, 14),    # P = 12, K = 96 (one partial channel block)
@@ -27,6 +27,10 @@ CASES = [
     (56, 56, 128, 48, 2, 14),    # P = 32
     (30, 30, 384, 144, 5, 14),   # P = 45 -> N = 48, C = 384 (three 128-channel chunks)
     (24, 24, 128, 128, 4, 10),   # F(10,3): N = 12 (144 positions), P = 36
+    (28, 28, 128, 128, 16, 14),  # P = 64
+    (28, 28, 256, 160, 20, 14),  # P = 80, K = 160
+    (28, 28, 128, 128, 23, 14),  # P = 92 -> N = 96 (single-buffered accumulators)
+    (28, 28, 512, 256, 32, 14),  # P = 128: the deep VGG16 layers at batch 32
 ]
 
 
@@ -35,6 +39,8 @@ def test_small_p_layer_matches_direct_conv(case):
     import paper_2007_12216_b200 as rnsw
 
     h, w, c, k, b, tm = case
+    if b * -(-h // tm) * -(-w // tm) > int(os.environ.get("RNSW_GEMM_T", "48")):
+        pytest.skip("P above the small-P GEMM's default range: covered by the forced run")
     rng = np.random.default_rng(hash(case) & 0xFFFFFFFF)
     x = rng.integers(-128, 128, (b, h, w, c), dtype=np.int8)
     wt = rng.integers(-128, 128, (3, 3, c, k), dtype=np.int8)
@@ -51,9 +57,11 @@ def test_small_p_layer_matches_direct_conv(case):
 
 
 @pytest.mark.skipif(os.environ.get("RNSW_GEMM_T") is not None, reason="already forced")
-def test_regular_gemm_for_the_same_shapes():
-    """RNSW_GEMM_T=0: the tile-row GEMM for every P; the same checks must hold."""
-    env = dict(os.environ, RNSW_GEMM_T="0")
+@pytest.mark.parametrize("max_p", ["0", "128"])
+def test_forced_gemm_choice_for_the_same_shapes(max_p):
+    """RNSW_GEMM_T=0: the tile-row GEMM for every P; =128: the small-P GEMM for
+    every case above (N up to 128); the same checks must hold."""
+    env = dict(os.environ, RNSW_GEMM_T=max_p)
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(here, "test_gpu_gemm_t.py"), "-k", "matches_direct"],
