@@ -364,7 +364,11 @@ def run_gpu_arm(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    # RNSW_BENCH_FORCE_DIST=1: initialise NCCL and run the gather / max-over-ranks
+    # collectives even with one rank (the multi-rank code path on a one-GPU box)
+    force = os.environ.get("RNSW_BENCH_FORCE_DIST") == "1" and "RANK" in os.environ
+    multi = world > 1 or force
+    if multi:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     # strong scaling (default): config 4's batch is split over the ranks;
     # weak: every rank serves its own --batch images.  The ranks meet once,
@@ -375,7 +379,7 @@ def run_gpu_arm(args):
     x_host = W.vgg16_images(shard, start=start)
     x_pinned = torch.from_numpy(x_host).pin_memory()
     x_dev = x_pinned.cuda()
-    gathered = torch.empty((global_batch, 7, 7, 512), dtype=torch.int8, device="cuda") if world > 1 else None
+    gathered = torch.empty((global_batch, 7, 7, 512), dtype=torch.int8, device="cuda") if multi else None
     out_pinned = torch.empty((global_batch if rank == 0 else shard, 7, 7, 512), dtype=torch.int8).pin_memory()
 
     fwd = net.forward if args.unfused else net.forward_fused
@@ -386,12 +390,12 @@ def run_gpu_arm(args):
     fwd_staged = net.forward_staged if args.unfused else net.forward_fused_staged
 
     def step(x):
-        return parallel.gather_maps(fwd(x), world, out=gathered)
+        return parallel.gather_maps(fwd(x), world, out=gathered, force=force)
 
     graph_used = not args.unfused and not args.no_graph
 
     def barrier():
-        if world > 1:
+        if multi:
             dist.barrier()
 
     # clocks are sampled from before the warm-up (nvidia-smi needs ~0.5 s to
@@ -414,7 +418,7 @@ def run_gpu_arm(args):
         e1.record()
         torch.cuda.synchronize()
         barrier()
-    elapsed = parallel.max_over_ranks(e0.elapsed_time(e1) / 1e3, world, device="cuda")
+    elapsed = parallel.max_over_ranks(e0.elapsed_time(e1) / 1e3, world, device="cuda", force=force)
     total_ops = W.VGGConfig(batch=global_batch).direct_ops() * args.steps
     value = total_ops / elapsed / 1e12
     ms_per_step = elapsed / args.steps * 1e3
@@ -446,7 +450,7 @@ def run_gpu_arm(args):
     if graph_used:
         host_in = [x_pinned] * args.steps
         host_out = [out_pinned if rank == 0 else None] * args.steps
-        post = (lambda y: parallel.gather_maps(y, world, out=gathered)) if world > 1 else None
+        post = (lambda y: parallel.gather_maps(y, world, out=gathered, force=force)) if multi else None
         net.run_stream(host_in[:2], host_out[:2], post=post)  # warm-up: graphs, buffers, streams
         torch.cuda.synchronize()
         barrier()
@@ -462,13 +466,13 @@ def run_gpu_arm(args):
                 out_pinned.copy_(y, non_blocking=True)
         h1.record()
     torch.cuda.synchronize()
-    e2e_elapsed = parallel.max_over_ranks(h0.elapsed_time(h1) / 1e3, world, device="cuda")
+    e2e_elapsed = parallel.max_over_ranks(h0.elapsed_time(h1) / 1e3, world, device="cuda", force=force)
     e2e_value = total_ops / e2e_elapsed / 1e12
     h2d = x_host.nbytes * world
     d2h = out_pinned.numel()
 
     if rank != 0:
-        if world > 1:
+        if multi:
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -563,8 +567,10 @@ def run_gpu_arm(args):
                       f"reference winograd_layer_conv (one thread per modulus, as shipped), filters precomputed; "
                       f"{wall:.1f} s",
         }
+    if force:
+        line["forced_collectives"] = "NCCL initialised with one rank; gather and max-over-ranks ran as collectives"
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -1,5 +1,5 @@
-// K3 for small tile counts (16-bit residues, P <= 80 tiles: VGG16 at batch 1,
-// the deep layers at batch 32): the per-position modular GEMM of
+// K3 for small tile counts (16-bit residues, P <= 48 tiles, <= 80 for C >= 512:
+// VGG16 at batch 1, the deep layers at batch <= 64): the per-position modular GEMM of
 // rw/layer.py:285-291 / rw/gemm.py:43-97 with the operand roles swapped.
 //
 // The general GEMM (gemm.cu) puts tiles on the MMA's M = 128 rows: with a
@@ -245,9 +245,14 @@ cudaError_t run_gemm_t(const GemmTArgs& a, const int8_t* V, const int8_t* U, int
 }  // namespace
 
 bool gemm_t_ok(const PlanDevice& d, int64_t P, int Cp, bool planar, bool pos_out) {
-  // RNSW_GEMM_T=0: never; =N: up to N tiles (default 48, at most 128)
+  // RNSW_GEMM_T=0: never; =N: up to N tiles (at most 128).  Default: up to 48
+  // tiles, and up to 80 for C >= 512, where streaming half the filter-bank
+  // bytes outweighs the costlier N = 64 / 80 MMAs (conv5 at batch 64: 0.077
+  // vs 0.106 ms; conv3 at batch 4, C = 256: 0.037 vs 0.029 ms the other way).
+  // At 96-128 tiles (single-buffered accumulators) the tile-row GEMM wins.
   static const char* env = getenv("RNSW_GEMM_T");
-  static const int max_p = env != nullptr ? std::min(atoi(env), 128) : 48;
+  static const int forced = env != nullptr ? std::min(atoi(env), 128) : -1;
+  const int max_p = forced >= 0 ? forced : (Cp >= 512 ? 80 : 48);
   if (!planar || !pos_out || P > max_p || Cp % kTBC != 0 || Cp > 8192 || !d.fast) return false;
   for (int r = 0; r < d.n_res; ++r)
     if (d.res[r].planes != 2) return false;

@@ -30,12 +30,14 @@ def shard_range(batch: int, world: int, rank: int) -> tuple[int, int]:
     return rank * per, per
 
 
-def gather_maps(local, world: int, out=None):
-    """All-gather equal-shaped per-rank tensors along dim 0 (rank order)."""
+def gather_maps(local, world: int, out=None, force: bool = False):
+    """All-gather equal-shaped per-rank tensors along dim 0 (rank order).
+    ``force`` runs the collective even for a single rank (a one-GPU check of
+    the NCCL path)."""
     import torch
     import torch.distributed as dist
 
-    if world == 1:
+    if world == 1 and not force:
         return local
     if out is None:
         out = torch.empty((local.shape[0] * world, *local.shape[1:]), dtype=local.dtype, device=local.device)
@@ -49,11 +51,11 @@ def gather_maps(local, world: int, out=None):
     return out
 
 
-def max_over_ranks(seconds: float, world: int, device=None) -> float:
+def max_over_ranks(seconds: float, world: int, device=None, force: bool = False) -> float:
     import torch
     import torch.distributed as dist
 
-    if world == 1:
+    if world == 1 and not force:
         return seconds
     t = torch.tensor([seconds], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)

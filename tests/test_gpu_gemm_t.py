@@ -1,6 +1,6 @@
 """The small-P GEMM (csrc/gemm_t.cu: output channels on the MMA rows, tiles on
 the columns, only the u limb planes of the filter bank, three accumulators)
-that whole-layer calls with 16-bit residues and at most 48 tiles take
+that whole-layer calls with 16-bit residues and at most 48 tiles (80 for C >= 512) take
 (rw/layer.py:285-291 semantics): end to end against the exact direct
 convolution, including tile counts that are not multiples of 16, K that is
 not a multiple of 128 (the last channel block is partly outside Kp), several
@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 SYS16 = (4001, 4331)
 
-# (h, w, c, k, batch, tile_m): P = batch * ceil(h/m) * ceil(w/m); P > 48 runs forced below
+# (h, w, c, k, batch, tile_m): P = batch * ceil(h/m) * ceil(w/m); both GEMMs run every case (forced below)
 CASES = [
     (14, 14, 128, 64, 1, 14),    # P = 1
     (28, 28, 256, 96, 3, 14),    # P = 12, K = 96 (one partial channel block)
@@ -31,6 +31,7 @@ CASES = [
     (28, 28, 256, 160, 20, 14),  # P = 80, K = 160
     (28, 28, 128, 128, 23, 14),  # P = 92 -> N = 96 (single-buffered accumulators)
     (28, 28, 512, 256, 32, 14),  # P = 128: the deep VGG16 layers at batch 32
+    (14, 14, 512, 128, 64, 14),  # P = 64, C = 512: small-P GEMM by default (conv5 at batch 64)
 ]
 
 
@@ -39,8 +40,6 @@ def test_small_p_layer_matches_direct_conv(case):
     import paper_2007_12216_b200 as rnsw
 
     h, w, c, k, b, tm = case
-    if b * -(-h // tm) * -(-w // tm) > int(os.environ.get("RNSW_GEMM_T", "48")):
-        pytest.skip("P above the small-P GEMM's default range: covered by the forced run")
     rng = np.random.default_rng(hash(case) & 0xFFFFFFFF)
     x = rng.integers(-128, 128, (b, h, w, c), dtype=np.int8)
     wt = rng.integers(-128, 128, (3, 3, c, k), dtype=np.int8)
