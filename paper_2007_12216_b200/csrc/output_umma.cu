@@ -70,8 +70,14 @@ constexpr int kOffB2 = kOffB1 + 2 * 1024;         // [res][step]       4 x 1 KB
 constexpr int kOffOut = kOffB2 + 4 * 1024;        // output staging
 constexpr int kPixB = 48;   // staged bytes per pixel, int8 modes (16-byte aligned rows for 16-byte stores)
 constexpr int kPixW = 33;   // staged words per pixel (int32 mode)
-constexpr int out_bytes(int mode) { return mode == 0 ? 196 * kPixW * 4 : (mode == 1 ? 196 * kPixB : 49 * kPixB); }
+// The int32 mode stages its 196 x 33-word tile in the A1 region (32 KB, free
+// once pass 1 has completed): the next unit's Mw8 boxes are then requested
+// after the stores instead of during the epilogues, and in exchange two CTAs
+// fit per SM like in the int8 modes (a separate 26 KB staging tile allowed one).
+constexpr int out_bytes(int mode) { return mode == 0 ? 0 : (mode == 1 ? 196 * kPixB : 49 * kPixB); }
+constexpr int out_off(int mode) { return mode == 0 ? kOffA1 : kOffOut; }
 constexpr int smem_bytes(int mode) { return 1024 + kOffOut + ((out_bytes(mode) + 15) & ~15) + 64; }
+static_assert(196 * kPixW * 4 <= 8 * kOpBytes, "the int32 tile must fit the A1 region");
 
 struct UArgs {
   Geometry g;
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kThr, 2)
     ph_mma ^= 1;
     tc_fence_after();
     // the second group's barrier means all of pass 1 is done: A1 is free
-    if (tid == kThr / 2 && u + u_step < args.units) issue_load(u + u_step);  // lands during the epilogues
+    if (kMode != 0 && tid == kThr / 2 && u + u_step < args.units) issue_load(u + u_step);  // lands during the epilogues
 
     // ---- epilogue 1: warp (q, h): columns j = 4 gg + q of residue h, lane = channel ----
     {
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(kThr, 2)
           for (int b = 0; b < 14; ++b) smem[kOffOut + stg_off(a * 14 + b, kl)] = (uint8_t)qv[b];
         }
       } else {
-        int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
+        int32_t* ys = reinterpret_cast<int32_t*>(smem + out_off(0));
         if (a < 14) {
 #pragma unroll
           for (int b = 0; b < 14; ++b) ys[(a * 14 + b) * kPixW + kl] = qv[b];
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(kThr, 2)
               if (e < nb) smem[kOffOut + stg_off(a * 14 + 8 * hf + e, kl)] = (uint8_t)qv[e];
           }
         } else {
-          int32_t* ys = reinterpret_cast<int32_t*>(smem + kOffOut);
+          int32_t* ys = reinterpret_cast<int32_t*>(smem + out_off(0));
           if (a < 14) {
 #pragma unroll
             for (int e = 0; e < kNb; ++e)
@@ -421,7 +427,7 @@ __global__ void __launch_bounds__(kThr, 2)
       load(1, 1, bH0, bL0, bH1, bL1);
       emit(1, 0, aH0, aL0, aH1, aL1);
       tmem_ld_wait();
-      if (RNSW_K4_EARLY_P1 && (kMode == 3 || RNSW_K4_EARLY_P1_ALL)) {
+      if (RNSW_K4_EARLY_P1 && (kMode == 3 || (RNSW_K4_EARLY_P1_ALL && kMode != 0))) {
         // (pooled mode only: -1 to -2% there, +2% on the unpooled layers)
         // this warp's TMEM reads are done: once all are, warp 0 issues the
         // next unit's pass 1 over the same columns (it then overlaps the
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(kThr, 2)
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
     K4T(6)
-    if (!(RNSW_K4_EARLY_P1 && RNSW_K4_EPI2_PIPE && (kMode == 3 || RNSW_K4_EARLY_P1_ALL)) && warp == 0 &&
+    if (kMode != 0 && !(RNSW_K4_EARLY_P1 && RNSW_K4_EPI2_PIPE && (kMode == 3 || (RNSW_K4_EARLY_P1_ALL && kMode != 0))) && warp == 0 &&
         u + u_step < args.units) {
       tc_fence_after();
       issue_p1();  // the next unit's pass 1 overlaps these stores
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(kThr, 2)
         bulk_commit();
       }
     } else if constexpr (kMode == 0) {
-      const int32_t* ys = reinterpret_cast<const int32_t*>(smem + kOffOut);
+      const int32_t* ys = reinterpret_cast<const int32_t*>(smem + out_off(0));
       if (g.layout == 0) {
         for (int idx = tid; idx < 196 * kKB; idx += kThr) {
           const int px = idx >> 5, c = idx & 31, a = px / 14, b = px - a * 14;
@@ -506,6 +512,17 @@ __global__ void __launch_bounds__(kThr, 2)
         if (ho >= Ho || wo >= Wo || k0 + 4 * wq >= g.K) continue;
         const uint32_t word = *reinterpret_cast<const uint32_t*>(smem + kOffOut + px * kPixB + 4 * wq);
         *reinterpret_cast<uint32_t*>(args.out8 + (((int64_t)b_img * Ho + ho) * Wo + wo) * g.K + k0 + 4 * wq) = word;
+      }
+    }
+    if constexpr (kMode == 0) {
+      // the staged tile (in A1) has been read by every thread: the async proxy may overwrite it
+      fence_proxy_async();
+      __syncthreads();
+      if (warp == 0 && u + u_step < args.units) {
+        if (lane == 0) issue_load(u + u_step);
+        __syncwarp();
+        tc_fence_after();
+        issue_p1();  // waits for the boxes; the other CTA of the SM computes meanwhile
       }
     }
     K4T(7)
@@ -598,10 +615,8 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
   auto launch = [&](auto kern, int smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    // persistent grid: as many CTAs as are co-resident -- 2 per SM for the
-    // int8 modes (launch bounds), 1 for the int32 mode, whose 26 KB staging
-    // tile does not fit twice in the 228 KB of shared memory (1 KB reserved
-    // per CTA)
+    // persistent grid: as many CTAs as are co-resident -- 2 per SM in every
+    // mode (launch bounds; the shared-memory footprint is checked below)
     e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     const int per_sm = (228 * 1024) / (smem + 1024) >= 2 ? 2 : 1;
