@@ -70,6 +70,15 @@ constexpr int kOffB2 = kOffB1 + 2 * 1024;         // [res][step]       4 x 1 KB
 constexpr int kOffOut = kOffB2 + 4 * 1024;        // output staging
 constexpr int kPixB = 48;   // staged bytes per pixel, int8 modes (16-byte aligned rows for 16-byte stores)
 constexpr int kPixW = 33;   // staged words per pixel (int32 mode)
+// Staging of the int8 tile when it leaves through one TMA bulk tensor store
+// (kTma): dense 32-byte pixels, every staged byte at a per-thread base plus a
+// literal.  Pooled (7 x 7): no swizzle (rows 224 bytes apart: the 7 storing
+// lanes of a warp meet 2-way).  Unpooled (14 x 14): 32B swizzle (16-byte chunk
+// ^= pixel bit 2; dense rows would put a warp's 16 rows a into two banks); the
+// swizzle bit of pixel (a, b) is bit 2 of (6 a mod 8) + b, so each thread
+// keeps four bases -- plain / flipped chunk, for columns whose bit agrees or
+// disagrees between even and odd rows -- and picks one per column at compile
+// time.
 // The int32 mode stages its 196 x 33-word tile in the A1 region (32 KB, free
 // once pass 1 has completed): the next unit's Mw8 boxes are then requested
 // after the stores instead of during the epilogues, and in exchange two CTAs
@@ -78,6 +87,37 @@ constexpr int out_bytes(int mode) { return mode == 0 ? 0 : (mode == 1 ? 196 * kP
 constexpr int out_off(int mode) { return mode == 0 ? kOffA1 : kOffOut; }
 constexpr int smem_bytes(int mode) { return 1024 + kOffOut + ((out_bytes(mode) + 15) & ~15) + 64; }
 static_assert(196 * kPixW * 4 <= 8 * kOpBytes, "the int32 tile must fit the A1 region");
+
+// The MMA batches of a pass are issued from ONE asm block: one elect.sync,
+// every descriptor = the (1024-byte aligned) shared-memory base in descriptor
+// units plus a literal, so the issuing warp spends a few instructions per MMA
+// (separate per-MMA blocks rebuilt both 64-bit descriptors from the address
+// and re-elected each time: ~17 instructions per MMA on the critical warp).
+#define K4_OFF_A1 0
+#define K4_OFF_A2 32768
+#define K4_OFF_B1 98304
+#define K4_OFF_B2 100352
+static_assert(K4_OFF_A1 == kOffA1 && K4_OFF_A2 == kOffA2 && K4_OFF_B1 == kOffB1 && K4_OFF_B2 == kOffB2, "asm offsets");
+#define K4_STR2(x) #x
+#define K4_STR(x) K4_STR2(x)
+// D columns, A byte offset / LBO field / high word, B byte offset, idesc operand, accumulate predicate
+#define K4_MMA(DCOL, AOFF, ALBO, AHI, BOFF, ID, ACCP)                           \
+  "add.u32 t, %0, " K4_STR(DCOL) ";\n\t"                                        \
+  "add.u32 al, %1, " K4_STR((((AOFF) >> 4) + ((ALBO) << 16))) ";\n\t"           \
+  "add.u32 bl, %1, " K4_STR((((BOFF) >> 4) + (1 << 16))) ";\n\t"                \
+  "mov.b64 da, {al, " K4_STR(AHI) "};\n\t"                                      \
+  "mov.b64 db, {bl, 0xC0004010};\n\t"                                           \
+  "@e tcgen05.mma.cta_group::1.kind::i8 [t], da, db, " ID ", " ACCP ";\n\t"
+#define K4_COMMIT(BAR) "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [" BAR "];\n\t"
+// pass 1, v = res * 4 + gg: A1 + v * 4 KB (MN-major, 32B swizzle, LBO 1 KB), B1 + res * 1 KB
+#define K4_P1(V) K4_MMA((V) * 32, K4_OFF_A1 + (V) * 4096, 64, 0xC0004010, K4_OFF_B1 + ((V) >> 2) * 1024, "%2", "pz")
+// pass 2, v = res * 4 + mb: A2 + v * 8 KB (MN-major, 128B swizzle; step 1 at + 4 KB), B2 + res * 2 KB (+ 1 KB)
+#define K4_P2(V)                                                                                              \
+  K4_MMA((V) * 32, K4_OFF_A2 + (V) * 8192, 1, 0x40004040, K4_OFF_B2 + ((V) >> 2) * 2048, "%2", "pz")           \
+  K4_MMA((V) * 32, K4_OFF_A2 + (V) * 8192 + 4096, 1, 0x40004040, K4_OFF_B2 + ((V) >> 2) * 2048 + 1024, "%3", "po")
+#define K4_ASM_HEAD                                                                                   \
+  "{\n\t.reg .pred e, pz, po;\n\t.reg .b32 t, al, bl;\n\t.reg .b64 da, db;\n\t"                        \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 pz, 0, 0;\n\tsetp.eq.b32 po, 0, 0;\n\t"
 
 struct UArgs {
   Geometry g;
@@ -100,7 +140,7 @@ struct UArgs {
 // (A single 16-warp CTA per SM that overlaps pass 1 of the next unit with
 // epilogue 2 in separate TMEM halves measured 25% slower: every warp then
 // waits on the same pass-2 completion and barriers.)
-template <int kMode>
+template <int kMode, bool kTma>
 __global__ void __launch_bounds__(kThr, 2)
     output_umma_kernel(const PlanDevice* __restrict__ plan, const __grid_constant__ CUtensorMap tm,
                        const __grid_constant__ CUtensorMap tmo, UArgs args) {
@@ -114,12 +154,34 @@ __global__ void __launch_bounds__(kThr, 2)
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
   pdl_trigger();
-  // staged byte of pixel px, channel kl (int8 modes): TMA-store layout = dense
-  // 32-byte pixel rows under the 32B swizzle (16-byte chunk ^= pixel bit 2);
-  // else kPixB-byte rows for the per-thread stores
-  auto stg_off = [&](int px, int kl) {
-    return args.tma_out ? px * 32 + (kl ^ (((px >> 2) & 1) << 4)) : px * kPixB + kl;
+  // staged bytes (int8 modes): this thread's rows (k, a) start at st_base; a
+  // pixel is kPix bytes, the second channel block of the warp group 8 further
+  constexpr int kPix = kTma ? 32 : kPixB;
+  uint8_t* st_base;
+  uint8_t* st_e[2];  // unpooled kTma: columns b with b % 4 < 2, swizzle bit = bit2(b) ^ s
+  uint8_t* st_f[2];  //                columns b with b % 4 >= 2
+  {
+    const int a = lane & 15, kl0 = 16 * h + 2 * q + (lane >> 4);
+    const int row = kMode == 3 ? (a >> 1) * 7 * kPix : a * 14 * kPix;
+    st_base = smem + kOffOut + row + kl0;
+    // bit 2 of (14 a + b) = bit2(b) ^ [a % 4 == 2]          for even a
+    //                     = bit2(b + 2) ^ [a % 4 == 1]      for odd a
+    const int flip = (a & 1) ? ((a & 3) == 1) : ((a & 3) == 2);
+    st_e[0] = st_base + 16 * (flip ? 1 - 2 * h : 0);  // chunk bit of kl0 is h: kl0 ^ 16
+    st_e[1] = st_base + 16 * (flip ? 0 : 1 - 2 * h);
+    st_f[0] = (a & 1) ? st_e[1] : st_e[0];  // bit2(b + 2) = !bit2(b) for b % 4 >= 2
+    st_f[1] = (a & 1) ? st_e[0] : st_e[1];
+  }
+  // address of column b of this thread's row, channel block mbi (unpooled)
+  auto st_col = [&](int mbi, int b) -> uint8_t* {
+    if constexpr (kTma && kMode == 1) {
+      const int s = (b >> 2) & 1;
+      return ((b & 3) < 2 ? st_e[s] : st_f[s]) + mbi * 8 + b * 32;
+    } else {
+      return st_base + mbi * 8 + b * kPix;
+    }
   };
+  constexpr int kStoreTid = 192;  // issues (and waits for) the bulk tensor stores: not the MMA warp
 
   if (tid == 0) {
     tma_prefetch_desc(&tm);
@@ -156,6 +218,8 @@ __global__ void __launch_bounds__(kThr, 2)
   constexpr uint32_t kIdP2s = idesc_i8x(128, 32, true, true, true, false);   // s8 MN-major x s8
   uint8_t* A1 = smem + kOffA1;
   uint8_t* A2 = smem + kOffA2;
+  const uint32_t dbase = (smem_u32(smem) >> 4) & 0x3FFF;  // descriptor start-address field of the operand area
+  const uint32_t bar1_addr = smem_u32(&bar[1]), bar2_addr = smem_u32(&bar[2]);
 
   // unit -> (tile p, channel offset k0); kb fastest
   auto unit_p = [&](int64_t u) { return (int)fdiv((uint32_t)u, args.div_kb); };
@@ -176,13 +240,11 @@ __global__ void __launch_bounds__(kThr, 2)
     mbar_wait(&bar[0], ph_tma);
     ph_tma ^= 1;
     tc_fence_after();
-#pragma unroll
-    for (int v = 0; v < 8; ++v) {  // v = res * 4 + gg; residue h feeds warp group h
-      mma_i8_warp(tbase + v * 32, umma_desc_mn_sw32(smem_u32(A1 + v * kOpBytes), 1024),
-                  umma_desc_kmajor(smem_u32(smem + kOffB1 + (v >> 2) * 1024), 32), kIdP1, 0u);
-      if (v == 3) mma_commit_warp(&bar[1]);
-    }
-    mma_commit_warp(&bar[2]);
+    // v = res * 4 + gg; residue h feeds warp group h
+    asm volatile(K4_ASM_HEAD K4_P1(0) K4_P1(1) K4_P1(2) K4_P1(3) K4_COMMIT("%4") K4_P1(4) K4_P1(5) K4_P1(6) K4_P1(7)
+                     K4_COMMIT("%5") "}" ::"r"(tbase),
+                 "r"(dbase), "r"(kIdP1), "r"(kIdP2s), "r"(bar1_addr), "r"(bar2_addr)
+                 : "memory");
   };
   if (warp == 0 && (int64_t)blockIdx.x < args.units) {
     if (lane == 0) issue_load(blockIdx.x);
@@ -271,7 +333,7 @@ __global__ void __launch_bounds__(kThr, 2)
 #endif
     }
     K4T(1)
-    if (kMode != 0 && args.tma_out && tid == 0) bulk_wait_read<0>();  // the previous tile's bulk store has read the staging
+    if (kTma && tid == kStoreTid) bulk_wait_read<0>();  // the previous tile's bulk stores have read the staging
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -280,18 +342,11 @@ __global__ void __launch_bounds__(kThr, 2)
     // ---- pass 2 into the same columns (pass 1 has been read) ----
     if (warp == 0) {
       tc_fence_after();
-#pragma unroll
-      for (int o = 0; o < 8; ++o) {  // channel blocks mb 0, 1 (warps 0-3) first, then mb 2, 3
-        const int v = (o & 2) * 2 + (o >> 2) * 2 + (o & 1);  // v = res * 4 + mb
-        const uint8_t* a2 = A2 + v * 2 * kOpBytes;
-        const uint8_t* b2 = smem + kOffB2 + (v >> 2) * 2 * 1024;
-        mma_i8_warp(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2)), umma_desc_kmajor(smem_u32(b2), 32), kIdP1,
-                    0u);
-        mma_i8_warp(tbase + v * 32, umma_desc_mn_sw128(smem_u32(a2 + kOpBytes)),
-                    umma_desc_kmajor(smem_u32(b2 + 1024), 32), kIdP2s, 1u);
-        if (o == 3) mma_commit_warp(&bar[1]);
-      }
-      mma_commit_warp(&bar[2]);
+      // channel blocks mb 0, 1 of both residues (warps 0-3) first, then mb 2, 3
+      asm volatile(K4_ASM_HEAD K4_P2(0) K4_P2(1) K4_P2(4) K4_P2(5) K4_COMMIT("%4") K4_P2(2) K4_P2(3) K4_P2(6) K4_P2(7)
+                       K4_COMMIT("%5") "}" ::"r"(tbase),
+                   "r"(dbase), "r"(kIdP1), "r"(kIdP2s), "r"(bar1_addr), "r"(bar2_addr)
+                   : "memory");
     }
     K4T(3)
     K4_WAIT(my_bar, ph_mma);
@@ -345,12 +400,12 @@ __global__ void __launch_bounds__(kThr, 2)
           int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
           m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
           m2 = min(m2 >> args.shift, 127);
-          if ((a & 1) == 0 && a < 14) smem[kOffOut + stg_off((a >> 1) * 7 + c, kl)] = (uint8_t)m2;
+          if ((a & 1) == 0 && a < 14) st_base[mbi * 8 + c * kPix] = (uint8_t)m2;
         }
       } else if constexpr (kMode == 1) {
         if (a < 14) {
 #pragma unroll
-          for (int b = 0; b < 14; ++b) smem[kOffOut + stg_off(a * 14 + b, kl)] = (uint8_t)qv[b];
+          for (int b = 0; b < 14; ++b) *st_col(mbi, b) = (uint8_t)qv[b];
         }
       } else {
         int32_t* ys = reinterpret_cast<int32_t*>(smem + out_off(0));
@@ -391,13 +446,13 @@ __global__ void __launch_bounds__(kThr, 2)
             int32_t m2 = max(qv[2 * c], qv[2 * c + 1]);
             m2 = max(m2, __shfl_xor_sync(0xffffffffu, m2, 1));  // rows a, a ^ 1
             m2 = min(m2 >> args.shift, 127);
-            if ((a & 1) == 0 && a < 14) smem[kOffOut + stg_off((a >> 1) * 7 + 4 * hf + c, kl)] = (uint8_t)m2;
+            if ((a & 1) == 0 && a < 14) st_base[mbi * 8 + (4 * hf + c) * kPix] = (uint8_t)m2;
           }
         } else if constexpr (kMode == 1) {
           if (a < 14) {
 #pragma unroll
             for (int e = 0; e < kNb; ++e)
-              if (e < nb) smem[kOffOut + stg_off(a * 14 + 8 * hf + e, kl)] = (uint8_t)qv[e];
+              if (e < nb) *st_col(mbi, 8 * hf + e) = (uint8_t)qv[e];
           }
         } else {
           int32_t* ys = reinterpret_cast<int32_t*>(smem + out_off(0));
@@ -455,7 +510,7 @@ __global__ void __launch_bounds__(kThr, 2)
 #endif
     }
     K4T(5)
-    if (kMode != 0 && args.tma_out) fence_proxy_async();  // staging writes -> visible to the bulk store
+    if (kTma) fence_proxy_async();  // staging writes -> visible to the bulk stores
     tc_fence_before();
     __syncthreads();  // staging complete; pass-2 accumulators read
     K4T(6)
@@ -466,12 +521,12 @@ __global__ void __launch_bounds__(kThr, 2)
     }
 
     // ---- stores ----
-    if (kMode != 0 && args.tma_out) {
+    if constexpr (kTma) {
       // one bulk tensor store of the staged tile (clipped at the image edges
       // and at K); the staging is rewritten only after the next epilogue 1,
-      // by when thread 0 has waited for the read
+      // by when the storing thread has waited for the read
       constexpr int side = kMode == 3 ? 7 : 14;
-      if (tid == 0) {
+      if (tid == kStoreTid) {
         tma_store_4d(&tmo, smem + kOffOut, k0, tj * side, ti * side, b_img);
         bulk_commit();
       }
@@ -528,7 +583,7 @@ __global__ void __launch_bounds__(kThr, 2)
     K4T(7)
   }
 
-  if (kMode != 0 && args.tma_out && tid == 0) bulk_wait<0>();
+  if (kTma && tid == kStoreTid) bulk_wait<0>();
 #ifdef RNSW_K4_PROF
   if (lane == 0 && blockIdx.x < 2 && (warp == 0 || warp == 1 || warp == 4) && pn > 0)
     printf("K4PROF cta %d warp %d units %d per-unit cycles: total %lld | wait_p1 %lld epi1 %lld bar1 %lld p2issue %lld wait_p2 %lld epi2 %lld bar2 %lld stores+p1issue %lld\n",
@@ -598,7 +653,8 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
       cuuint32_t box[4] = {(cuuint32_t)kKB, (cuuint32_t)side, (cuuint32_t)side, 1};
       cuuint32_t es[4] = {1, 1, 1, 1};
       a.tma_out = encode(&tmo, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, out8, dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, pooled ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_32B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS ? 1 : 0;
     }
   }
@@ -623,9 +679,10 @@ cudaError_t launch_output_transform_umma(const PlanHost& plan, const Geometry& g
     const unsigned grid = (unsigned)std::min<int64_t>(a.units, (int64_t)per_sm * num_sms);
     return launch_ex(kern, dim3(grid), dim3(kThr), (size_t)smem, s, 1, (const PlanDevice*)plan.d_plan, tm, tmo, a);
   };
-  if (mode == 0) return launch(output_umma_kernel<0>, smem_bytes(0));
-  if (mode == 1) return launch(output_umma_kernel<1>, smem_bytes(1));
-  return launch(output_umma_kernel<3>, smem_bytes(3));
+  if (mode == 0) return launch(output_umma_kernel<0, false>, smem_bytes(0));
+  if (mode == 1)
+    return a.tma_out ? launch(output_umma_kernel<1, true>, smem_bytes(1)) : launch(output_umma_kernel<1, false>, smem_bytes(1));
+  return a.tma_out ? launch(output_umma_kernel<3, true>, smem_bytes(3)) : launch(output_umma_kernel<3, false>, smem_bytes(3));
 }
 
 }  // namespace rnsw
