@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int warp = threadIdx.x / 32;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);  // warp-uniform for the compiler (role branches, MMA operands in uniform registers)
   const int lane = threadIdx.x % 32;
   const int rank = CS == 2 ? (int)cluster_ctarank() : 0;
   // work units: (kb fastest, pb group of CS tiles, pos, res); this CTA takes

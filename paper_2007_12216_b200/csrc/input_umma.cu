@@ -153,6 +153,56 @@ struct K1UConfig {
       1024 + (size_t)kStages * kStageBytes + kNStg * (size_t)kStgBytes + kBiasBytes + 256;
 };
 
+// One unit's MMAs (16-bit plans, one CTA per group) from ONE asm block: one
+// elect.sync, the two bias MMAs, kKs K-steps x two limbs, both commits; every
+// operand is a base register plus a literal, so the issuing warp spends ~4
+// uniform-datapath instructions per MMA (a separate block per MMA re-elected
+// and moved each descriptor through R2UR: ~10 instructions per 32-cycle MMA).
+// B descriptors: the patch stage / bias tiles, MN-major, 64B swizzle; the
+// start-address field advances by 128 (2 KB) per K-step.
+#define K1_MMA_TS(D, A) "@e tcgen05.mma.cta_group::1.kind::i8 [" D "], [" A "], db, %7, po;\n\t"
+#define K1_KSTEP(KS)                                                         \
+  "add.u32 a, %1, " #KS " * 8;\n\tadd.u32 bl, %3, " #KS " * 128;\n\t"         \
+  "mov.b64 db, {bl, %4};\n\t" K1_MMA_TS("%0", "a")                            \
+  "add.u32 a, %1, 64 + " #KS " * 8;\n\t" K1_MMA_TS("t", "a")
+#define K1_UNIT_HEAD                                                                              \
+  "{\n\t.reg .pred e, pz, po;\n\t.reg .b32 t, a, bl;\n\t.reg .b64 db;\n\t"                          \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 pz, 0, 0;\n\tsetp.eq.b32 po, 0, 0;\n\t"               \
+  "add.u32 t, %0, 64;\n\t"                                                                          \
+  "mov.b64 db, {%5, %4};\n\t@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%2], db, %7, pz;\n\t"       \
+  "mov.b64 db, {%6, %4};\n\t@e tcgen05.mma.cta_group::1.kind::i8 [t], [%2], db, %7, pz;\n\t"
+#define K1_UNIT_TAIL                                                                              \
+  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t"             \
+  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}"
+#define K1_UNIT_ASM(STEPS)                                                                                  \
+  asm volatile(K1_UNIT_HEAD STEPS K1_UNIT_TAIL ::"r"(d0), "r"(ta), "r"(bias_col), "r"(db_lo), "r"(db_hi),  \
+               "r"(dbh_lo), "r"(dbl_lo), "r"(idesc), "r"(bar_empty), "r"(bar_tfull)                        \
+               : "memory")
+#define K1_S1 K1_KSTEP(0)
+#define K1_S2 K1_S1 K1_KSTEP(1)
+#define K1_S3 K1_S2 K1_KSTEP(2)
+#define K1_S4 K1_S3 K1_KSTEP(3)
+#define K1_S5 K1_S4 K1_KSTEP(4)
+#define K1_S6 K1_S5 K1_KSTEP(5)
+#define K1_S7 K1_S6 K1_KSTEP(6)
+#define K1_S8 K1_S7 K1_KSTEP(7)
+// (one instance per K-step count: a jump table in front of the block made the
+// compiler treat the warp as possibly diverged and re-elect per MMA)
+template <int kKs>
+RNSW_DEV void k1_issue_unit16(uint32_t d0, uint32_t ta, uint32_t bias_col, uint32_t db_lo, uint32_t db_hi,
+                              uint32_t dbh_lo, uint32_t dbl_lo, uint32_t idesc, uint32_t bar_empty,
+                              uint32_t bar_tfull) {
+  __syncwarp();  // converged: the compiler then keeps the block's operands in uniform registers
+  if constexpr (kKs == 8) K1_UNIT_ASM(K1_S8);
+  else if constexpr (kKs == 7) K1_UNIT_ASM(K1_S7);
+  else if constexpr (kKs == 6) K1_UNIT_ASM(K1_S6);
+  else if constexpr (kKs == 5) K1_UNIT_ASM(K1_S5);
+  else if constexpr (kKs == 4) K1_UNIT_ASM(K1_S4);
+  else if constexpr (kKs == 3) K1_UNIT_ASM(K1_S3);
+  else if constexpr (kKs == 2) K1_UNIT_ASM(K1_S2);
+  else K1_UNIT_ASM(K1_S1);
+}
+
 // kPair: a 2-CTA cluster serves both 128-position blocks of a residue (N*N >
 // 128): one cta_group::2 MMA of M = 256 per K-step and limb, A = each CTA's
 // block of Kr in its own TMEM, B = the patch split by channels (32 per CTA),
@@ -180,7 +230,9 @@ __global__ void __launch_bounds__(kUThreads, 1)
   uint64_t* sempty = sfull + Cfg::kNStg;   // staging buffer read by its bulk store
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + Cfg::kNStg);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // the warp index through a shuffle: the compiler then treats the role branches (and everything
+  // computed inside them) as warp-uniform and keeps the MMA operands in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0), lane = threadIdx.x % 32;
   const uint32_t crank = kPair ? cluster_ctarank() : 0u;
   const int cid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // cluster (or CTA) id
   const int ncl = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
@@ -389,6 +441,24 @@ __global__ void __launch_bounds__(kUThreads, 1)
 #endif
       const uint32_t d0 = tmem_base + as * Cfg::kAccCols;
       const uint64_t db_stage = db0 + (uint64_t)(stage * kStageStep);
+#if !defined(RNSW_K1_PROF) && !RNSW_K1_EPI_BIAS && !RNSW_K1_ONE_MMA && !defined(RNSW_K1_OLD_ISSUE)
+      if constexpr (kLimbs == 2 && !kPair) {
+        if (ksteps == 8 || ksteps == 4) {  // N*N = 256 (F(14,3), the VGG16 plan) / 128-position blocks of N = 12
+          if (ksteps == 8)
+            k1_issue_unit16<8>(d0, ta, tmem_base + Cfg::kBiasCol, (uint32_t)db_stage, (uint32_t)(db0 >> 32),
+                               (uint32_t)dbh, (uint32_t)dbl, idesc, smem_u32(&empty[stage]), smem_u32(&tfull[as]));
+          else
+            k1_issue_unit16<4>(d0, ta, tmem_base + Cfg::kBiasCol, (uint32_t)db_stage, (uint32_t)(db0 >> 32),
+                               (uint32_t)dbh, (uint32_t)dbl, idesc, smem_u32(&empty[stage]), smem_u32(&tfull[as]));
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+          ++it;
+          continue;
+        }
+      }
+#endif
       if (kLimbs == 2 && !RNSW_K1_EPI_BIAS) {  // the bias: D_hi = 127 S1, D_lo = 127 S2 (overwrites the buffer)
         mma_ts(d0, tmem_base + Cfg::kBiasCol, dbh, idesc, 0u);
         mma_ts(d0 + kUnitN, tmem_base + Cfg::kBiasCol, dbl, idesc, 0u);

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kKThreads, 1)
   // only after its own yfull for it + 1 completed, i.e. after this CTA
   // pushed it + 1, which every thread does after reading ybuf[b] for it.
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0), lane = threadIdx.x % 32;  // warp-uniform for the compiler
   const int rank = (int)cluster_ctarank();  // = residue
   const int partner = rank ^ 1;
   const int cid = (int)(blockIdx.x >> 1), ncl = (int)(gridDim.x >> 1);
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kKThreads, 1)
   uint64_t* sempty = sfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + 2);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x / 32, 0), lane = threadIdx.x % 32;  // warp-uniform for the compiler
   const int rb = (int)(blockIdx.x % args.npb);
   const int u_begin = (int)(blockIdx.x / args.npb), u_step = (int)(gridDim.x / args.npb);
   const Geometry& g = args.g;

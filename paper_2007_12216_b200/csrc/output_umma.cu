@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThr, 2)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffOut + ((out_bytes(kMode) + 15) & ~15));
   uint64_t* bar_tfree = bar + 3;  // RNSW_K4_EARLY_P1: every warp has read its pass-2 accumulators
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // warp-uniform for the compiler
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
   pdl_trigger();
