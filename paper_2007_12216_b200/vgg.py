@@ -89,9 +89,11 @@ class VGG16Rns:
                 "name": name,
                 "input_transform_bytes": batch * side * side * c + planes * npos * tiles * c,
                 "gemm_ops": 2 * tiles * npos * c * k * mma_per_product,
-                # V in, the filter bank once, the Winograd-domain product out
-                "gemm_bytes": planes * npos * tiles * c + sum(1 if m < 256 else 4 for m in self.cfg.moduli)
-                * npos * k * c + len(self.cfg.moduli) * npos * tiles * k * 2,
+                # V in, the filter residues once (one byte per 8-bit modulus, two per
+                # 16-bit one: the tile-row GEMM also streams the two derived 256 u mod m
+                # planes, the small-P GEMM does not), the Winograd-domain product out
+                "gemm_bytes": planes * npos * tiles * c + planes * npos * k * c
+                + len(self.cfg.moduli) * npos * tiles * k * 2,
                 "output_transform_bytes": len(self.cfg.moduli) * npos * tiles * k * 2 + (
                     batch * oside * oside * k if fused else batch * side * side * k * 4),
                 "glue_bytes": batch * side * side * k * 4 + batch * oside * oside * k,
