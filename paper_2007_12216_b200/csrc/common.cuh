@@ -420,6 +420,18 @@ RNSW_DEV void mma_i8_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint
       "}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// ... warp-collective (one elected lane; operands stay in uniform registers)
+RNSW_DEV void mma_i8_warp_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
 // one issuing thread: commit the pair's prior MMAs to the mbarrier at this offset in both CTAs
 RNSW_DEV void mma_commit_2sm(uint64_t* bar) {
   asm volatile(
@@ -510,6 +522,15 @@ RNSW_DEV void mma_commit_warp(uint64_t* bar) {
 RNSW_DEV void mma_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+RNSW_DEV void mma_commit_warp_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
           smem_u32(bar)),
       "h"(mask)
       : "memory");

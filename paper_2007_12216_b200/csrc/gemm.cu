@@ -586,8 +586,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && (!CG2 || rank == 0)) {
-      // ---------------- MMA issuer ----------------
+    if (!CG2 || rank == 0) {
+      // ---------------- MMA issuer (warp-collective: every lane runs the loop, one elected lane
+      // issues; the operands are warp-uniform and stay in uniform registers) ----------------
       constexpr uint32_t idesc = idesc_i8(kBlockM, BN);
       constexpr uint32_t idesc2 = idesc_i8(CG2 ? 2 * kBlockM : kBlockM, 2 * BN);  // 16-bit: [A256 | A1] in one MMA
       int stage = 0;
@@ -638,13 +639,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
               const uint64_t db_p = umma_desc_kmajor(b0 + 32 * k, BC);                      // u'_hi | u'_lo half
               const uint64_t db_u = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);  // u_hi | u_lo half
-              mma_i8_2sm(d0, da_hi, db_p, idesc2, acc);
-              mma_i8_2sm(d0, da_lo, db_u, idesc2, 1u);
+              mma_i8_warp_2sm(d0, da_hi, db_p, idesc2, acc);
+              mma_i8_warp_2sm(d0, da_lo, db_u, idesc2, 1u);
             }
           } else if (MAXPL == 1 || pl == 1) {
 #pragma unroll
             for (int k = 0; k < BC / 32; ++k)
-              mma_i8(d0, umma_desc_kmajor(a0 + 32 * k, BC), umma_desc_kmajor(b0 + 32 * k, BC), idesc,
+              mma_i8_warp(d0, umma_desc_kmajor(a0 + 32 * k, BC), umma_desc_kmajor(b0 + 32 * k, BC), idesc,
                      (kc | k) != 0);
           } else if (MAXPL == 3) {
 #pragma unroll
@@ -655,10 +656,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
               const uint64_t db_hi = umma_desc_kmajor(b0 + 32 * k, BC);                      // slot 0: u_hi
               const uint64_t db_ul = umma_desc_kmajor(b0 + Cfg::kBPlaneBytes + 32 * k, BC);   // slot 1: u_lo
-              mma_i8(d0, da_hi, db_hi, idesc, acc);
-              mma_i8(d0 + BN, da_hi, db_ul, idesc, acc);
-              mma_i8(d0 + BN, da_lo, db_hi, idesc, 1u);
-              mma_i8(d0 + 2 * BN, da_lo, db_ul, idesc, acc);
+              mma_i8_warp(d0, da_hi, db_hi, idesc, acc);
+              mma_i8_warp(d0 + BN, da_hi, db_ul, idesc, acc);
+              mma_i8_warp(d0 + BN, da_lo, db_hi, idesc, 1u);
+              mma_i8_warp(d0 + 2 * BN, da_lo, db_ul, idesc, acc);
             }
           } else {
 #pragma unroll
@@ -670,16 +671,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t da_hi = umma_desc_kmajor(a0 + Cfg::kAPlaneBytes + 32 * k, BC);
               const uint64_t db_p = umma_desc_kmajor(b0 + 32 * k, BC);                         // [u'_hi ; u'_lo]
               const uint64_t db_u = umma_desc_kmajor(b0 + 2 * Cfg::kBPlaneBytes + 32 * k, BC);  // [u_hi ; u_lo]
-              mma_i8(d0, da_hi, db_p, idesc2, acc);
-              mma_i8(d0, da_lo, db_u, idesc2, 1u);
+              mma_i8_warp(d0, da_hi, db_p, idesc2, acc);
+              mma_i8_warp(d0, da_lo, db_u, idesc2, 1u);
             }
           }
           if (CG2)
-            mma_commit_2sm(&empty[stage]);
+            mma_commit_warp_2sm(&empty[stage]);
           else if (MC == 2)
-            mma_commit_mc(&empty[stage], (uint16_t)0x3);
+            mma_commit_warp_mc(&empty[stage], (uint16_t)0x3);
           else
-            mma_commit(&empty[stage]);
+            mma_commit_warp(&empty[stage]);
 #ifdef RNSW_GEMM_PROF
           g_is += clock64() - g3;
 #endif
@@ -692,18 +693,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         long long g4 = clock64();
 #endif
         if (CG2)
-          mma_commit_2sm(&tfull[as]);
+          mma_commit_warp_2sm(&tfull[as]);
         else
-          mma_commit(&tfull[as]);
+          mma_commit_warp(&tfull[as]);
 #ifdef RNSW_GEMM_PROF
         g_cm += clock64() - g4;
 #endif
       }
 #ifdef RNSW_GEMM_PROF
-      if (blockIdx.x < 2 && it > 0) printf("GEMMPROF2 cta %d tile_coord %lld commit %lld\n", blockIdx.x, g_tc, g_cm);
+      if (lane == 0 && blockIdx.x < 2 && it > 0) printf("GEMMPROF2 cta %d tile_coord %lld commit %lld\n", blockIdx.x, g_tc, g_cm);
 #endif
 #ifdef RNSW_GEMM_PROF
-      if (blockIdx.x < 2 && it > 0)
+      if (lane == 0 && blockIdx.x < 2 && it > 0)
         printf("GEMMPROF cta %d BN %d BC %d tiles %d mmas %lld total %lld wait_tempty %lld wait_full %lld issue %lld (cyc/mma %.1f)\n",
                blockIdx.x, BN, BC, it, g_mma, clock64() - g_0, g_te, g_f, g_is, (double)(clock64() - g_0) / g_mma);
 #endif
