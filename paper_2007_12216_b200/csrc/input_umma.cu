@@ -865,7 +865,11 @@ cudaError_t launch_input_transform_umma(const PlanHost& plan, const Geometry& g,
     if (a.pair128) {
       // tile pairs as 128-byte rows: (2 Cp, P / 2, npos, planes)
       cuuint64_t dims2[4] = {(cuuint64_t)(2 * g.Cp), (cuuint64_t)(g.P / 2), (cuuint64_t)npos, (cuuint64_t)d.n_planes};
+#if RNSW_K1_DIAG == 4
+      cuuint64_t strides2[3] = {(cuuint64_t)(2 * g.Cp) * npos, (cuuint64_t)(2 * g.Cp), (cuuint64_t)g.P * g.Cp * npos};
+#else
       cuuint64_t strides2[3] = {(cuuint64_t)(2 * g.Cp), (cuuint64_t)g.P * g.Cp, (cuuint64_t)g.P * g.Cp * npos};
+#endif
       cuuint32_t boxp[4] = {(cuuint32_t)(2 * kUnitN), 1, (cuuint32_t)kGroupRows, 1};
       if (encode(&tmV, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, V, dims2, strides2, boxp, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                  RNSW_K1_STG_SWZ ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
