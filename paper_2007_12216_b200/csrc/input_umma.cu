@@ -298,10 +298,20 @@ __global__ void __launch_bounds__(kUThreads, 1)
     if (hh < kLimbs) {
       const uint4* src = reinterpret_cast<const uint4*>(kr + (size_t)kr_group * args.group_bytes +
                                                         ((size_t)hh * kGroupRows + row) * args.kp);
-      for (int c8 = 0; c8 < args.kp / 32; ++c8) {  // 8 columns = 32 K bytes per store
-        const uint4 w0 = __ldg(src + 2 * c8), w1 = __ldg(src + 2 * c8 + 1);
-        const uint32_t v[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        tmem_st8(trow + Cfg::kACol + hh * 64 + c8 * 8, v);
+      // 8 columns = 32 K bytes per store; four stores' loads in flight together
+      // (one dependent load per store made this prologue ~8 L2 latencies long)
+      const int n8 = args.kp / 32;
+      for (int c8 = 0; c8 < n8; c8 += 4) {
+        uint4 w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) w[e] = c8 + (e >> 1) < n8 ? __ldg(src + 2 * c8 + e) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (c8 + e >= n8) break;
+          const uint32_t v[8] = {w[2 * e].x, w[2 * e].y, w[2 * e].z, w[2 * e].w,
+                                 w[2 * e + 1].x, w[2 * e + 1].y, w[2 * e + 1].z, w[2 * e + 1].w};
+          tmem_st8(trow + Cfg::kACol + hh * 64 + (c8 + e) * 8, v);
+        }
       }
     }
     if (kLimbs == 2 && hh == 0) {
