@@ -54,6 +54,13 @@ namespace {
 #ifndef RNSW_K4_SLEEP
 #define RNSW_K4_SLEEP 0
 #endif
+// 1: every pair of pass-1 MMAs (one column group of both residues) and every
+// channel block of pass 2 commits to its own mbarrier, so an epilogue starts on
+// the first block while the rest of the batch still runs (0: two commits per
+// batch, one per warp group)
+#ifndef RNSW_K4_FINE
+#define RNSW_K4_FINE 1
+#endif
 #if RNSW_K4_SLEEP
 #define K4_WAIT(b, ph) mbar_wait_sleep(b, ph, RNSW_K4_SLEEP)
 #else
@@ -85,7 +92,7 @@ constexpr int kPixW = 33;   // staged words per pixel (int32 mode)
 // fit per SM like in the int8 modes (a separate 26 KB staging tile allowed one).
 constexpr int out_bytes(int mode) { return mode == 0 ? 0 : (mode == 1 ? 196 * kPixB : 49 * kPixB); }
 constexpr int out_off(int mode) { return mode == 0 ? kOffA1 : kOffOut; }
-constexpr int smem_bytes(int mode) { return 1024 + kOffOut + ((out_bytes(mode) + 15) & ~15) + 64; }
+constexpr int smem_bytes(int mode) { return 1024 + kOffOut + ((out_bytes(mode) + 15) & ~15) + 128; }
 static_assert(196 * kPixW * 4 <= 8 * kOpBytes, "the int32 tile must fit the A1 region");
 
 // The MMA batches of a pass are issued from ONE asm block: one elect.sync,
@@ -109,6 +116,7 @@ static_assert(K4_OFF_A1 == kOffA1 && K4_OFF_A2 == kOffA2 && K4_OFF_B1 == kOffB1 
   "mov.b64 db, {bl, 0xC0004010};\n\t"                                           \
   "@e tcgen05.mma.cta_group::1.kind::i8 [t], da, db, " ID ", " ACCP ";\n\t"
 #define K4_COMMIT(BAR) "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [" BAR "];\n\t"
+#define K4_COMMIT_AT(BASE, I) "add.u32 ba, " BASE ", " #I " * 8;\n\t" K4_COMMIT("ba")
 // pass 1, v = res * 4 + gg: A1 + v * 4 KB (MN-major, 32B swizzle, LBO 1 KB), B1 + res * 1 KB
 #define K4_P1(V) K4_MMA((V) * 32, K4_OFF_A1 + (V) * 4096, 64, 0xC0004010, K4_OFF_B1 + ((V) >> 2) * 1024, "%2", "pz")
 // pass 2, v = res * 4 + mb: A2 + v * 8 KB (MN-major, 128B swizzle; step 1 at + 4 KB), B2 + res * 2 KB (+ 1 KB)
@@ -116,7 +124,7 @@ static_assert(K4_OFF_A1 == kOffA1 && K4_OFF_A2 == kOffA2 && K4_OFF_B1 == kOffB1 
   K4_MMA((V) * 32, K4_OFF_A2 + (V) * 8192, 1, 0x40004040, K4_OFF_B2 + ((V) >> 2) * 2048, "%2", "pz")           \
   K4_MMA((V) * 32, K4_OFF_A2 + (V) * 8192 + 4096, 1, 0x40004040, K4_OFF_B2 + ((V) >> 2) * 2048 + 1024, "%3", "po")
 #define K4_ASM_HEAD                                                                                   \
-  "{\n\t.reg .pred e, pz, po;\n\t.reg .b32 t, al, bl;\n\t.reg .b64 da, db;\n\t"                        \
+  "{\n\t.reg .pred e, pz, po;\n\t.reg .b32 t, al, bl, ba;\n\t.reg .b64 da, db;\n\t"                        \
   "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 pz, 0, 0;\n\tsetp.eq.b32 po, 0, 0;\n\t"
 
 struct UArgs {
@@ -149,7 +157,9 @@ __global__ void __launch_bounds__(kThr, 2)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffOut + ((out_bytes(kMode) + 15) & ~15));
   uint64_t* bar_tfree = bar + 3;  // RNSW_K4_EARLY_P1: every warp has read its pass-2 accumulators
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint64_t* bar_p1 = bar + 4;     // RNSW_K4_FINE: pass 1, column group gg of both residues complete
+  uint64_t* bar_p2 = bar + 8;     // RNSW_K4_FINE: pass 2, channel block mbi of warp group h complete (index 2 mbi + h)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 12);
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // warp-uniform for the compiler
   const int q = warp & 3, h = warp >> 2;
   const Geometry& g = args.g;
@@ -189,6 +199,10 @@ __global__ void __launch_bounds__(kThr, 2)
     mbar_init(&bar[1], 1);  // MMA batch for warps 0-3 complete
     mbar_init(&bar[2], 1);  // MMA batch for warps 4-7 complete (implies bar[1]: commits track all prior MMAs)
     mbar_init(bar_tfree, kThr / 32);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&bar_p1[i], 1);
+      mbar_init(&bar_p2[i], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<256>(tslot);
@@ -219,7 +233,8 @@ __global__ void __launch_bounds__(kThr, 2)
   uint8_t* A1 = smem + kOffA1;
   uint8_t* A2 = smem + kOffA2;
   const uint32_t dbase = (smem_u32(smem) >> 4) & 0x3FFF;  // descriptor start-address field of the operand area
-  const uint32_t bar1_addr = smem_u32(&bar[1]), bar2_addr = smem_u32(&bar[2]);
+  const uint32_t bar1_addr = smem_u32(RNSW_K4_FINE ? &bar_p1[0] : &bar[1]);
+  const uint32_t bar2_addr = smem_u32(RNSW_K4_FINE ? &bar_p2[0] : &bar[2]);
 
   // unit -> (tile p, channel offset k0); kb fastest
   auto unit_p = [&](int64_t u) { return (int)fdiv((uint32_t)u, args.div_kb); };
@@ -234,17 +249,26 @@ __global__ void __launch_bounds__(kThr, 2)
   const int64_t u_step = gridDim.x;
   // each MMA batch is committed in two halves, one per warp group (h), so the
   // first group starts its epilogue while the second half still runs
-  uint32_t ph_tma = 0, ph_mma = 0, ph_tfree = 0;
+  uint32_t ph_tma = 0, ph_mma = 0, ph_tfree = 0, ph1 = 0, ph2 = 0;
   uint64_t* my_bar = &bar[1 + h];
+  (void)ph_mma;
+  (void)my_bar;
   auto issue_p1 = [&]() {  // warp 0: pass 1 into the 256 TMEM columns once the boxes landed
     mbar_wait(&bar[0], ph_tma);
     ph_tma ^= 1;
     tc_fence_after();
     // v = res * 4 + gg; residue h feeds warp group h
+#if RNSW_K4_FINE
+    asm volatile(K4_ASM_HEAD K4_P1(0) K4_P1(4) K4_COMMIT_AT("%4", 0) K4_P1(1) K4_P1(5) K4_COMMIT_AT("%4", 1) K4_P1(2)
+                     K4_P1(6) K4_COMMIT_AT("%4", 2) K4_P1(3) K4_P1(7) K4_COMMIT_AT("%4", 3) "}" ::"r"(tbase),
+                 "r"(dbase), "r"(kIdP1), "r"(kIdP2s), "r"(bar1_addr), "r"(bar2_addr)
+                 : "memory");
+#else
     asm volatile(K4_ASM_HEAD K4_P1(0) K4_P1(1) K4_P1(2) K4_P1(3) K4_COMMIT("%4") K4_P1(4) K4_P1(5) K4_P1(6) K4_P1(7)
                      K4_COMMIT("%5") "}" ::"r"(tbase),
                  "r"(dbase), "r"(kIdP1), "r"(kIdP2s), "r"(bar1_addr), "r"(bar2_addr)
                  : "memory");
+#endif
   };
   if (warp == 0 && (int64_t)blockIdx.x < args.units) {
     if (lane == 0) issue_load(blockIdx.x);
@@ -266,12 +290,25 @@ __global__ void __launch_bounds__(kThr, 2)
 #endif
     const int p = unit_p(u), k0 = (int)(u - (int64_t)p * args.kblocks) * kKB;
     // ---- pass 1 (issued before the previous unit's stores) ----
+#if RNSW_K4_FINE
+    // column group gg of this unit's pass 1 (both residues) has completed
+    auto wait_p1 = [&](int gg) {
+      K4_WAIT(&bar_p1[gg], ph1);
+      tc_fence_after();
+      // the last group's barrier means all of pass 1 is done: A1 is free
+      if (gg == 3 && kMode != 0 && tid == kThr / 2 && u + u_step < args.units) issue_load(u + u_step);  // lands during the epilogues
+    };
+    wait_p1(0);
+    K4T(0)
+#else
+    auto wait_p1 = [&](int) {};
     K4_WAIT(my_bar, ph_mma);
     K4T(0)
     ph_mma ^= 1;
     tc_fence_after();
     // the second group's barrier means all of pass 1 is done: A1 is free
     if (kMode != 0 && tid == kThr / 2 && u + u_step < args.units) issue_load(u + u_step);  // lands during the epilogues
+#endif
 
     // ---- epilogue 1: warp (q, h): columns j = 4 gg + q of residue h, lane = channel ----
     {
@@ -312,25 +349,30 @@ __global__ void __launch_bounds__(kThr, 2)
 #pragma unroll
         for (int gg = 0; gg < 4; ++gg) body(gg, hv[gg], lv[gg]);
       }
+      static_assert(!RNSW_K4_FINE, "RNSW_K4_EPI1_ALLLD needs RNSW_K4_FINE=0");
 #else
       int32_t hA[16], lA[16], hB[16], lB[16];
       tmem_ld16(ta, hA);
       tmem_ld16(ta + 16, lA);
       tmem_ld_wait();
+      wait_p1(1);
       tmem_ld16(ta + 32, hB);
       tmem_ld16(ta + 48, lB);
       body(0, hA, lA);
       tmem_ld_wait();
+      wait_p1(2);
       tmem_ld16(ta + 64, hA);
       tmem_ld16(ta + 80, lA);
       body(1, hB, lB);
       tmem_ld_wait();
+      wait_p1(3);
       tmem_ld16(ta + 96, hB);
       tmem_ld16(ta + 112, lB);
       body(2, hA, lA);
       tmem_ld_wait();
       body(3, hB, lB);
 #endif
+      ph1 ^= 1;
     }
     K4T(1)
     if (kTma && tid == kStoreTid) bulk_wait_read<0>();  // the previous tile's bulk stores have read the staging
@@ -342,16 +384,35 @@ __global__ void __launch_bounds__(kThr, 2)
     // ---- pass 2 into the same columns (pass 1 has been read) ----
     if (warp == 0) {
       tc_fence_after();
+#if RNSW_K4_FINE
+      // each warp group's first channel block (both residues) first, then the second blocks
+      asm volatile(K4_ASM_HEAD K4_P2(0) K4_P2(4) K4_COMMIT_AT("%5", 0) K4_P2(2) K4_P2(6) K4_COMMIT_AT("%5", 1) K4_P2(1)
+                       K4_P2(5) K4_COMMIT_AT("%5", 2) K4_P2(3) K4_P2(7) K4_COMMIT_AT("%5", 3) "}" ::"r"(tbase),
+                   "r"(dbase), "r"(kIdP1), "r"(kIdP2s), "r"(bar1_addr), "r"(bar2_addr)
+                   : "memory");
+#else
       // channel blocks mb 0, 1 of both residues (warps 0-3) first, then mb 2, 3
       asm volatile(K4_ASM_HEAD K4_P2(0) K4_P2(1) K4_P2(4) K4_P2(5) K4_COMMIT("%4") K4_P2(2) K4_P2(3) K4_P2(6) K4_P2(7)
                        K4_COMMIT("%5") "}" ::"r"(tbase),
                    "r"(dbase), "r"(kIdP1), "r"(kIdP2s), "r"(bar1_addr), "r"(bar2_addr)
                    : "memory");
+#endif
     }
     K4T(3)
+#if RNSW_K4_FINE
+    // channel block mbi of this warp group (both residues) has completed
+    auto wait_p2 = [&](int mbi) {
+      K4_WAIT(&bar_p2[2 * mbi + h], ph2);
+      tc_fence_after();
+    };
+    wait_p2(0);
+    if (!RNSW_K4_EPI2_PIPE) wait_p2(1);
+#else
+    auto wait_p2 = [&](int) {};
     K4_WAIT(my_bar, ph_mma);
     ph_mma ^= 1;
     tc_fence_after();
+#endif
     K4T(4)
 
     // ---- epilogue 2: lane row (k, a) = (2q + lane/16, lane % 16) of channel blocks mb = 2h, 2h+1 ----
@@ -476,6 +537,7 @@ __global__ void __launch_bounds__(kThr, 2)
       load(0, 1, bH0, bL0, bH1, bL1);
       emit(0, 0, aH0, aL0, aH1, aL1);
       tmem_ld_wait();
+      wait_p2(1);
       load(1, 0, aH0, aL0, aH1, aL1);
       emit(0, 1, bH0, bL0, bH1, bL1);
       tmem_ld_wait();
@@ -509,6 +571,7 @@ __global__ void __launch_bounds__(kThr, 2)
       }
 #endif
     }
+    ph2 ^= 1;
     K4T(5)
     if (kTma) fence_proxy_async();  // staging writes -> visible to the bulk stores
     tc_fence_before();
