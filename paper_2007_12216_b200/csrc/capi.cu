@@ -20,9 +20,10 @@ struct rnsw_plan {
 // Programmatic dependent launch for the layer kernels (declared in
 // common.cuh) when the layer is small: its kernels are short and launch /
 // prologue latency matters (VGG16 batch 1: -8%, batch 32: -1.6%); at batch
-// 256 it measured +4.5%.  The layer entry points record the tile count
+// 256 it measured +3 to +4.5% when the 65536-tile layers take part and
+// -0.4% up to 16384 tiles.  The layer entry points record the tile count
 // (pdl_layer_hint); RNSW_PDL=0 disables it, RNSW_PDL=N sets the tile limit
-// (default 8192).
+// (default 16384).
 namespace {
 thread_local int64_t g_pdl_tiles = 0;
 }
@@ -32,7 +33,7 @@ void pdl_layer_hint(int64_t P) { g_pdl_tiles = P; }
 bool pdl_enabled() {
   static const int64_t max_tiles = [] {
     const char* e = getenv("RNSW_PDL");
-    return e == nullptr ? (int64_t)8192 : (int64_t)atoll(e) * (atoll(e) == 1 ? 8192 : 1);
+    return e == nullptr ? (int64_t)16384 : (int64_t)atoll(e) * (atoll(e) == 1 ? 16384 : 1);
   }();
   return g_pdl_tiles > 0 && g_pdl_tiles <= max_tiles;
 }
