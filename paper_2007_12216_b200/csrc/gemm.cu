@@ -979,7 +979,7 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   // (3 stages of 64 KB: conv4_2 -6%, conv5 -2%); C = 256 is faster with
   // 64-byte chunks (6 stages; +10% with 128)
   static const char* cg2_env0 = getenv("RNSW_GEMM_CG2");
-  const bool cg2_planned = (cg2_env0 != nullptr ? atoi(cg2_env0) != 0 : Cp >= 256) && (P + kBlockM - 1) / kBlockM >= 2 &&
+  const bool cg2_planned = (cg2_env0 != nullptr ? atoi(cg2_env0) != 0 : Cp >= 128) && (P + kBlockM - 1) / kBlockM >= 2 &&
                            getenv("RNSW_GEMM_NO_MC") == nullptr;
   const bool cg2_bc128 = cg2_planned && Cp >= 512 && Cp % 128 == 0;
   if (maxpl == 2 && bc > 64 && !cg2_bc128) {
@@ -998,11 +998,12 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   for (int r = 0; r < d.n_res; ++r) all16 = all16 && d.res[r].planes == 2;
   static const bool no_mc = getenv("RNSW_GEMM_NO_MC") != nullptr;  // A/B switch
   // CTA pairs as cta_group::2 MMAs of M = 256 (each CTA stages half of the
-  // filter planes) for C >= 256, where the operand stream bounds the GEMM
-  // (VGG16 conv4_2: -15%, conv3_2: -5%); multicast pairs for smaller C
-  // (+3% on conv2_x).  RNSW_GEMM_CG2=0/1 forces either.
+  // filter planes) for C >= 128, where the operand stream bounds the GEMM
+  // (VGG16 conv4_2: -15%, conv3_2: -5%; since the warp-collective issue also
+  // conv3_1: -15%, conv2_2: -7%); multicast pairs for C = 64 (cta_group::2:
+  // +6% on conv1_2).  RNSW_GEMM_CG2=0/1 forces either.
   static const char* cg2_env = getenv("RNSW_GEMM_CG2");
-  const bool cg2 = cg2_env != nullptr ? atoi(cg2_env) != 0 : Cp >= 256;
+  const bool cg2 = cg2_env != nullptr ? atoi(cg2_env) != 0 : Cp >= 128;
   // RNSW_GEMM_U2=1: the two-plane-bank variant (MAXPL 3) for every 16-bit
   // layer, =2: where the bank stream dominates (4 K C >= 2 P C + 4 P K).  Off
   // by default: on B200 it measured slower even at batch 1 (0.83 vs 0.63 ms
