@@ -981,7 +981,8 @@ cudaError_t launch_winograd_gemm(const PlanHost& plan, const int8_t* V, const in
   static const char* cg2_env0 = getenv("RNSW_GEMM_CG2");
   const bool cg2_planned = (cg2_env0 != nullptr ? atoi(cg2_env0) != 0 : Cp >= 128) && (P + kBlockM - 1) / kBlockM >= 2 &&
                            getenv("RNSW_GEMM_NO_MC") == nullptr;
-  const bool cg2_bc128 = cg2_planned && Cp >= 512 && Cp % 128 == 0;
+  static const int bc128_min = getenv("RNSW_GEMM_BC128_MIN") ? atoi(getenv("RNSW_GEMM_BC128_MIN")) : 512;  // A/B switch
+  const bool cg2_bc128 = cg2_planned && Cp >= bc128_min && Cp % 128 == 0;
   if (maxpl == 2 && bc > 64 && !cg2_bc128) {
     bc = 64;
     a.nkc = Cp / bc;
