@@ -24,8 +24,11 @@
 //           add a multiple of m as the reduction bias; D2 = [A256 | A1] per
 //           b.  y = 256 A256 + A1 reduces once to the mixed-radix digit.
 //
-// Per unit: 8 TMA boxes, 8 + 16 MMAs, two TMEM round trips; the next unit's
-// boxes load during this unit's epilogues.
+// Per unit: 2 TMA boxes (one per residue), 8 + 16 MMAs issued from one asm
+// block per pass, two TMEM round trips; every column group of pass 1 and every
+// channel block of pass 2 commits to its own mbarrier, so each epilogue starts
+// on the first block while the rest of the batch runs; the next unit's boxes
+// load during this unit's epilogues.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
